@@ -1,0 +1,147 @@
+/*
+ * gfs.h — C ABI of libgfs.so, the B200-native GPUfs-style sequential-read layer.
+ *
+ * Drop-in boundary for the reference's sequential gread path
+ * (/root/reference/pkg/src/gpuiosim).  The reference is a Python package;
+ * its outer API is Simulation(cfg, seed).run() -> MetricsReport
+ * (simulation.py:98-242) and its inner contract is ThreadBlock._gread
+ * (gpu_exec.py:107-129) over GpuPageCache (gpu_cache.py:92-212), the private
+ * prefetch buffer (prefetcher.py:13-68), RpcQueue.submit/release
+ * (rpc.py:82-113) and HostOs.pread (host_os.py:221).  Each entry point below
+ * names the reference interface it replaces.  Plain pointers and sizes only:
+ * no torch types cross this boundary (device buffers are raw CUDA pointers).
+ *
+ * Errors: every int-returning call returns 0 on success and a negative
+ * GFS_E* code on failure; gfs_last_error() gives the thread's message.  The
+ * Python layer maps them to GfsError (== the reference's SimError,
+ * simcore.py:13).
+ */
+#ifndef GFS_H
+#define GFS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GFS_ABI_VERSION 1
+
+enum { GFS_OK = 0, GFS_EINVAL = -1, GFS_ECUDA = -2, GFS_EIO = -3, GFS_ENOMEM = -4,
+       GFS_ETIMEDOUT = -5, GFS_EDEVICE = -6, GFS_ESTATE = -7 };
+
+/* gpufs.policy (gpu_cache.py:27-29) */
+enum { GFS_POLICY_GLOBAL_LRU = 0, GFS_POLICY_PER_TB_LRA = 1 };
+/* io.readahead: static = the reference span page+prefetch (prefetcher.py:13-25);
+ * adaptive = window doubling on sequential continuation up to ra_max_bytes */
+enum { GFS_RA_STATIC = 0, GFS_RA_ADAPTIVE = 1 };
+/* io.transfer: zerocopy = SMs pull the span from mapped pinned staging;
+ * dma = daemon cudaMemcpyAsync's staging -> HBM landing, doorbell after it */
+enum { GFS_XFER_ZEROCOPY = 0, GFS_XFER_DMA = 1 };
+/* gopen flags: read-only files are the only ones prefetched (prefetcher.py:22-24) */
+enum { GFS_O_RDONLY = 0, GFS_O_RDWR = 2 };
+/* log kinds (deterministic mode) */
+enum { GFS_LOG_DELIVERIES = 0, GFS_LOG_RPCS = 1, GFS_LOG_VICTIMS = 2, GFS_LOG_WINDOWS = 3 };
+
+typedef struct gfs_config {
+  int64_t page_size;       /* gpufs.page_size (multiple of 4096) */
+  int64_t cache_bytes;     /* gpufs.cache_bytes: frame pool in HBM */
+  int64_t prefetch_bytes;  /* gpufs.prefetch_bytes */
+  int64_t staging_bytes;   /* rpc.staging_bytes: PCIe batch size (accounting, rpc.py:31-55) */
+  int64_t ra_max_bytes;    /* io.ra_max_bytes: adaptive window cap */
+  int64_t max_request_bytes; /* largest gread request (raw mode sizes staging to it) */
+  int32_t policy;          /* GFS_POLICY_* */
+  int32_t resident_limit;  /* reference residency (gpu_exec.py:44-50): sets the LRA quota */
+  int32_t readahead;       /* GFS_RA_* */
+  int32_t transfer;        /* GFS_XFER_* */
+  int32_t io_workers;      /* host daemon threads */
+  int32_t io_direct;       /* O_DIRECT preads (aligned requests) */
+  int32_t device;          /* CUDA ordinal */
+  int32_t cta_threads;     /* threads per resident CTA (one CTA = one active TB) */
+  int32_t max_ctas;        /* cap on resident CTAs (0 = min(resident_limit, occupancy)) */
+  int32_t raw_mode;        /* mode.gpu_cache_disabled (gpu_exec.py:114-119) */
+  int32_t pcie_disabled;   /* mode.pcie_disabled: accounting only */
+  int32_t log;             /* record delivery / RPC / victim logs on the device */
+  int32_t verify;          /* check every fetched word against the synthetic law */
+  int32_t reserved[3];
+} gfs_config;
+
+/* One gread program set (workloads.py:24-31 programs, flattened).
+ * TB t reads segments segs[prog_off[t] .. prog_off[t+1]) in order, request_bytes
+ * at a time (gpu_exec.py:95-105); its bytes land at dst + dst_off[t] + (position
+ * within its program).  order[] is the activation order (gpu_exec.py:242-265). */
+typedef struct gfs_program {
+  int32_t n_tb;
+  int32_t reserved;
+  int64_t request_bytes;
+  const int64_t* segs;     /* [n_segs][3]: file id, offset, length */
+  const int64_t* prog_off; /* [n_tb + 1] */
+  const int64_t* dst_off;  /* [n_tb] */
+  const int32_t* order;    /* [n_tb] */
+} gfs_program;
+
+/* Counters: names follow gpuiosim.metrics.Metrics (metrics.py:12-46) + timing. */
+#define GFS_STAT_FIELDS(X)                                                                    \
+  X(greads) X(user_bytes) X(cache_hit_user_bytes) X(tag_mismatches) X(pc_lookups) X(pc_hits) \
+  X(pc_hit_pending) X(pc_misses) X(pc_allocs) X(pc_evictions) X(pc_remaps) X(pb_hits)        \
+  X(pb_misses) X(pb_filled_bytes) X(pb_consumed_bytes) X(pb_discarded_bytes) X(rpc_count)    \
+  X(rpc_requested_bytes) X(slot_collisions) X(preads) X(pread_bytes) X(storage_bytes)       \
+  X(pcie_bytes) X(pcie_transfers) X(victims) X(kernel_ns) X(wall_ns) X(ctas) X(word_mismatches)
+
+enum {
+#define GFS_X(name) GFS_STAT_##name,
+  GFS_STAT_FIELDS(GFS_X)
+#undef GFS_X
+  GFS_NSTATS
+};
+
+typedef struct gfs_stats {
+  int64_t v[GFS_NSTATS];
+} gfs_stats;
+
+typedef struct gfs_ctx gfs_ctx;
+
+/* ---- lifecycle: replaces Simulation.__init__ wiring (simulation.py:101-212) ---- */
+int gfs_create(const gfs_config* cfg, gfs_ctx** out);
+void gfs_destroy(gfs_ctx* ctx);
+
+/* ---- files.  The reference has no gopen/gclose: "open" is WorkloadSpec.files /
+ * read_only (workloads.py:24-31) and "close" is the TB-done drain + retire
+ * (gpu_exec.py:281-291).  content_id >= 0 marks a synthetic file whose words
+ * follow W(content_id, i) so the device can verify them (page_tag analogue,
+ * gpu_exec.py:159-160); -1 = arbitrary content. ---- */
+int gfs_gopen(gfs_ctx* ctx, const char* path, int flags, int64_t content_id, int* fid);
+int gfs_gclose(gfs_ctx* ctx, int fid);
+int gfs_file_size(gfs_ctx* ctx, int fid, int64_t* size);
+
+/* ---- the hot path: every TB's gread loop (gpu_exec.py:95-239) on the GPU, fed by
+ * the host daemon (rpc.py:144-229 + host_os.py:221).  dst: device buffer (NULL =
+ * consume-only: pages are cached but not copied out).  Blocks until every TB is
+ * done; cold page cache per run (as a fresh Simulation). ---- */
+int gfs_run(gfs_ctx* ctx, const gfs_program* prog, void* dst, uint64_t dst_bytes, gfs_stats* out);
+
+/* ---- logs of the last run (metrics.deliveries, recorded trace, victim_log) ---- */
+int gfs_log_len(gfs_ctx* ctx, int kind, int64_t* n);
+int gfs_log_copy(gfs_ctx* ctx, int kind, int64_t* out, int64_t cap_records);
+
+/* ---- device consumers ---- */
+/* sum_i mix64(word_i ^ ((i + word_base) * golden)) over nbytes of a device buffer */
+int gfs_checksum(gfs_ctx* ctx, const void* dev_buf, uint64_t nbytes, uint64_t word_base, uint64_t* out);
+/* count words of dev_buf (laid out as prog's user buffer) that differ from W(content of file) */
+int gfs_verify_dst(gfs_ctx* ctx, const gfs_program* prog, const void* dev_buf, uint64_t dst_bytes,
+                   int64_t* mismatched_words);
+
+/* ---- synthetic files (K6): write W(content_id, i) words, multi-threaded ---- */
+int gfs_gen_file(const char* path, int64_t content_id, int64_t size, int threads);
+
+/* ---- introspection ---- */
+const char* gfs_last_error(void);
+int gfs_abi_version(void);
+int gfs_stat_count(void);
+const char* gfs_stat_name(int i);
+int gfs_resident_ctas(gfs_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GFS_H */

@@ -1,0 +1,61 @@
+"""Build libgfs.so in-tree for sm_100a (nvcc cross-compiles without a GPU).
+
+    python -m paper_2109_05366_b200.build [--force]
+
+Output: paper_2109_05366_b200/_lib/libgfs.so (git-ignored, travels to the GPU box
+with the repo snapshot).  Flags: -gencode arch=compute_100a,code=sm_100a -lineinfo -O3.
+"""
+
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+OUT_DIR = os.path.join(PKG, "_lib")
+LIB = os.path.join(OUT_DIR, "libgfs.so")
+SOURCES = [os.path.join(CSRC, "gfs_host.cpp"), os.path.join(CSRC, "gfs_kernels.cu")]
+HEADERS = [os.path.join(CSRC, "gfs_shared.h"), os.path.join(ROOT, "include", "gfs.h")]
+GENCODE = "arch=compute_100a,code=sm_100a"
+
+
+def nvcc() -> str:
+    for cand in (shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
+        if cand and os.path.exists(cand):
+            return cand
+    raise RuntimeError("nvcc not found")
+
+
+def stale() -> bool:
+    if not os.path.exists(LIB):
+        return True
+    t = os.path.getmtime(LIB)
+    return any(os.path.getmtime(p) > t for p in SOURCES + HEADERS)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and not stale():
+        return LIB
+    os.makedirs(OUT_DIR, exist_ok=True)
+    tmp = LIB + ".tmp"
+    cmd = [nvcc(), "-O3", "-std=c++17", "-gencode", GENCODE, "-lineinfo",
+           "-Xcompiler", "-fPIC,-Wall", "-shared",
+           "-I" + os.path.join(ROOT, "include"), "-I" + CSRC,
+           "-o", tmp, *SOURCES, "-lpthread"]
+    if verbose:
+        cmd.append("-Xptxas=-v")
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"nvcc failed ({res.returncode}):\n{res.stderr[-4000:]}")
+    if verbose:
+        sys.stderr.write(res.stderr)
+    os.replace(tmp, LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

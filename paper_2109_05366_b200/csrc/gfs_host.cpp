@@ -1,0 +1,798 @@
+// gfs_host.cpp — host runtime of libgfs.so: context, files, pinned RPC ring, I/O daemon,
+// run orchestration, synthetic-file generator.  C ABI declared in include/gfs.h.
+//
+// Daemon (replaces HostWorker, rpc.py:116-229, and HostOs.pread, host_os.py:221):
+//   io_workers threads share one request ring in mapped pinned memory.  A worker claims
+//   the next ring position (fetch_add), waits for the GPU to publish it, preads the span
+//   (O_DIRECT when aligned) into the CTA slot's pinned staging buffer and completes it:
+//     zerocopy: release-store of {nbytes, seq} into the slot's mapped response mailbox;
+//               the CTA pulls the bytes over PCIe itself (K1);
+//     dma:      cudaMemcpyAsync staging -> HBM landing on the worker's stream, then
+//               cuStreamWriteValue64 of (nbytes << 32 | seq) into the slot's device
+//               doorbell, ordered after the copy.
+//   A shared ring (instead of the reference's tb % n_slots slot partitioning) keeps all
+//   workers busy: the reference's worker-imbalance pathology (criterion 2) cannot occur.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <errno.h>
+#include <fcntl.h>
+#include <immintrin.h>
+#include <pthread.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+#include <sys/stat.h>
+#include <time.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "gfs.h"
+#include "gfs_shared.h"
+
+namespace gfs {
+cudaError_t launch_gread(const DevCtx& c, int cta_threads, cudaStream_t st);
+cudaError_t occupancy_gread(int cta_threads, int* blocks_per_sm);
+cudaError_t launch_checksum(const void* buf, uint64_t nbytes, uint64_t word_base,
+                            unsigned long long* out, int sms, cudaStream_t st);
+cudaError_t launch_verify_dst(const void* buf, const int64_t* segs, const int64_t* seg_dst,
+                              int64_t n_segs, const DevFile* files, unsigned long long* out,
+                              int sms, cudaStream_t st);
+}  // namespace gfs
+
+using namespace gfs;
+
+// ------------------------------------------------------------------- errors
+
+static thread_local std::string g_err;
+
+static int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                     \
+  do {                                                                                     \
+    cudaError_t e_ = (expr);                                                               \
+    if (e_ != cudaSuccess)                                                                 \
+      return fail(GFS_ECUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, \
+                  __LINE__);                                                               \
+  } while (0)
+
+static const char* const kStatNames[GFS_NSTATS] = {
+#define GFS_X(name) #name,
+    GFS_STAT_FIELDS(GFS_X)
+#undef GFS_X
+};
+
+static int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+
+static uint64_t now_ns() {
+  timespec t;
+  clock_gettime(CLOCK_MONOTONIC, &t);
+  return (uint64_t)t.tv_sec * 1000000000ull + (uint64_t)t.tv_nsec;
+}
+
+// ------------------------------------------------------------------- context
+
+struct HostFile {
+  std::string path;
+  int fd_direct = -1;
+  int fd_buffered = -1;
+  int64_t size = 0;
+  int64_t npages = 0;
+  int read_only = 1;
+  int64_t content_id = -1;
+  uint32_t* d_pt = nullptr;
+  bool open = false;
+};
+
+template <typename T>
+struct DevBuf {  // grow-only device buffer
+  T* p = nullptr;
+  size_t n = 0;
+  cudaError_t reserve(size_t count) {
+    if (count <= n) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    cudaError_t e = cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T));
+    if (e == cudaSuccess) n = count;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+struct gfs_ctx {
+  gfs_config cfg{};
+  int sms = 0;
+  int n_ctas = 0;
+  int64_t nframes = 0, quota = 0, pb_cap = 0, slot_bytes = 0, gfifo_cap = 0;
+  uint32_t ring_size = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+
+  // device memory
+  uint8_t* d_frames = nullptr;
+  unsigned long long* d_fkey = nullptr;
+  uint32_t* d_fstate = nullptr;
+  uint32_t* d_own_q = nullptr;
+  uint32_t* d_retired = nullptr;
+  uint32_t* d_gfifo = nullptr;
+  uint32_t* d_recycled = nullptr;
+  DevGlobals* d_g = nullptr;
+  uint8_t* d_landing = nullptr;
+  unsigned long long* d_doorbell = nullptr;
+  int32_t* d_ring_owner = nullptr;
+  unsigned long long* d_cta_wait = nullptr;
+  long long* d_stats = nullptr;
+  unsigned long long* d_scratch = nullptr;
+  DevBuf<int64_t> d_segs, d_prog_off, d_dst_off, d_seg_dst;
+  DevBuf<int32_t> d_order;
+  DevBuf<DevFile> d_files;
+  DevBuf<long long> d_logs[4];
+  unsigned long long log_cap[4] = {0, 0, 0, 0};
+  unsigned long long log_n[4] = {0, 0, 0, 0};
+
+  // mapped pinned host memory
+  RpcReq* h_ring = nullptr;
+  RpcResp* h_resp = nullptr;
+  uint8_t* h_staging = nullptr;
+
+  std::vector<HostFile> files;
+
+  // daemon
+  std::vector<std::thread> workers;
+  std::vector<cudaStream_t> worker_streams;
+  std::atomic<uint64_t> req_head{0};
+  std::atomic<bool> stop{false};
+  std::atomic<int> worker_error{0};
+  std::atomic<uint64_t> served{0};
+  bool has_run = false;
+  // driver entry point resolved through cudart (libgfs does not link libcuda, so it
+  // loads on machines without a driver; CUDA calls then fail loudly)
+  CUresult (*write_value64)(CUstream, CUdeviceptr, cuuint64_t, unsigned int) = nullptr;
+};
+
+// ------------------------------------------------------------------- daemon
+
+static int64_t do_pread(gfs_ctx* ctx, const HostFile& f, int64_t off, int64_t size, uint8_t* buf) {
+  if (off >= f.size || size <= 0) return 0;
+  int64_t n = std::min(size, f.size - off);
+  bool direct = f.fd_direct >= 0 && (off & 4095) == 0 && (((uintptr_t)buf) & 4095) == 0;
+  int fd = direct ? f.fd_direct : f.fd_buffered;
+  int64_t want = direct ? round_up(n, 4096) : n;
+  if (want > ctx->slot_bytes) want = n;  // never write past the staging slot
+  int64_t got = 0;
+  while (got < n) {
+    ssize_t k = pread(fd, buf + got, (size_t)(want - got), (off_t)(off + got));
+    if (k < 0) {
+      if (errno == EINTR) continue;
+      if (direct && errno == EINVAL) {  // filesystem refused O_DIRECT: buffered from here on
+        direct = false;
+        fd = f.fd_buffered;
+        want = n;
+        continue;
+      }
+      return -(int64_t)errno;
+    }
+    if (k == 0) break;
+    got += k;
+    if (direct && (got & 4095)) {  // short O_DIRECT read (EOF); finish buffered
+      direct = false;
+      fd = f.fd_buffered;
+      want = n;
+    }
+  }
+  return std::min(got, n);
+}
+
+static void worker_main(gfs_ctx* ctx, int wid) {
+  const uint32_t mask = ctx->ring_size - 1;
+  cudaStream_t st = ctx->cfg.transfer == GFS_XFER_DMA ? ctx->worker_streams[wid] : nullptr;
+  if (st) cudaSetDevice(ctx->cfg.device);
+  while (!ctx->stop.load(std::memory_order_relaxed)) {
+    uint64_t h = ctx->req_head.fetch_add(1, std::memory_order_relaxed);
+    RpcReq* e = &ctx->h_ring[h & mask];
+    const uint32_t seq = (uint32_t)(h + 1);
+    uint64_t spins = 0;
+    while (__atomic_load_n(&e->seq, __ATOMIC_ACQUIRE) != seq) {
+      if (ctx->stop.load(std::memory_order_relaxed)) return;
+      if (++spins < 20000) {
+        _mm_pause();
+      } else {
+        timespec ts{0, 20000};  // idle: back off to 20 us naps
+        nanosleep(&ts, nullptr);
+      }
+    }
+    const int64_t off = e->offset, size = e->size;
+    const int fid = e->fid, slot = e->slot;
+    int64_t n;
+    uint8_t* stg = ctx->h_staging + (int64_t)slot * ctx->slot_bytes;
+    if (slot < 0 || slot >= ctx->n_ctas || fid < 0 || fid >= (int)ctx->files.size() ||
+        !ctx->files[fid].open || size > ctx->slot_bytes) {
+      n = -EINVAL;
+    } else {
+      n = do_pread(ctx, ctx->files[fid], off, size, stg);
+    }
+    if (n < 0) ctx->worker_error.store((int)-n);
+    if (ctx->cfg.transfer == GFS_XFER_DMA) {
+      if (n > 0)
+        cudaMemcpyAsync(ctx->d_landing + (int64_t)slot * ctx->slot_bytes, stg, (size_t)n,
+                        cudaMemcpyHostToDevice, st);
+      uint64_t v = ((uint64_t)(n < 0 ? 0xFFFFFFFFull : (uint64_t)n) << 32) | seq;
+      ctx->write_value64((CUstream)st, (CUdeviceptr)(ctx->d_doorbell + slot), (cuuint64_t)v, 0);
+    } else {
+      RpcResp* r = &ctx->h_resp[slot];
+      r->nbytes = n;
+      __atomic_store_n(&r->seq, seq, __ATOMIC_RELEASE);
+    }
+    ctx->served.fetch_add(1, std::memory_order_relaxed);
+  }
+}
+
+static void stop_workers(gfs_ctx* ctx) {
+  ctx->stop.store(true);
+  for (auto& t : ctx->workers)
+    if (t.joinable()) t.join();
+  ctx->workers.clear();
+}
+
+// ------------------------------------------------------------------- lifecycle
+
+static void free_all(gfs_ctx* ctx) {
+  stop_workers(ctx);
+  for (auto& f : ctx->files) {
+    if (f.fd_direct >= 0) close(f.fd_direct);
+    if (f.fd_buffered >= 0) close(f.fd_buffered);
+    if (f.d_pt) cudaFree(f.d_pt);
+  }
+  ctx->files.clear();
+  for (auto s : ctx->worker_streams)
+    if (s) cudaStreamDestroy(s);
+  void* dev[] = {ctx->d_frames, ctx->d_fkey, ctx->d_fstate, ctx->d_own_q, ctx->d_retired,
+                 ctx->d_gfifo, ctx->d_recycled, ctx->d_g, ctx->d_landing, ctx->d_doorbell,
+                 ctx->d_ring_owner, ctx->d_cta_wait, ctx->d_stats, ctx->d_scratch};
+  for (void* p : dev)
+    if (p) cudaFree(p);
+  ctx->d_segs.release();
+  ctx->d_prog_off.release();
+  ctx->d_dst_off.release();
+  ctx->d_seg_dst.release();
+  ctx->d_order.release();
+  ctx->d_files.release();
+  for (auto& l : ctx->d_logs) l.release();
+  void* host[] = {ctx->h_ring, ctx->h_resp, ctx->h_staging};
+  for (void* p : host)
+    if (p) cudaFreeHost(p);
+  if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+  if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+}
+
+extern "C" int gfs_create(const gfs_config* cfg_in, gfs_ctx** out) {
+  if (!cfg_in || !out) return fail(GFS_EINVAL, "gfs_create: null argument");
+  *out = nullptr;
+  gfs_config cfg = *cfg_in;
+  if (cfg.page_size < 4096 || cfg.page_size % 4096)
+    return fail(GFS_EINVAL, "page_size must be a positive multiple of 4096 (got %lld)",
+                (long long)cfg.page_size);
+  if (cfg.prefetch_bytes < 0 || cfg.prefetch_bytes % cfg.page_size)
+    return fail(GFS_EINVAL, "prefetch_bytes must be a multiple of page_size");
+  if (cfg.cache_bytes < cfg.page_size) return fail(GFS_EINVAL, "cache_bytes smaller than one page");
+  if (cfg.resident_limit < 1) return fail(GFS_EINVAL, "resident_limit must be >= 1");
+  if (cfg.staging_bytes < 1) return fail(GFS_EINVAL, "staging_bytes must be >= 1");
+  if (cfg.policy != GFS_POLICY_GLOBAL_LRU && cfg.policy != GFS_POLICY_PER_TB_LRA)
+    return fail(GFS_EINVAL, "unknown policy %d", cfg.policy);
+  if (cfg.readahead == GFS_RA_ADAPTIVE && (cfg.ra_max_bytes < cfg.page_size || cfg.ra_max_bytes % cfg.page_size))
+    return fail(GFS_EINVAL, "ra_max_bytes must be a positive multiple of page_size");
+  if (cfg.cta_threads != 128 && cfg.cta_threads != 256 && cfg.cta_threads != 512) cfg.cta_threads = 256;
+  if (cfg.io_workers < 1) cfg.io_workers = 1;
+  if (cfg.io_workers > 256) cfg.io_workers = 256;
+  const int64_t nframes = cfg.cache_bytes / cfg.page_size;
+  if (nframes >= (int64_t)PT_INFLIGHT) return fail(GFS_EINVAL, "too many frames (%lld)", (long long)nframes);
+  const int64_t quota = nframes / cfg.resident_limit;  // gpu_cache.py:32-34
+  if (cfg.policy == GFS_POLICY_PER_TB_LRA && quota < 1 && !cfg.raw_mode)
+    return fail(GFS_EINVAL,
+                "per-tb-lra needs cache_bytes/page_size >= resident TBs (%lld frames for %d TBs)",
+                (long long)nframes, cfg.resident_limit);
+  int64_t pb_cap = cfg.prefetch_bytes;
+  if (cfg.readahead == GFS_RA_ADAPTIVE && cfg.ra_max_bytes - cfg.page_size > pb_cap)
+    pb_cap = cfg.ra_max_bytes - cfg.page_size;
+  if (pb_cap / cfg.page_size >= MAX_PB_ENTRIES)
+    return fail(GFS_EINVAL, "private buffer of %lld pages exceeds %d", (long long)(pb_cap / cfg.page_size),
+                MAX_PB_ENTRIES - 1);
+
+  gfs_ctx* ctx = new gfs_ctx();
+  ctx->cfg = cfg;
+  ctx->nframes = nframes;
+  ctx->quota = quota;
+  ctx->pb_cap = pb_cap;
+  int64_t span_max = cfg.page_size + pb_cap;
+  if (cfg.raw_mode) span_max = std::max<int64_t>(cfg.max_request_bytes, 4096);
+  ctx->slot_bytes = round_up(span_max, 4096);
+  auto bail = [&](int rc) {
+    free_all(ctx);
+    delete ctx;
+    return rc;
+  };
+#define TRY(expr)                                                                            \
+  do {                                                                                       \
+    cudaError_t e_ = (expr);                                                                 \
+    if (e_ != cudaSuccess)                                                                   \
+      return bail(fail(GFS_ECUDA, "%s failed: %s", #expr, cudaGetErrorString(e_)));          \
+  } while (0)
+  TRY(cudaSetDevice(cfg.device));
+  TRY(cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, cfg.device));
+  int per_sm = 0;
+  TRY(occupancy_gread(cfg.cta_threads, &per_sm));
+  int hw = std::max(1, per_sm) * ctx->sms;
+  int want = cfg.max_ctas > 0 ? std::min(cfg.max_ctas, cfg.resident_limit) : cfg.resident_limit;
+  ctx->n_ctas = std::max(1, std::min(want, hw));
+  uint32_t q = 1;
+  while (q < (uint32_t)(4 * ctx->n_ctas) || q < 1024) q <<= 1;
+  ctx->ring_size = q;
+  ctx->gfifo_cap = 2 * nframes + 65536;
+
+  TRY(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+  TRY(cudaEventCreate(&ctx->ev0));
+  TRY(cudaEventCreate(&ctx->ev1));
+  if (!cfg.raw_mode) {
+    TRY(cudaMalloc(&ctx->d_frames, (size_t)(nframes * cfg.page_size)));
+    TRY(cudaMalloc(&ctx->d_fkey, (size_t)nframes * 8));
+    TRY(cudaMalloc(&ctx->d_fstate, (size_t)nframes * 4));
+    TRY(cudaMalloc(&ctx->d_retired, (size_t)nframes * 2 * 4));
+    TRY(cudaMalloc(&ctx->d_recycled, (size_t)nframes * 4));
+    if (cfg.policy == GFS_POLICY_PER_TB_LRA)
+      TRY(cudaMalloc(&ctx->d_own_q, (size_t)ctx->n_ctas * (size_t)std::max<int64_t>(quota, 1) * 4));
+    else
+      TRY(cudaMalloc(&ctx->d_gfifo, (size_t)ctx->gfifo_cap * 4));
+  }
+  TRY(cudaMalloc(&ctx->d_g, sizeof(DevGlobals)));
+  TRY(cudaMalloc(&ctx->d_ring_owner, (size_t)ctx->ring_size * 4));
+  TRY(cudaMalloc(&ctx->d_cta_wait, (size_t)ctx->n_ctas * 8));
+  TRY(cudaMalloc(&ctx->d_stats, (size_t)ctx->n_ctas * GFS_NSTATS * 8));
+  TRY(cudaMalloc(&ctx->d_scratch, 64));
+  TRY(cudaHostAlloc(&ctx->h_ring, (size_t)ctx->ring_size * sizeof(RpcReq),
+                    cudaHostAllocMapped | cudaHostAllocPortable));
+  TRY(cudaHostAlloc(&ctx->h_resp, (size_t)ctx->n_ctas * sizeof(RpcResp),
+                    cudaHostAllocMapped | cudaHostAllocPortable));
+  TRY(cudaHostAlloc(&ctx->h_staging, (size_t)(ctx->n_ctas * ctx->slot_bytes),
+                    cudaHostAllocMapped | cudaHostAllocPortable));
+  memset(ctx->h_ring, 0, (size_t)ctx->ring_size * sizeof(RpcReq));
+  memset(ctx->h_resp, 0, (size_t)ctx->n_ctas * sizeof(RpcResp));
+  if (cfg.transfer == GFS_XFER_DMA) {
+    TRY(cudaMalloc(&ctx->d_landing, (size_t)(ctx->n_ctas * ctx->slot_bytes)));
+    TRY(cudaMalloc(&ctx->d_doorbell, (size_t)ctx->n_ctas * 8));
+    TRY(cudaMemset(ctx->d_doorbell, 0, (size_t)ctx->n_ctas * 8));
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    TRY(cudaGetDriverEntryPoint("cuStreamWriteValue64", &fn, cudaEnableDefault, &qr));
+    if (!fn || qr != cudaDriverEntryPointSuccess)
+      return bail(fail(GFS_ECUDA, "cuStreamWriteValue64 unavailable (stream memory operations)"));
+    ctx->write_value64 = (CUresult(*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int))fn;
+    ctx->worker_streams.resize(cfg.io_workers, nullptr);
+    for (auto& s : ctx->worker_streams) TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  }
+  TRY(cudaDeviceSynchronize());
+#undef TRY
+  for (int w = 0; w < cfg.io_workers; w++) ctx->workers.emplace_back(worker_main, ctx, w);
+  *out = ctx;
+  return GFS_OK;
+}
+
+extern "C" void gfs_destroy(gfs_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->cfg.device);
+  cudaStreamSynchronize(ctx->stream);
+  free_all(ctx);
+  delete ctx;
+}
+
+extern "C" int gfs_resident_ctas(gfs_ctx* ctx) { return ctx ? ctx->n_ctas : 0; }
+
+// ------------------------------------------------------------------- files
+
+extern "C" int gfs_gopen(gfs_ctx* ctx, const char* path, int flags, int64_t content_id, int* fid) {
+  if (!ctx || !path || !fid) return fail(GFS_EINVAL, "gfs_gopen: null argument");
+  HostFile f;
+  f.path = path;
+  f.read_only = (flags & GFS_O_RDWR) ? 0 : 1;
+  f.content_id = content_id;
+  f.fd_buffered = open(path, O_RDONLY);
+  if (f.fd_buffered < 0) return fail(GFS_EIO, "open %s: %s", path, strerror(errno));
+  if (ctx->cfg.io_direct) f.fd_direct = open(path, O_RDONLY | O_DIRECT);  // may be -1: buffered only
+  struct stat sb;
+  if (fstat(f.fd_buffered, &sb) != 0) {
+    close(f.fd_buffered);
+    if (f.fd_direct >= 0) close(f.fd_direct);
+    return fail(GFS_EIO, "stat %s: %s", path, strerror(errno));
+  }
+  f.size = (int64_t)sb.st_size;
+  f.npages = (f.size + ctx->cfg.page_size - 1) / ctx->cfg.page_size + 1;
+  cudaSetDevice(ctx->cfg.device);
+  if (!ctx->cfg.raw_mode) {
+    cudaError_t e = cudaMalloc(&f.d_pt, (size_t)f.npages * 4);
+    if (e != cudaSuccess) {
+      close(f.fd_buffered);
+      if (f.fd_direct >= 0) close(f.fd_direct);
+      return fail(GFS_ECUDA, "page table for %s: %s", path, cudaGetErrorString(e));
+    }
+  }
+  f.open = true;
+  ctx->files.push_back(f);
+  *fid = (int)ctx->files.size() - 1;
+  return GFS_OK;
+}
+
+extern "C" int gfs_gclose(gfs_ctx* ctx, int fid) {
+  if (!ctx || fid < 0 || fid >= (int)ctx->files.size() || !ctx->files[fid].open)
+    return fail(GFS_EINVAL, "gfs_gclose: bad file id %d", fid);
+  HostFile& f = ctx->files[fid];
+  cudaSetDevice(ctx->cfg.device);
+  cudaStreamSynchronize(ctx->stream);
+  if (f.fd_direct >= 0) close(f.fd_direct);
+  if (f.fd_buffered >= 0) close(f.fd_buffered);
+  if (f.d_pt) cudaFree(f.d_pt);
+  f.fd_direct = f.fd_buffered = -1;
+  f.d_pt = nullptr;
+  f.open = false;
+  return GFS_OK;
+}
+
+extern "C" int gfs_file_size(gfs_ctx* ctx, int fid, int64_t* size) {
+  if (!ctx || !size || fid < 0 || fid >= (int)ctx->files.size() || !ctx->files[fid].open)
+    return fail(GFS_EINVAL, "gfs_file_size: bad file id %d", fid);
+  *size = ctx->files[fid].size;
+  return GFS_OK;
+}
+
+// ------------------------------------------------------------------- run
+
+static int upload_files(gfs_ctx* ctx) {
+  std::vector<DevFile> df(ctx->files.size());
+  for (size_t i = 0; i < ctx->files.size(); i++) {
+    const HostFile& f = ctx->files[i];
+    df[i].pt = f.d_pt;
+    df[i].size = f.open ? f.size : 0;
+    df[i].npages = f.npages;
+    df[i].read_only = f.read_only;
+    df[i].content_id = (int32_t)f.content_id;
+  }
+  CUDA_TRY(ctx->d_files.reserve(std::max<size_t>(df.size(), 1)));
+  if (!df.empty())
+    CUDA_TRY(cudaMemcpyAsync(ctx->d_files.p, df.data(), df.size() * sizeof(DevFile),
+                             cudaMemcpyHostToDevice, ctx->stream));
+  return GFS_OK;
+}
+
+static int upload_program(gfs_ctx* ctx, const gfs_program* prog, int64_t* n_segs_out) {
+  const int n_tb = prog->n_tb;
+  const int64_t n_segs = prog->prog_off[n_tb];
+  CUDA_TRY(ctx->d_segs.reserve((size_t)std::max<int64_t>(3 * n_segs, 3)));
+  CUDA_TRY(ctx->d_prog_off.reserve((size_t)n_tb + 1));
+  CUDA_TRY(ctx->d_dst_off.reserve((size_t)std::max(n_tb, 1)));
+  CUDA_TRY(ctx->d_order.reserve((size_t)std::max(n_tb, 1)));
+  if (n_segs)
+    CUDA_TRY(cudaMemcpyAsync(ctx->d_segs.p, prog->segs, (size_t)(3 * n_segs) * 8,
+                             cudaMemcpyHostToDevice, ctx->stream));
+  CUDA_TRY(cudaMemcpyAsync(ctx->d_prog_off.p, prog->prog_off, (size_t)(n_tb + 1) * 8,
+                           cudaMemcpyHostToDevice, ctx->stream));
+  if (n_tb) {
+    CUDA_TRY(cudaMemcpyAsync(ctx->d_dst_off.p, prog->dst_off, (size_t)n_tb * 8,
+                             cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_TRY(cudaMemcpyAsync(ctx->d_order.p, prog->order, (size_t)n_tb * 4,
+                             cudaMemcpyHostToDevice, ctx->stream));
+  }
+  *n_segs_out = n_segs;
+  return GFS_OK;
+}
+
+static int validate_program(gfs_ctx* ctx, const gfs_program* prog, uint64_t dst_bytes, bool has_dst) {
+  if (!prog || prog->n_tb < 0 || !prog->prog_off) return fail(GFS_EINVAL, "bad program");
+  if (prog->request_bytes < 1) return fail(GFS_EINVAL, "request_bytes must be positive");
+  if (ctx->cfg.raw_mode && prog->request_bytes > ctx->slot_bytes)
+    return fail(GFS_EINVAL, "raw request of %lld bytes exceeds the staging slot (%lld)",
+                (long long)prog->request_bytes, (long long)ctx->slot_bytes);
+  std::vector<char> seen((size_t)prog->n_tb, 0);
+  for (int k = 0; k < prog->n_tb; k++) {
+    int t = prog->order[k];
+    if (t < 0 || t >= prog->n_tb || seen[t]) return fail(GFS_EINVAL, "order is not a permutation");
+    seen[t] = 1;
+    if (prog->prog_off[k + 1] < prog->prog_off[k]) return fail(GFS_EINVAL, "prog_off not monotone");
+  }
+  for (int t = 0; t < prog->n_tb; t++) {
+    int64_t pos = prog->dst_off[t];
+    for (int64_t s = prog->prog_off[t]; s < prog->prog_off[t + 1]; s++) {
+      int64_t fid = prog->segs[3 * s], off = prog->segs[3 * s + 1], len = prog->segs[3 * s + 2];
+      if (fid < 0 || fid >= (int64_t)ctx->files.size() || !ctx->files[fid].open)
+        return fail(GFS_EINVAL, "segment %lld names unopened file %lld", (long long)s, (long long)fid);
+      if (off < 0 || len < 0) return fail(GFS_EINVAL, "negative segment offset/length");
+      pos += len;
+      if (has_dst && (uint64_t)pos > dst_bytes)
+        return fail(GFS_EINVAL, "user buffer of %llu bytes too small for TB %d's program",
+                    (unsigned long long)dst_bytes, t);
+    }
+  }
+  return GFS_OK;
+}
+
+extern "C" int gfs_run(gfs_ctx* ctx, const gfs_program* prog, void* dst, uint64_t dst_bytes,
+                       gfs_stats* out) {
+  const uint64_t w0 = now_ns();
+  if (!ctx || !prog || !out) return fail(GFS_EINVAL, "gfs_run: null argument");
+  int rc = validate_program(ctx, prog, dst_bytes, dst != nullptr);
+  if (rc) return rc;
+  CUDA_TRY(cudaSetDevice(ctx->cfg.device));
+  const gfs_config& cfg = ctx->cfg;
+  int64_t n_segs = 0;
+  if ((rc = upload_files(ctx)) || (rc = upload_program(ctx, prog, &n_segs))) return rc;
+
+  // log capacities: one delivery per page step, bounded by pages + 2 per request
+  int64_t pages = 0, requests = 0;
+  for (int64_t s = 0; s < n_segs; s++) {
+    int64_t len = prog->segs[3 * s + 2];
+    pages += len / cfg.page_size + 2;
+    requests += len / prog->request_bytes + 1;
+  }
+  for (int k = 0; k < 4; k++) {
+    ctx->log_cap[k] = 0;
+    ctx->log_n[k] = 0;
+  }
+  if (cfg.log) {
+    const int width[4] = {3, 4, 3, 2};
+    const int64_t cap[4] = {pages + 2 * requests + 16, pages + 2 * requests + 16,
+                            pages + 2 * requests + 16, pages + 2 * requests + 16};
+    for (int k = 0; k < 4; k++) {
+      CUDA_TRY(ctx->d_logs[k].reserve((size_t)(cap[k] * width[k])));
+      ctx->log_cap[k] = (unsigned long long)cap[k];
+    }
+  }
+
+  // cold cache + fresh run state (a new Simulation starts empty)
+  for (auto& f : ctx->files)
+    if (f.open && f.d_pt) CUDA_TRY(cudaMemsetAsync(f.d_pt, 0xFF, (size_t)f.npages * 4, ctx->stream));
+  if (!cfg.raw_mode) {
+    CUDA_TRY(cudaMemsetAsync(ctx->d_fstate, 0, (size_t)ctx->nframes * 4, ctx->stream));
+    CUDA_TRY(cudaMemsetAsync(ctx->d_retired, 0, (size_t)ctx->nframes * 8, ctx->stream));
+    if (ctx->d_gfifo) CUDA_TRY(cudaMemsetAsync(ctx->d_gfifo, 0, (size_t)ctx->gfifo_cap * 4, ctx->stream));
+  }
+  CUDA_TRY(cudaMemsetAsync(ctx->d_g, 0, sizeof(DevGlobals), ctx->stream));
+  CUDA_TRY(cudaMemsetAsync(ctx->d_cta_wait, 0, (size_t)ctx->n_ctas * 8, ctx->stream));
+  CUDA_TRY(cudaMemsetAsync(ctx->d_stats, 0, (size_t)ctx->n_ctas * GFS_NSTATS * 8, ctx->stream));
+  CUDA_TRY(cudaMemsetAsync(ctx->d_ring_owner, 0, (size_t)ctx->ring_size * 4, ctx->stream));
+
+  DevCtx c{};
+  c.page_size = cfg.page_size;
+  c.prefetch_bytes = cfg.prefetch_bytes;
+  c.ra_max_bytes = cfg.ra_max_bytes;
+  c.pb_cap_bytes = ctx->pb_cap;
+  c.slot_bytes = ctx->slot_bytes;
+  c.staging_bytes = cfg.staging_bytes;
+  c.request_bytes = prog->request_bytes;
+  c.nframes = ctx->nframes;
+  c.quota = ctx->quota;
+  c.gfifo_cap = ctx->gfifo_cap;
+  c.policy = cfg.policy;
+  c.readahead = cfg.readahead;
+  c.transfer = cfg.transfer;
+  c.raw_mode = cfg.raw_mode;
+  c.log = cfg.log;
+  c.verify = cfg.verify;
+  c.pcie_disabled = cfg.pcie_disabled;
+  c.n_files = (int32_t)ctx->files.size();
+  c.n_tb = prog->n_tb;
+  c.n_ctas = ctx->n_ctas;
+  c.ring_mask = ctx->ring_size - 1;
+  c.timeout_ns = 60ull * 1000000000ull;
+  c.segs = ctx->d_segs.p;
+  c.prog_off = ctx->d_prog_off.p;
+  c.dst_off = ctx->d_dst_off.p;
+  c.order = ctx->d_order.p;
+  c.dst = (uint8_t*)dst;
+  c.files = ctx->d_files.p;
+  c.frames = ctx->d_frames;
+  c.fkey = ctx->d_fkey;
+  c.fstate = ctx->d_fstate;
+  c.own_q = ctx->d_own_q;
+  c.retired = ctx->d_retired;
+  c.gfifo = ctx->d_gfifo;
+  c.recycled = ctx->d_recycled;
+  c.g = ctx->d_g;
+  c.ring = ctx->h_ring;
+  c.resp = ctx->h_resp;
+  c.staging = ctx->h_staging;
+  c.landing = ctx->d_landing;
+  c.doorbell = ctx->d_doorbell;
+  c.ring_owner = ctx->d_ring_owner;
+  c.cta_wait = ctx->d_cta_wait;
+  c.stats = ctx->d_stats;
+  for (int k = 0; k < 4; k++) {
+    c.logs[k] = ctx->d_logs[k].p;
+    c.log_cap[k] = ctx->log_cap[k];
+  }
+  ctx->worker_error.store(0);
+  if (prog->n_tb > 0) {
+    CUDA_TRY(cudaEventRecord(ctx->ev0, ctx->stream));
+    CUDA_TRY(launch_gread(c, cfg.cta_threads, ctx->stream));
+    CUDA_TRY(cudaEventRecord(ctx->ev1, ctx->stream));
+  }
+  // wait (GIL is released by the ctypes caller); the kernel has its own device timeout
+  const uint64_t deadline = now_ns() + 600ull * 1000000000ull;
+  for (;;) {
+    cudaError_t q = cudaStreamQuery(ctx->stream);
+    if (q == cudaSuccess) break;
+    if (q != cudaErrorNotReady) return fail(GFS_ECUDA, "gread kernel failed: %s", cudaGetErrorString(q));
+    if (now_ns() > deadline) return fail(GFS_ETIMEDOUT, "gread kernel did not finish in 600 s");
+    std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+  float ms = 0.f;
+  if (prog->n_tb > 0) CUDA_TRY(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+
+  DevGlobals g{};
+  CUDA_TRY(cudaMemcpy(&g, ctx->d_g, sizeof g, cudaMemcpyDeviceToHost));
+  std::vector<long long> st((size_t)ctx->n_ctas * GFS_NSTATS);
+  CUDA_TRY(cudaMemcpy(st.data(), ctx->d_stats, st.size() * 8, cudaMemcpyDeviceToHost));
+  memset(out, 0, sizeof *out);
+  for (int b = 0; b < ctx->n_ctas; b++)
+    for (int k = 0; k < GFS_NSTATS; k++) out->v[k] += st[(size_t)b * GFS_NSTATS + k];
+  out->v[GFS_STAT_kernel_ns] = (int64_t)((double)ms * 1e6);
+  out->v[GFS_STAT_ctas] = ctx->n_ctas;
+  for (int k = 0; k < 4; k++) ctx->log_n[k] = std::min(g.log_n[k], ctx->log_cap[k]);
+  ctx->has_run = true;
+  out->v[GFS_STAT_wall_ns] = (int64_t)(now_ns() - w0);
+  if (g.error) {
+    static const char* names[] = {"none", "every frame is in flight (global-lru-dealloc)",
+                                  "per-tb-lra: TB has no frames to recycle and none are free",
+                                  "I/O error from the host daemon", "device wait timed out",
+                                  "global FIFO overflow", "log overflow", "bad program",
+                                  "private buffer overflow"};
+    const char* what = g.error < 9 ? names[g.error] : "unknown";
+    int werr = ctx->worker_error.load();
+    return fail(g.error == ERR_IO ? GFS_EIO : (g.error == ERR_TIMEOUT ? GFS_ETIMEDOUT : GFS_EDEVICE),
+                "device error %d: %s (info %d, arg %llu)%s%s", g.error, what, g.error_info,
+                (unsigned long long)g.error_arg, werr ? "; daemon errno: " : "",
+                werr ? strerror(werr) : "");
+  }
+  return GFS_OK;
+}
+
+// ------------------------------------------------------------------- logs
+
+extern "C" int gfs_log_len(gfs_ctx* ctx, int kind, int64_t* n) {
+  if (!ctx || !n || kind < 0 || kind > 3) return fail(GFS_EINVAL, "gfs_log_len: bad argument");
+  *n = (int64_t)ctx->log_n[kind];
+  return GFS_OK;
+}
+
+extern "C" int gfs_log_copy(gfs_ctx* ctx, int kind, int64_t* out, int64_t cap_records) {
+  if (!ctx || !out || kind < 0 || kind > 3) return fail(GFS_EINVAL, "gfs_log_copy: bad argument");
+  const int width[4] = {3, 4, 3, 2};
+  int64_t n = std::min<int64_t>((int64_t)ctx->log_n[kind], cap_records);
+  if (n > 0)
+    CUDA_TRY(cudaMemcpy(out, ctx->d_logs[kind].p, (size_t)(n * width[kind]) * 8, cudaMemcpyDeviceToHost));
+  return GFS_OK;
+}
+
+// ------------------------------------------------------------------- consumers
+
+extern "C" int gfs_checksum(gfs_ctx* ctx, const void* dev_buf, uint64_t nbytes, uint64_t word_base,
+                            uint64_t* out) {
+  if (!ctx || !out || (!dev_buf && nbytes)) return fail(GFS_EINVAL, "gfs_checksum: bad argument");
+  CUDA_TRY(cudaSetDevice(ctx->cfg.device));
+  CUDA_TRY(cudaMemsetAsync(ctx->d_scratch, 0, 8, ctx->stream));
+  if (nbytes) CUDA_TRY(launch_checksum(dev_buf, nbytes, word_base, ctx->d_scratch, ctx->sms, ctx->stream));
+  unsigned long long v = 0;
+  CUDA_TRY(cudaMemcpyAsync(&v, ctx->d_scratch, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  *out = v;
+  return GFS_OK;
+}
+
+extern "C" int gfs_verify_dst(gfs_ctx* ctx, const gfs_program* prog, const void* dev_buf,
+                              uint64_t dst_bytes, int64_t* mismatched_words) {
+  if (!ctx || !prog || !dev_buf || !mismatched_words) return fail(GFS_EINVAL, "gfs_verify_dst: null argument");
+  int rc = validate_program(ctx, prog, dst_bytes, true);
+  if (rc) return rc;
+  CUDA_TRY(cudaSetDevice(ctx->cfg.device));
+  int64_t n_segs = 0;
+  if ((rc = upload_files(ctx)) || (rc = upload_program(ctx, prog, &n_segs))) return rc;
+  std::vector<int64_t> seg_dst((size_t)std::max<int64_t>(n_segs, 1));
+  for (int t = 0; t < prog->n_tb; t++) {
+    int64_t pos = prog->dst_off[t];
+    for (int64_t s = prog->prog_off[t]; s < prog->prog_off[t + 1]; s++) {
+      seg_dst[s] = pos;
+      pos += prog->segs[3 * s + 2];
+    }
+  }
+  CUDA_TRY(ctx->d_seg_dst.reserve(seg_dst.size()));
+  CUDA_TRY(cudaMemcpyAsync(ctx->d_seg_dst.p, seg_dst.data(), seg_dst.size() * 8, cudaMemcpyHostToDevice,
+                           ctx->stream));
+  CUDA_TRY(cudaMemsetAsync(ctx->d_scratch, 0, 8, ctx->stream));
+  if (n_segs)
+    CUDA_TRY(launch_verify_dst(dev_buf, ctx->d_segs.p, ctx->d_seg_dst.p, n_segs, ctx->d_files.p,
+                               ctx->d_scratch, ctx->sms, ctx->stream));
+  unsigned long long v = 0;
+  CUDA_TRY(cudaMemcpyAsync(&v, ctx->d_scratch, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  *mismatched_words = (int64_t)v;
+  return GFS_OK;
+}
+
+// ------------------------------------------------------------------- synthetic files (K6)
+
+static inline uint64_t h_mix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+extern "C" int gfs_gen_file(const char* path, int64_t content_id, int64_t size, int threads) {
+  if (!path || size < 0 || content_id < 0) return fail(GFS_EINVAL, "gfs_gen_file: bad argument");
+  int fd = open(path, O_CREAT | O_WRONLY | O_TRUNC, 0644);
+  if (fd < 0) return fail(GFS_EIO, "create %s: %s", path, strerror(errno));
+  if (ftruncate(fd, (off_t)size) != 0) {
+    close(fd);
+    return fail(GFS_EIO, "truncate %s: %s", path, strerror(errno));
+  }
+  if (threads < 1) threads = 1;
+  const int64_t chunk = 8 << 20;
+  const int64_t nchunks = (size + chunk - 1) / chunk;
+  std::atomic<int64_t> next{0};
+  std::atomic<int> err{0};
+  auto body = [&]() {
+    std::vector<uint64_t> buf((size_t)(chunk / 8) + 1);
+    for (;;) {
+      int64_t k = next.fetch_add(1);
+      if (k >= nchunks || err.load()) return;
+      const int64_t off = k * chunk, n = std::min(chunk, size - off);
+      const int64_t w0 = off >> 3, nw = (n + 7) >> 3;
+      for (int64_t i = 0; i < nw; i++) {
+        int64_t wi = w0 + i;
+        uint64_t tag = h_mix64(((uint64_t)content_id << 40) ^ (uint64_t)(wi >> 9) ^ 0xA5A5A5A5A5A5A5A5ull);
+        buf[(size_t)i] = h_mix64(tag ^ (uint64_t)wi);
+      }
+      const uint8_t* p = (const uint8_t*)buf.data();
+      int64_t done = 0;
+      while (done < n) {
+        ssize_t w = pwrite(fd, p + done, (size_t)(n - done), (off_t)(off + done));
+        if (w < 0) {
+          if (errno == EINTR) continue;
+          err.store(errno);
+          return;
+        }
+        done += w;
+      }
+    }
+  };
+  std::vector<std::thread> ts;
+  for (int t = 0; t < threads; t++) ts.emplace_back(body);
+  for (auto& t : ts) t.join();
+  if (!err.load() && fsync(fd) != 0) err.store(errno);
+  close(fd);
+  if (err.load()) return fail(GFS_EIO, "write %s: %s", path, strerror(err.load()));
+  return GFS_OK;
+}
+
+// ------------------------------------------------------------------- introspection
+
+extern "C" const char* gfs_last_error(void) { return g_err.c_str(); }
+extern "C" int gfs_abi_version(void) { return GFS_ABI_VERSION; }
+extern "C" int gfs_stat_count(void) { return GFS_NSTATS; }
+extern "C" const char* gfs_stat_name(int i) { return (i >= 0 && i < GFS_NSTATS) ? kStatNames[i] : nullptr; }

@@ -1,0 +1,953 @@
+// gfs_kernels.cu — sm_100a device side of the GPUfs-style sequential-read layer.
+//
+// K3  gread_driver : persistent grid, one CTA per resident TB slot.  Each CTA pulls TB
+//                    ids from the dispatcher ticket and runs that TB's gread loop
+//                    (reference gpu_exec.py:95-239) against the HBM page cache:
+//                    lookup+claim in a direct-mapped page table, per-TB LRA or global
+//                    LRU-dealloc allocation (gpu_cache.py:104-179), private prefetch
+//                    buffer (prefetcher.py:38-68), RPC to the host daemon through a
+//                    mapped pinned ring (rpc.py:82-113), completion polling.
+// K1  span copy    : staging (mapped pinned, zero-copy) or HBM landing (DMA) -> frame
+//                    and user buffer in one pass, 16-byte vectors, word-law verify.
+// K2  hit copy     : frame -> user buffer (16 B vectors, congruence-aware).
+// K4  checksum / verify_dst consumers over a device buffer.
+//
+// Metadata decisions of a TB are made by thread 0 (they are inherently sequential in the
+// reference: page p's RPC fills the private buffer that serves page p+1); every data
+// movement is done by the whole CTA.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "gfs_shared.h"
+
+namespace gfs {
+
+// ------------------------------------------------------------------ primitives
+
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+// W(f, i) = mix64(page_tag(f, i >> 9) ^ i): the synthetic content law.
+__device__ __forceinline__ uint64_t word_law(int64_t cid, int64_t i) {
+  uint64_t tag = mix64(((uint64_t)cid << 40) ^ (uint64_t)(i >> 9) ^ 0xA5A5A5A5A5A5A5A5ull);
+  return mix64(tag ^ (uint64_t)i);
+}
+
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t ld_acquire_sys64(const unsigned long long* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
+  return *(volatile const unsigned long long*)p;
+}
+
+// source kinds for K1/K2 loads
+enum { SRC_HBM = 0, SRC_SYS = 1 };
+
+template <int SRC>
+__device__ __forceinline__ uint4 ld16(const uint4* p) {
+  if (SRC == SRC_SYS) return __ldcv(p);  // mapped pinned host memory: always refetch
+  return __ldcg(p);                      // HBM written by other SMs / copy engine: bypass L1
+}
+template <int SRC>
+__device__ __forceinline__ uint8_t ld1(const uint8_t* p) {
+  if (SRC == SRC_SYS) return *(volatile const uint8_t*)p;
+  return __ldcg((const unsigned char*)p);
+}
+
+// ----------------------------------------------------------------- CTA state
+
+struct Smem {
+  // broadcast from thread 0
+  int act;
+  int abort;
+  uint32_t frame;
+  int64_t n;        // RPC result bytes
+  int64_t nb;       // bytes installed into the frame
+  int64_t src_off;  // offset of the page inside the span buffer
+  int64_t k;        // dispatcher ticket
+  int any_bad;
+  // TB state (thread 0)
+  int tb;
+  int64_t own_head, own_len;
+  long long last_gfifo_pos;
+  int64_t pb_fid, pb_base, pb_count, pb_filled;
+  int64_t ra_win, ra_next_fid, ra_next_page;
+  int pending_seen;
+  long long st[GFS_NSTATS];
+  int32_t pb_nb[MAX_PB_ENTRIES];
+};
+
+enum { A_HIT = 1, A_PBHIT = 2, A_RPC = 3, A_ABORT = 4 };
+
+#define ST(name) s.st[GFS_STAT_##name]
+
+__device__ void set_error(const DevCtx& c, int code, int info, unsigned long long arg) {
+  if (atomicCAS(&c.g->error, 0, code) == 0) {
+    c.g->error_info = info;
+    c.g->error_arg = arg;
+  }
+}
+
+__device__ __forceinline__ bool has_error(const DevCtx& c) {
+  return *(volatile int*)&c.g->error != 0;
+}
+
+// spin helper: true while waiting may continue (no error, no timeout)
+__device__ __forceinline__ bool keep_waiting(const DevCtx& c, uint64_t t0, int info) {
+  if (has_error(c)) return false;
+  if (globaltimer() - t0 > c.timeout_ns) {
+    set_error(c, ERR_TIMEOUT, info, 0);
+    return false;
+  }
+  return true;
+}
+
+__device__ void log_rec(const DevCtx& c, int kind, long long a, long long b, long long d, long long e) {
+  if (!c.log) return;
+  unsigned long long i = atomicAdd(&c.g->log_n[kind], 1ull);
+  if (i >= c.log_cap[kind]) {
+    set_error(c, ERR_LOG_OVERFLOW, kind, i);
+    return;
+  }
+  const int width = kind == GFS_LOG_RPCS ? 4 : (kind == GFS_LOG_WINDOWS ? 2 : 3);
+  long long* r = c.logs[kind] + i * width;
+  r[0] = a;
+  r[1] = b;
+  if (width > 2) r[2] = d;
+  if (width > 3) r[3] = e;
+}
+
+// ------------------------------------------------------------ frame ownership
+
+__device__ __forceinline__ unsigned long long page_key(int64_t fid, int64_t page) {
+  return ((unsigned long long)fid << 40) | (unsigned long long)page;
+}
+
+// Unmap a VALID, unreferenced frame (gpu_cache.py:139-147, 165-178).  Fails if a
+// reader holds a reference or the frame is not valid.
+__device__ bool try_evict(const DevCtx& c, Smem& s, uint32_t v) {
+  if (atomicCAS(&c.fstate[v], FR_VALID, 0u) != FR_VALID) return false;
+  unsigned long long key = c.fkey[v];
+  int64_t vfid = (int64_t)(key >> 40), vpage = (int64_t)(key & ((1ull << 40) - 1));
+  atomicCAS(&c.files[vfid].pt[vpage], v, PT_EMPTY);
+  log_rec(c, GFS_LOG_VICTIMS, s.tb, vfid, vpage, 0);
+  ST(victims)++;
+  return true;
+}
+
+__device__ bool evict_spin(const DevCtx& c, Smem& s, uint32_t v) {
+  uint64_t t0 = globaltimer();
+  while (!try_evict(c, s, v)) {
+    if (!keep_waiting(c, t0, 10)) return false;
+    __nanosleep(100);
+  }
+  return true;
+}
+
+__device__ uint32_t take_recycled(const DevCtx& c) {
+  if (ld_volatile_u64(&c.g->recycled_n) == 0) return PT_EMPTY;
+  while (atomicCAS(&c.g->recycled_lock, 0, 1) != 0) __nanosleep(32);
+  __threadfence();
+  uint32_t f = PT_EMPTY;
+  if (c.g->recycled_n > 0) f = c.recycled[--c.g->recycled_n];
+  __threadfence();
+  atomicExch(&c.g->recycled_lock, 0);
+  return f;
+}
+
+// A free frame (never used, or released at EOF), or PT_EMPTY when none is left.
+__device__ uint32_t take_free(const DevCtx& c) {
+  if (ld_volatile_u64(&c.g->fresh_next) < (unsigned long long)c.nframes) {
+    unsigned long long k = atomicAdd(&c.g->fresh_next, 1ull);
+    if (k < (unsigned long long)c.nframes) return (uint32_t)k;
+  }
+  return take_recycled(c);
+}
+
+__device__ uint32_t retired_pop(const DevCtx& c) {
+  const unsigned long long cap = 2ull * (unsigned long long)c.nframes;
+  for (;;) {
+    unsigned long long h = ld_volatile_u64(&c.g->ret_head);
+    unsigned long long t = ld_volatile_u64(&c.g->ret_tail);
+    if (h >= t) return PT_EMPTY;
+    if (atomicCAS(&c.g->ret_head, h, h + 1) == h) {
+      uint32_t* e = &c.retired[h % cap];
+      uint64_t t0 = globaltimer();
+      uint32_t v;
+      while ((v = ld_acquire_gpu(e)) == 0) {
+        if (!keep_waiting(c, t0, 11)) return PT_EMPTY;
+      }
+      *e = 0;
+      return v - 1;
+    }
+  }
+}
+
+__device__ __forceinline__ void own_push(const DevCtx& c, Smem& s, uint32_t f) {
+  c.own_q[(int64_t)blockIdx.x * c.quota + (s.own_head + s.own_len) % c.quota] = f;
+  s.own_len++;
+}
+
+// per-tb-lra allocation (gpu_cache.py:149-179)
+__device__ uint32_t alloc_per_tb(const DevCtx& c, Smem& s) {
+  if (s.own_len < c.quota) {
+    uint32_t f = take_free(c);
+    if (f != PT_EMPTY) {
+      own_push(c, s, f);
+      ST(pc_allocs)++;
+      return f;
+    }
+    uint32_t v = retired_pop(c);
+    if (v != PT_EMPTY) {
+      if (!evict_spin(c, s, v)) return PT_EMPTY;
+      ST(pc_remaps)++;
+      own_push(c, s, v);
+      return v;
+    }
+    if (has_error(c)) return PT_EMPTY;
+  }
+  if (s.own_len == 0) {
+    set_error(c, ERR_NO_FRAME, s.tb, 0);
+    return PT_EMPTY;
+  }
+  int64_t qi = (int64_t)blockIdx.x * c.quota + s.own_head % c.quota;
+  uint32_t v = c.own_q[qi];
+  s.own_head++;
+  s.own_len--;
+  if (!evict_spin(c, s, v)) return PT_EMPTY;
+  ST(pc_remaps)++;
+  own_push(c, s, v);  // remapped in place, now the most recently allocated
+  return v;
+}
+
+__device__ void gfifo_append(const DevCtx& c, Smem& s, uint32_t f) {
+  unsigned long long pos = atomicAdd(&c.g->g_tail, 1ull);
+  if (pos - ld_volatile_u64(&c.g->g_head) >= (unsigned long long)c.gfifo_cap) {
+    set_error(c, ERR_FIFO_OVERFLOW, 0, pos);
+    return;
+  }
+  st_release_gpu(&c.gfifo[pos % c.gfifo_cap], f + 1);
+  s.last_gfifo_pos = (long long)pos;
+}
+
+// global-lru-dealloc allocation (gpu_cache.py:126-147).  Fresh frames are handed out
+// lock-free (their FIFO position is their ticket order); eviction scans the global
+// allocation-order FIFO for the first valid, unreferenced frame under the global lock.
+__device__ uint32_t alloc_global(const DevCtx& c, Smem& s) {
+  uint32_t f = take_free(c);
+  if (f != PT_EMPTY) {
+    gfifo_append(c, s, f);
+    ST(pc_allocs)++;
+    return f;
+  }
+  uint64_t t0 = globaltimer();
+  for (;;) {
+    while (atomicCAS(&c.g->lock, 0, 1) != 0) {
+      if (!keep_waiting(c, t0, 12)) return PT_EMPTY;
+      __nanosleep(64);
+    }
+    __threadfence();
+    uint32_t victim = PT_EMPTY;
+    unsigned long long head = c.g->g_head;
+    unsigned long long tail = ld_volatile_u64(&c.g->g_tail);
+    for (unsigned long long p = head; p < tail; p++) {
+      uint32_t* e = &c.gfifo[p % c.gfifo_cap];
+      uint32_t val;
+      while ((val = ld_acquire_gpu(e)) == 0) {  // reserved, not yet written
+        if (!keep_waiting(c, t0, 13)) break;
+      }
+      if (val == 0) break;
+      if (val == RING_TOMB) continue;
+      if (try_evict(c, s, val - 1)) {
+        victim = val - 1;
+        *e = RING_TOMB;
+        break;
+      }
+    }
+    // drop leading tombstones
+    while (head < tail && *(volatile uint32_t*)&c.gfifo[head % c.gfifo_cap] == RING_TOMB) {
+      c.gfifo[head % c.gfifo_cap] = 0;
+      head++;
+    }
+    c.g->g_head = head;
+    __threadfence();
+    atomicExch(&c.g->lock, 0);
+    if (victim != PT_EMPTY) {
+      gfifo_append(c, s, victim);
+      ST(pc_evictions)++;
+      ST(pc_allocs)++;
+      return victim;
+    }
+    // every frame in flight or referenced: the reference fails here; a real GPU
+    // may see transient references, so retry until the timeout.
+    if (!keep_waiting(c, t0, 14)) {
+      if (c.g->error == ERR_TIMEOUT) c.g->error = ERR_ALL_INFLIGHT;
+      return PT_EMPTY;
+    }
+    __nanosleep(200);
+  }
+}
+
+// zero-byte RPC result: unbind the in-flight frame (gpu_cache.py:191-206)
+__device__ void release_frame(const DevCtx& c, Smem& s, uint32_t f, uint32_t* pte) {
+  if (c.policy == GFS_POLICY_GLOBAL_LRU) {
+    if (s.last_gfifo_pos >= 0) c.gfifo[s.last_gfifo_pos % c.gfifo_cap] = RING_TOMB;
+  } else {
+    s.own_len--;  // it is the newest own frame
+  }
+  c.fstate[f] = 0;
+  st_release_gpu(pte, PT_EMPTY);
+  while (atomicCAS(&c.g->recycled_lock, 0, 1) != 0) __nanosleep(32);
+  __threadfence();
+  c.recycled[c.g->recycled_n++] = f;
+  __threadfence();
+  atomicExch(&c.g->recycled_lock, 0);
+}
+
+// ---------------------------------------------------------- private buffer
+
+__device__ int64_t page_bytes(const DevFile& F, int64_t pg, int64_t page) {
+  int64_t b = F.size - page * pg;
+  return b < pg ? b : pg;
+}
+
+// prefetcher.py:38-50.  The fill's pages are base+1 .. base+m-1 of one RPC span; their
+// bytes stay in the slot's span buffer at (page - base) * pg.
+__device__ void pb_fill(const DevCtx& c, Smem& s, int64_t fid, int64_t base, int64_t m,
+                        int64_t rest_bytes) {
+  ST(pb_discarded_bytes) += s.pb_filled;  // every unconsumed entry is stale
+  s.pb_fid = fid;
+  s.pb_base = base;
+  s.pb_filled = 0;
+  const DevFile& F = c.files[fid];
+  int64_t remaining = rest_bytes;
+  int64_t cnt = m - 1;
+  if (cnt >= MAX_PB_ENTRIES) {
+    set_error(c, ERR_PB, (int)cnt, 0);
+    cnt = MAX_PB_ENTRIES - 1;
+  }
+  for (int64_t i = 1; i <= cnt; i++) {
+    int64_t nb = page_bytes(F, c.page_size, base + i);
+    if (nb > remaining) nb = remaining;
+    remaining -= nb;
+    if (s.pb_filled + nb > c.pb_cap_bytes) {
+      ST(pb_discarded_bytes) += nb;  // no room, never served
+      s.pb_nb[i] = 0;
+      continue;
+    }
+    s.pb_nb[i] = (int32_t)nb;
+    s.pb_filled += nb;
+    ST(pb_filled_bytes) += nb;
+  }
+  s.pb_count = cnt;
+}
+
+// prefetcher.py:52-61
+__device__ int64_t pb_take(Smem& s, int64_t fid, int64_t page) {
+  int64_t i = page - s.pb_base;
+  if (s.pb_count > 0 && fid == s.pb_fid && i >= 1 && i <= s.pb_count && s.pb_nb[i] > 0) {
+    int64_t nb = s.pb_nb[i];
+    s.pb_nb[i] = 0;
+    s.pb_filled -= nb;
+    ST(pb_hits)++;
+    ST(pb_consumed_bytes) += nb;
+    return nb;
+  }
+  ST(pb_misses)++;
+  return 0;
+}
+
+// request_span (prefetcher.py:13-25) + the adaptive window (io.readahead=adaptive)
+__device__ int64_t rpc_span(const DevCtx& c, Smem& s, int64_t fid, int64_t page, int64_t seg_end) {
+  const DevFile& F = c.files[fid];
+  const int64_t pg = c.page_size;
+  int64_t off = page * pg;
+  if (off >= F.size) return 0;
+  bool ro = F.read_only != 0;
+  int64_t want = (ro && c.prefetch_bytes > 0) ? pg + c.prefetch_bytes : pg;
+  bool adaptive = c.readahead == GFS_RA_ADAPTIVE && ro;
+  if (adaptive) {
+    int64_t base = pg + c.prefetch_bytes;
+    if (s.ra_win > 0 && fid == s.ra_next_fid && page == s.ra_next_page) {
+      s.ra_win = 2 * s.ra_win < c.ra_max_bytes ? 2 * s.ra_win : c.ra_max_bytes;
+    } else {
+      s.ra_win = base;
+    }
+    want = s.ra_win;
+    int64_t seg_lim = (seg_end + pg - 1) / pg * pg - off;  // stay inside this TB's segment
+    if (want > seg_lim) want = seg_lim;
+    if (want < pg) want = pg;
+  }
+  int64_t span = want < F.size - off ? want : F.size - off;
+  if (adaptive) {
+    s.ra_next_fid = fid;
+    s.ra_next_page = page + (span + pg - 1) / pg;
+    log_rec(c, GFS_LOG_WINDOWS, s.tb, span, 0, 0);
+  }
+  return span;
+}
+
+// ----------------------------------------------------------------------- RPC
+
+__device__ __forceinline__ void account_transfer(const DevCtx& c, Smem& s, int64_t n) {
+  ST(preads)++;
+  ST(pread_bytes) += n;
+  ST(storage_bytes) += n;
+  if (!c.pcie_disabled && n > 0) {
+    ST(pcie_bytes) += n;
+    ST(pcie_transfers) += (n + c.staging_bytes - 1) / c.staging_bytes;  // rpc.py:31-55
+  }
+}
+
+// Submit one request for this CTA's slot and wait for its completion (thread 0).
+// Returns bytes read, or -1 on abort.  rpc.py:82-102 (submit), 192-229 (service).
+__device__ int64_t rpc_call(const DevCtx& c, Smem& s, int64_t fid, int64_t off, int64_t size) {
+  const unsigned slot = blockIdx.x;
+  const unsigned long long Q = (unsigned long long)c.ring_mask + 1;
+  unsigned long long pos = atomicAdd(&c.g->req_tail, 1ull);
+  uint64_t t0 = globaltimer();
+  if (pos >= Q) {  // the entry Q positions back must have been taken by a worker
+    unsigned long long j = pos - Q;
+    int owner = *(volatile int32_t*)&c.ring_owner[j & c.ring_mask];
+    while (ld_volatile_u64(&c.cta_wait[owner]) == j + 1) {
+      if (!keep_waiting(c, t0, 20)) return -1;
+      __nanosleep(500);
+    }
+  }
+  c.ring_owner[pos & c.ring_mask] = (int32_t)slot;
+  *(volatile unsigned long long*)&c.cta_wait[slot] = pos + 1;
+  __threadfence();
+  RpcReq* e = &c.ring[pos & c.ring_mask];
+  volatile RpcReq* ve = e;
+  ve->offset = off;
+  ve->size = size;
+  ve->fid = (int32_t)fid;
+  ve->slot = (int32_t)slot;
+  ve->tb = s.tb;
+  const uint32_t seq = (uint32_t)(pos + 1);
+  __threadfence_system();
+  st_release_sys(&e->seq, seq);
+  int64_t n;
+  if (c.transfer == GFS_XFER_DMA) {
+    const unsigned long long* bell = &c.doorbell[slot];
+    for (;;) {
+      uint64_t v = ld_acquire_sys64(bell);
+      if ((uint32_t)v == seq) {
+        n = (int64_t)(v >> 32);
+        if (n == 0xFFFFFFFFll) n = -1;
+        break;
+      }
+      if (!keep_waiting(c, t0, 21)) return -1;
+      __nanosleep(256);
+    }
+  } else {
+    const RpcResp* r = &c.resp[slot];
+    __nanosleep(2000);
+    for (;;) {
+      if (ld_acquire_sys(&r->seq) == seq) {
+        n = *(volatile const int64_t*)&r->nbytes;
+        break;
+      }
+      if (!keep_waiting(c, t0, 22)) return -1;
+      __nanosleep(4000);
+    }
+  }
+  *(volatile unsigned long long*)&c.cta_wait[slot] = 0;
+  if (n < 0) {
+    set_error(c, ERR_IO, (int)fid, (unsigned long long)off);
+    return -1;
+  }
+  return n;
+}
+
+// ------------------------------------------------------------------ copies (all threads)
+
+// Generic congruence-aware copy of n bytes (K2 and partial deliveries).
+template <int BS, int SRC>
+__device__ void copy_bytes(uint8_t* dst, const uint8_t* src, int64_t n) {
+  const int tid = threadIdx.x;
+  if (n <= 0) return;
+  uintptr_t d = (uintptr_t)dst, sp = (uintptr_t)src;
+  if (((d ^ sp) & 15) == 0) {
+    int64_t head = (int64_t)((16 - (d & 15)) & 15);
+    if (head > n) head = n;
+    if (tid < head) dst[tid] = ld1<SRC>(src + tid);
+    int64_t body = (n - head) >> 4;
+    const uint4* s4 = (const uint4*)(src + head);
+    uint4* d4 = (uint4*)(dst + head);
+    int64_t v = tid;
+    for (; v + 3 * BS < body; v += 4 * BS) {
+      uint4 a = ld16<SRC>(s4 + v), b = ld16<SRC>(s4 + v + BS);
+      uint4 x = ld16<SRC>(s4 + v + 2 * BS), y = ld16<SRC>(s4 + v + 3 * BS);
+      d4[v] = a;
+      d4[v + BS] = b;
+      d4[v + 2 * BS] = x;
+      d4[v + 3 * BS] = y;
+    }
+    for (; v < body; v += BS) d4[v] = ld16<SRC>(s4 + v);
+    int64_t t0 = head + (body << 4);
+    for (int64_t i = t0 + tid; i < n; i += BS) dst[i] = ld1<SRC>(src + i);
+  } else {
+    for (int64_t i = tid; i < n; i += BS) dst[i] = ld1<SRC>(src + i);
+  }
+}
+
+// K1: copy a page's nb bytes from the span buffer into its frame (and, when the page is
+// delivered whole to a 16 B-aligned destination, into the user buffer in the same pass),
+// checking every word against W(cid, .).  Returns this thread's mismatching-word count.
+template <int BS, int SRC>
+__device__ int copy_page_in(uint8_t* frame, uint8_t* dst_whole, const uint8_t* src, int64_t nb,
+                            int64_t file_off, int64_t cid) {
+  const int tid = threadIdx.x;
+  int bad = 0;
+  const bool chk = cid >= 0;
+  const int64_t nv = nb >> 4;
+  const uint4* s4 = (const uint4*)src;
+  uint4* f4 = (uint4*)frame;
+  uint4* d4 = (uint4*)dst_whole;
+  const int64_t w0 = file_off >> 3;
+  int64_t v = tid;
+  for (; v + 3 * BS < nv; v += 4 * BS) {
+    uint4 q[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) q[u] = ld16<SRC>(s4 + v + u * BS);
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      f4[v + u * BS] = q[u];
+      if (d4) d4[v + u * BS] = q[u];
+      if (chk) {
+        int64_t wi = w0 + 2 * (v + u * BS);
+        uint64_t lo = ((uint64_t)q[u].y << 32) | q[u].x, hi = ((uint64_t)q[u].w << 32) | q[u].z;
+        bad += (lo != word_law(cid, wi)) + (hi != word_law(cid, wi + 1));
+      }
+    }
+  }
+  for (; v < nv; v += BS) {
+    uint4 q = ld16<SRC>(s4 + v);
+    f4[v] = q;
+    if (d4) d4[v] = q;
+    if (chk) {
+      int64_t wi = w0 + 2 * v;
+      uint64_t lo = ((uint64_t)q.y << 32) | q.x, hi = ((uint64_t)q.w << 32) | q.z;
+      bad += (lo != word_law(cid, wi)) + (hi != word_law(cid, wi + 1));
+    }
+  }
+  for (int64_t i = (nv << 4) + tid; i < nb; i += BS) {  // sub-16 B tail (EOF pages)
+    uint8_t b = ld1<SRC>(src + i);
+    frame[i] = b;
+    if (dst_whole) dst_whole[i] = b;
+    if (chk) {
+      int64_t fo = file_off + i;
+      uint64_t w = word_law(cid, fo >> 3);
+      bad += b != (uint8_t)(w >> (8 * (fo & 7)));
+    }
+  }
+  return bad;
+}
+
+// ----------------------------------------------------------------- gread (all threads)
+
+// One gread of `size` bytes at `offset` of `fid` (gpu_exec.py:107-239).  `dst` is the
+// user-buffer address of byte `offset` (nullptr = consume-only).  Returns delivered bytes,
+// or -1 when the run aborts.
+template <int BS>
+__device__ int64_t gread(const DevCtx& c, Smem& s, int64_t fid, int64_t offset, int64_t size,
+                         int64_t seg_end, uint8_t* dst, int& bad_words) {
+  const int tid = threadIdx.x;
+  const int64_t pg = c.page_size;
+  const DevFile& F = c.files[fid];
+  const int64_t fs = F.size;
+  uint8_t* span_buf = (c.transfer == GFS_XFER_DMA ? c.landing : c.staging) +
+                      (int64_t)blockIdx.x * c.slot_bytes;
+  if (tid == 0) ST(greads)++;
+
+  if (c.raw_mode) {  // gpu_exec.py:114-119, 131-138: whole request, no page cache
+    if (tid == 0) {
+      int64_t n = rpc_call(c, s, fid, offset, size);
+      s.n = n;
+      if (n >= 0) {
+        log_rec(c, GFS_LOG_RPCS, s.tb, fid, offset, size);
+        ST(rpc_count)++;
+        ST(rpc_requested_bytes) += size;
+        account_transfer(c, s, n);
+        ST(user_bytes) += n;
+      }
+    }
+    __syncthreads();
+    int64_t n = s.n;
+    if (n < 0) return -1;
+    if (dst) {
+      if (c.transfer == GFS_XFER_DMA) copy_bytes<BS, SRC_HBM>(dst, span_buf, n);
+      else copy_bytes<BS, SRC_SYS>(dst, span_buf, n);
+    }
+    __syncthreads();
+    return n;
+  }
+
+  int64_t g_pos = offset;
+  const int64_t g_end = offset + size;
+  uint32_t* pt = F.pt;
+  for (;;) {
+    if (g_pos >= g_end || g_pos >= fs) return g_pos - offset;
+    const int64_t page = g_pos / pg;
+    const int64_t page_end = (page + 1) * pg < fs ? (page + 1) * pg : fs;
+    int64_t want = (g_end < page_end ? g_end : page_end) - g_pos;
+    const int64_t in_page = g_pos - page * pg;
+    const unsigned long long key = page_key(fid, page);
+
+    if (tid == 0) {  // ---- decide (gpu_exec.py:142-199) ----
+      int act = A_ABORT;
+      ST(pc_lookups)++;
+      bool pending = false;
+      uint64_t t0 = globaltimer();
+      uint32_t f = PT_EMPTY;
+      bool miss = false;
+      for (;;) {
+        if (has_error(c)) break;
+        uint32_t e = ld_acquire_gpu(&pt[page]);
+        if (e == PT_CLAIMED || (e != PT_EMPTY && (e & PT_INFLIGHT))) {
+          if (!pending) {  // another TB is fetching it: single flight, wait (:167-172)
+            ST(pc_hit_pending)++;
+            pending = true;
+          }
+          if (!keep_waiting(c, t0, 30)) break;
+          __nanosleep(128);
+          continue;
+        }
+        if (pending) {  // woken: the reference re-runs _page_step, one more lookup
+          ST(pc_lookups)++;
+          pending = false;
+        }
+        if (e == PT_EMPTY) {
+          if (atomicCAS(&pt[page], PT_EMPTY, PT_CLAIMED) == PT_EMPTY) {
+            miss = true;
+            break;
+          }
+          continue;
+        }
+        uint32_t old = atomicAdd(&c.fstate[e], FR_REF);
+        if ((old & FR_VALID) && c.fkey[e] == key) {
+          f = e;
+          act = A_HIT;
+          ST(pc_hits)++;
+          break;
+        }
+        atomicSub(&c.fstate[e], FR_REF);  // remapped under us: look again
+      }
+      if (miss) {
+        ST(pc_misses)++;
+        f = c.policy == GFS_POLICY_GLOBAL_LRU ? alloc_global(c, s) : alloc_per_tb(c, s);
+        if (f != PT_EMPTY) {
+          c.fkey[f] = key;
+          st_release_gpu(&pt[page], f | PT_INFLIGHT);
+          int64_t nb = pb_take(s, fid, page);
+          if (nb > 0) {
+            act = A_PBHIT;
+            s.nb = nb;
+            s.src_off = (page - s.pb_base) * pg;
+          } else {
+            int64_t span = rpc_span(c, s, fid, page, seg_end);
+            int64_t n = span > 0 ? rpc_call(c, s, fid, page * pg, span) : 0;
+            if (n >= 0) {
+              log_rec(c, GFS_LOG_RPCS, s.tb, fid, page * pg, span);
+              ST(rpc_count)++;
+              ST(rpc_requested_bytes) += span;
+              account_transfer(c, s, n);
+              act = A_RPC;
+              s.n = n;
+              s.nb = n < pg ? n : pg;
+              s.src_off = 0;
+            }
+          }
+        }
+      }
+      if (has_error(c)) act = A_ABORT;
+      s.act = act;
+      s.frame = f;
+    }
+    __syncthreads();
+    const int act = s.act;
+    const uint32_t f = s.frame;
+    if (act == A_ABORT) return -1;
+    uint8_t* fmem = c.frames + (int64_t)f * pg;
+    uint8_t* d = dst ? dst + (g_pos - offset) : nullptr;
+
+    if (act == A_HIT) {  // K2: frame -> user buffer
+      if (d) copy_bytes<BS, SRC_HBM>(d, fmem + in_page, want);
+      __syncthreads();
+      if (tid == 0) {
+        atomicSub(&c.fstate[f], FR_REF);
+        ST(user_bytes) += want;
+        ST(cache_hit_user_bytes) += want;
+        log_rec(c, GFS_LOG_DELIVERIES, s.tb, fid, page, 0);
+      }
+      g_pos += want;
+      continue;
+    }
+
+    if (act == A_RPC && s.n == 0) {  // zero bytes: page at/after EOF (gpu_exec.py:207-211)
+      if (tid == 0) release_frame(c, s, f, &pt[page]);
+      __syncthreads();
+      return g_pos - offset;
+    }
+
+    // K1: span buffer -> frame (+ user buffer)
+    const int64_t nb = s.nb;
+    if (act == A_RPC) {  // the page may be cut short by the returned byte count
+      const int64_t pend = page * pg + nb < fs ? page * pg + nb : fs;
+      want = (g_end < pend ? g_end : pend) - g_pos;
+    }
+    const bool whole = d && in_page == 0 && want == nb && (((uintptr_t)d & 15) == 0);
+    const uint8_t* src = span_buf + s.src_off;
+    int bad = c.transfer == GFS_XFER_DMA
+                  ? copy_page_in<BS, SRC_HBM>(fmem, whole ? d : nullptr, src, nb, page * pg,
+                                              c.verify ? F.content_id : -1)
+                  : copy_page_in<BS, SRC_SYS>(fmem, whole ? d : nullptr, src, nb, page * pg,
+                                              c.verify ? F.content_id : -1);
+    bad_words += bad;
+    int page_bad = __syncthreads_or(bad);
+    if (d && !whole) {
+      copy_bytes<BS, SRC_HBM>(d, fmem + in_page, want);
+      __syncthreads();
+    }
+    if (tid == 0) {  // install (gpu_cache.py:181-189): data first, then VALID, then the PTE
+      __threadfence();
+      atomicOr(&c.fstate[f], FR_VALID);
+      st_release_gpu(&pt[page], f);
+      if (page_bad) ST(tag_mismatches)++;
+      if (act == A_RPC) {
+        int64_t m = (s.n + pg - 1) / pg;
+        if (m > 1) pb_fill(c, s, fid, page, m, s.n - nb);
+      }
+      ST(user_bytes) += want;
+      log_rec(c, GFS_LOG_DELIVERIES, s.tb, fid, page, 0);
+    }
+    g_pos += want;
+    __syncthreads();
+  }
+}
+
+// TB program (gpu_exec.py:95-105) and TB done (drain + retire, gpu_exec.py:281-291).
+template <int BS>
+__device__ bool run_tb(const DevCtx& c, Smem& s, int tb, int& bad_words) {
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    s.tb = tb;
+    s.own_head = 0;
+    s.own_len = 0;
+    s.pb_count = 0;
+    s.pb_filled = 0;
+    s.pb_fid = -1;
+    s.pb_base = 0;
+    s.ra_win = 0;
+    s.ra_next_fid = -1;
+    s.ra_next_page = -1;
+    s.last_gfifo_pos = -1;
+  }
+  __syncthreads();
+  int64_t pos = c.dst_off[tb];
+  const int64_t s0 = c.prog_off[tb], s1 = c.prog_off[tb + 1];
+  for (int64_t sg = s0; sg < s1; sg++) {
+    const int64_t fid = c.segs[3 * sg], base = c.segs[3 * sg + 1], len = c.segs[3 * sg + 2];
+    if (fid < 0 || fid >= c.n_files) {
+      if (tid == 0) set_error(c, ERR_BAD_PROGRAM, tb, (unsigned long long)sg);
+      return false;
+    }
+    int64_t seg_off = 0;
+    while (seg_off < len) {
+      int64_t size = c.request_bytes < len - seg_off ? c.request_bytes : len - seg_off;
+      uint8_t* d = c.dst ? c.dst + pos + seg_off : nullptr;
+      int64_t got = gread<BS>(c, s, fid, base + seg_off, size, base + len, d, bad_words);
+      if (got < 0) return false;
+      seg_off += got;
+      if (got < size) break;  // short read: rest of the segment is skipped
+    }
+    pos += len;
+  }
+  // TB done: drain the private buffer, retire own frames (pages stay hittable)
+  __shared__ unsigned long long ret_pos;
+  if (tid == 0) {
+    ST(pb_discarded_bytes) += s.pb_filled;
+    s.pb_filled = 0;
+    s.pb_count = 0;
+    if (c.policy == GFS_POLICY_PER_TB_LRA && s.own_len > 0)
+      ret_pos = atomicAdd(&c.g->ret_tail, (unsigned long long)s.own_len);
+  }
+  __syncthreads();
+  if (c.policy == GFS_POLICY_PER_TB_LRA && s.own_len > 0) {
+    const unsigned long long cap = 2ull * (unsigned long long)c.nframes;
+    for (int64_t i = tid; i < s.own_len; i += BS) {
+      uint32_t f = c.own_q[(int64_t)blockIdx.x * c.quota + (s.own_head + i) % c.quota];
+      st_release_gpu(&c.retired[(ret_pos + i) % cap], f + 1);
+    }
+  }
+  __syncthreads();
+  return true;
+}
+
+template <int BS>
+__global__ void __launch_bounds__(BS, 1024 / BS) gread_driver(DevCtx c) {
+  __shared__ Smem s;
+  const int tid = threadIdx.x;
+  if (tid == 0)
+    for (int i = 0; i < GFS_NSTATS; i++) s.st[i] = 0;
+  int bad_words = 0;
+  for (;;) {
+    if (tid == 0) {
+      s.k = has_error(c) ? (int64_t)c.n_tb : (int64_t)atomicAdd(&c.g->next_tb, 1ull);
+    }
+    __syncthreads();
+    const int64_t k = s.k;
+    __syncthreads();
+    if (k >= c.n_tb) break;
+    if (!run_tb<BS>(c, s, c.order[k], bad_words)) break;
+  }
+  __shared__ int mism;
+  if (tid == 0) mism = 0;
+  __syncthreads();
+  if (bad_words) atomicAdd(&mism, bad_words);
+  __syncthreads();
+  if (tid == 0) {
+    s.st[GFS_STAT_word_mismatches] += mism;
+    long long* out = c.stats + (int64_t)blockIdx.x * GFS_NSTATS;
+    for (int i = 0; i < GFS_NSTATS; i++) out[i] = s.st[i];
+    atomicAdd(&c.g->done_ctas, 1ull);
+  }
+}
+
+// ------------------------------------------------------------------ K4 consumers
+
+__global__ void checksum_kernel(const uint8_t* buf, uint64_t nbytes, uint64_t word_base,
+                                unsigned long long* out) {
+  const uint64_t nw = nbytes >> 3;
+  const uint64_t* w = (const uint64_t*)buf;
+  uint64_t acc = 0;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * 2;
+  for (uint64_t i = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * 2; i < nw; i += stride) {
+    if (i + 1 < nw) {
+      uint4 q = __ldcs((const uint4*)(w + i));
+      uint64_t lo = ((uint64_t)q.y << 32) | q.x, hi = ((uint64_t)q.w << 32) | q.z;
+      acc += mix64(lo ^ ((i + word_base) * 0x9E3779B97F4A7C15ull));
+      acc += mix64(hi ^ ((i + 1 + word_base) * 0x9E3779B97F4A7C15ull));
+    } else {
+      acc += mix64(w[i] ^ ((i + word_base) * 0x9E3779B97F4A7C15ull));
+    }
+  }
+  if ((nbytes & 7) && blockIdx.x == 0 && threadIdx.x == 0) {
+    uint64_t last = 0;
+    for (uint64_t b = 0; b < (nbytes & 7); b++) last |= (uint64_t)buf[(nw << 3) + b] << (8 * b);
+    acc += mix64(last ^ ((nw + word_base) * 0x9E3779B97F4A7C15ull));
+  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  __shared__ uint64_t part[32];
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t t = 0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); i++) t += part[i];
+    atomicAdd(out, (unsigned long long)t);
+  }
+}
+
+// Compare the user buffer with the synthetic law, segment by segment.
+__global__ void verify_dst_kernel(const uint8_t* buf, const int64_t* segs, const int64_t* seg_dst,
+                                  int64_t n_segs, const DevFile* files,
+                                  unsigned long long* mismatches) {
+  unsigned long long bad = 0;
+  for (int64_t sg = blockIdx.x; sg < n_segs; sg += gridDim.x) {
+    const int64_t fid = segs[3 * sg], off = segs[3 * sg + 1];
+    int64_t len = segs[3 * sg + 2];
+    const DevFile& F = files[fid];
+    if (F.content_id < 0) continue;
+    if (off + len > F.size) len = F.size > off ? F.size - off : 0;
+    const uint8_t* d = buf + seg_dst[sg];
+    if ((((uintptr_t)d - (uintptr_t)off) & 7) == 0) {
+      int64_t head = (8 - (off & 7)) & 7;
+      if (head > len) head = len;
+      for (int64_t i = threadIdx.x; i < head; i += blockDim.x) {
+        int64_t fo = off + i;
+        bad += d[i] != (uint8_t)(word_law(F.content_id, fo >> 3) >> (8 * (fo & 7)));
+      }
+      const uint64_t* dw = (const uint64_t*)(d + head);
+      const int64_t w0 = (off + head) >> 3, nw = (len - head) >> 3;
+      for (int64_t i = threadIdx.x; i < nw; i += blockDim.x)
+        bad += __ldcs(dw + i) != word_law(F.content_id, w0 + i);
+      for (int64_t i = head + (nw << 3) + threadIdx.x; i < len; i += blockDim.x) {
+        int64_t fo = off + i;
+        bad += d[i] != (uint8_t)(word_law(F.content_id, fo >> 3) >> (8 * (fo & 7)));
+      }
+    } else {
+      for (int64_t i = threadIdx.x; i < len; i += blockDim.x) {
+        int64_t fo = off + i;
+        bad += d[i] != (uint8_t)(word_law(F.content_id, fo >> 3) >> (8 * (fo & 7)));
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
+  if ((threadIdx.x & 31) == 0 && bad) atomicAdd(mismatches, bad);
+}
+
+// ------------------------------------------------------------------ host-side launchers
+
+cudaError_t launch_gread(const DevCtx& c, int cta_threads, cudaStream_t st) {
+  switch (cta_threads) {
+    case 128: gread_driver<128><<<c.n_ctas, 128, 0, st>>>(c); break;
+    case 512: gread_driver<512><<<c.n_ctas, 512, 0, st>>>(c); break;
+    default: gread_driver<256><<<c.n_ctas, 256, 0, st>>>(c); break;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t occupancy_gread(int cta_threads, int* blocks_per_sm) {
+  switch (cta_threads) {
+    case 128: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, gread_driver<128>, 128, 0);
+    case 512: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, gread_driver<512>, 512, 0);
+    default: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, gread_driver<256>, 256, 0);
+  }
+}
+
+cudaError_t launch_checksum(const void* buf, uint64_t nbytes, uint64_t word_base,
+                            unsigned long long* out, int sms, cudaStream_t st) {
+  int grid = sms * 4;
+  checksum_kernel<<<grid, 512, 0, st>>>((const uint8_t*)buf, nbytes, word_base, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_verify_dst(const void* buf, const int64_t* segs, const int64_t* seg_dst,
+                              int64_t n_segs, const DevFile* files, unsigned long long* out,
+                              int sms, cudaStream_t st) {
+  int grid = (int)(n_segs < (int64_t)sms * 8 ? n_segs : (int64_t)sms * 8);
+  if (grid < 1) grid = 1;
+  verify_dst_kernel<<<grid, 512, 0, st>>>((const uint8_t*)buf, segs, seg_dst, n_segs, files, out);
+  return cudaGetLastError();
+}
+
+}  // namespace gfs

@@ -1,0 +1,115 @@
+// gfs_shared.h — layouts shared by the host runtime (gfs_host.cpp) and the
+// device kernels (gfs_kernels.cu).  Plain PODs; every pointer is either device
+// memory or mapped pinned host memory (UVA), as noted.
+#pragma once
+#include <stdint.h>
+
+#include "gfs.h"
+
+namespace gfs {
+
+constexpr uint32_t PT_EMPTY = 0xFFFFFFFFu;    // page-table entry: not cached
+constexpr uint32_t PT_CLAIMED = 0xFFFFFFFEu;  // claimed by a TB, frame not bound yet
+constexpr uint32_t PT_INFLIGHT = 0x80000000u; // frame bound, data not installed
+constexpr uint32_t FR_VALID = 1u;             // frame state bit 0; refcount in bits 1..
+constexpr uint32_t FR_REF = 2u;
+constexpr uint32_t RING_TOMB = 0xFFFFFFFFu;   // global FIFO tombstone
+constexpr int MAX_PB_ENTRIES = 2048;          // private-buffer entries per TB (smem)
+
+// Request record in the mapped request ring (device writes, host daemon reads).
+struct alignas(32) RpcReq {
+  int64_t offset;
+  int64_t size;
+  int32_t fid;
+  int32_t slot;     // resident CTA slot: response + staging index
+  int32_t tb;
+  uint32_t seq;     // written last (release): ring position + 1
+};
+
+// Response mailbox per CTA slot (host writes, device polls).  One cache line
+// each so concurrent workers never share a line.
+struct alignas(64) RpcResp {
+  int64_t nbytes;   // bytes read (EOF-clamped), < 0 = -errno
+  uint32_t seq;     // request seq this answers (written last, release)
+  uint32_t pad[13];
+};
+
+struct DevFile {
+  uint32_t* pt;       // page table: npages entries (device)
+  int64_t size;
+  int64_t npages;
+  int32_t read_only;
+  int32_t content_id; // >= 0: synthetic law W(content_id, i); -1 = unverified
+};
+
+// Global run state in device memory (zeroed per run).
+struct DevGlobals {
+  unsigned long long next_tb;      // dispatcher ticket
+  unsigned long long fresh_next;   // never-used frames handed out in order
+  unsigned long long ret_head, ret_tail;  // retired FIFO (per-tb-lra)
+  unsigned long long g_head, g_tail;      // global FIFO (global-lru-dealloc)
+  unsigned long long req_tail;     // request ring producer counter
+  unsigned long long log_n[4];     // log record counts
+  unsigned long long recycled_n;   // released (EOF) frames stack depth
+  int lock;                        // global policy structural lock
+  int recycled_lock;
+  int error;                       // first error code (GFS_E*), 0 = ok
+  int error_info;
+  unsigned long long error_arg;
+  unsigned long long done_ctas;
+};
+
+enum { ERR_NONE = 0, ERR_ALL_INFLIGHT = 1, ERR_NO_FRAME = 2, ERR_IO = 3, ERR_TIMEOUT = 4,
+       ERR_FIFO_OVERFLOW = 5, ERR_LOG_OVERFLOW = 6, ERR_BAD_PROGRAM = 7, ERR_PB = 8 };
+
+struct DevCtx {
+  // configuration
+  int64_t page_size;
+  int64_t prefetch_bytes;
+  int64_t ra_max_bytes;
+  int64_t pb_cap_bytes;      // private-buffer capacity (bytes)
+  int64_t slot_bytes;        // span buffer bytes per CTA slot
+  int64_t staging_bytes;     // PCIe batch accounting unit
+  int64_t request_bytes;
+  int64_t nframes;
+  int64_t quota;             // per-TB LRA queue cap
+  int64_t gfifo_cap;
+  int32_t policy, readahead, transfer, raw_mode, log, verify, pcie_disabled;
+  int32_t n_files, n_tb, n_ctas;
+  uint32_t ring_mask;
+  uint64_t timeout_ns;
+  // program (device)
+  const int64_t* segs;
+  const int64_t* prog_off;
+  const int64_t* dst_off;
+  const int32_t* order;
+  uint8_t* dst;              // user buffer or nullptr
+  // files (device)
+  const DevFile* files;
+  // page cache (device)
+  uint8_t* frames;
+  unsigned long long* fkey;  // (fid << 40) | page
+  uint32_t* fstate;
+  uint32_t* own_q;           // [n_ctas][quota]
+  uint32_t* retired;         // [2 * nframes], value + 1, 0 = empty
+  uint32_t* gfifo;           // [gfifo_cap], value + 1, 0 = reserved-unwritten
+  uint32_t* recycled;        // [nframes]
+  DevGlobals* g;
+  // RPC (mapped pinned host memory, device-usable pointers)
+  RpcReq* ring;
+  RpcResp* resp;
+  uint8_t* staging;          // [n_ctas][slot_bytes] (zerocopy span buffers)
+  // DMA mode (device)
+  uint8_t* landing;          // [n_ctas][slot_bytes]
+  unsigned long long* doorbell; // [n_ctas] (nbytes << 32 | seq), written by cuStreamWriteValue64
+  // ring reuse guard (device)
+  int32_t* ring_owner;       // [ring_mask + 1]
+  unsigned long long* cta_wait;  // [n_ctas]: ring position the CTA waits on (+1), 0 = none
+  // counters (device): [n_ctas][GFS_NSTATS]
+  long long* stats;
+  // logs (device): [cap][width]
+  long long* logs[4];
+  unsigned long long log_cap[4];
+};
+
+}  // namespace gfs

@@ -1,0 +1,106 @@
+"""ctypes binding of libgfs.so (include/gfs.h).
+
+There is no fallback: if the library is missing or a call fails, a GfsError is
+raised.  The binding releases the GIL for every call (ctypes does), so the host
+I/O daemon threads inside libgfs and Python threads run concurrently.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from .errors import GfsError
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "_lib", "libgfs.so")
+
+POLICY = {"global-lru-dealloc": 0, "per-tb-lra": 1}
+READAHEAD = {"static": 0, "adaptive": 1}
+TRANSFER = {"zerocopy": 0, "dma": 1}
+O_RDONLY, O_RDWR = 0, 2
+LOG_DELIVERIES, LOG_RPCS, LOG_VICTIMS, LOG_WINDOWS = 0, 1, 2, 3
+LOG_WIDTH = {LOG_DELIVERIES: 3, LOG_RPCS: 4, LOG_VICTIMS: 3, LOG_WINDOWS: 2}
+
+# Every entry point declared in include/gfs.h (tests check the library exports them).
+EXPORTS = ["gfs_create", "gfs_destroy", "gfs_gopen", "gfs_gclose", "gfs_file_size", "gfs_run",
+           "gfs_log_len", "gfs_log_copy", "gfs_checksum", "gfs_verify_dst", "gfs_gen_file",
+           "gfs_last_error", "gfs_abi_version", "gfs_stat_count", "gfs_stat_name",
+           "gfs_resident_ctas"]
+
+
+class GfsConfig(C.Structure):
+    _fields_ = [
+        ("page_size", C.c_int64), ("cache_bytes", C.c_int64), ("prefetch_bytes", C.c_int64),
+        ("staging_bytes", C.c_int64), ("ra_max_bytes", C.c_int64), ("max_request_bytes", C.c_int64),
+        ("policy", C.c_int32), ("resident_limit", C.c_int32), ("readahead", C.c_int32),
+        ("transfer", C.c_int32), ("io_workers", C.c_int32), ("io_direct", C.c_int32),
+        ("device", C.c_int32), ("cta_threads", C.c_int32), ("max_ctas", C.c_int32),
+        ("raw_mode", C.c_int32), ("pcie_disabled", C.c_int32), ("log", C.c_int32),
+        ("verify", C.c_int32), ("reserved", C.c_int32 * 3),
+    ]
+
+
+class GfsProgram(C.Structure):
+    _fields_ = [
+        ("n_tb", C.c_int32), ("reserved", C.c_int32), ("request_bytes", C.c_int64),
+        ("segs", C.POINTER(C.c_int64)), ("prog_off", C.POINTER(C.c_int64)),
+        ("dst_off", C.POINTER(C.c_int64)), ("order", C.POINTER(C.c_int32)),
+    ]
+
+
+_lib = None
+_nstats = None
+
+
+def load(path: str = LIB_PATH):
+    """Load libgfs.so (raises GfsError when it is absent: no CPU fallback exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise GfsError(f"{path} is not built; run `python -m paper_2109_05366_b200.build` "
+                       "(the B200 path has no CPU fallback)")
+    L = C.CDLL(path)
+    vp, i32, i64, u64 = C.c_void_p, C.c_int, C.c_int64, C.c_uint64
+    L.gfs_create.argtypes = [C.POINTER(GfsConfig), C.POINTER(vp)]
+    L.gfs_destroy.argtypes = [vp]
+    L.gfs_destroy.restype = None
+    L.gfs_gopen.argtypes = [vp, C.c_char_p, i32, i64, C.POINTER(i32)]
+    L.gfs_gclose.argtypes = [vp, i32]
+    L.gfs_file_size.argtypes = [vp, i32, C.POINTER(i64)]
+    L.gfs_run.argtypes = [vp, C.POINTER(GfsProgram), vp, u64, vp]
+    L.gfs_log_len.argtypes = [vp, i32, C.POINTER(i64)]
+    L.gfs_log_copy.argtypes = [vp, i32, C.POINTER(i64), i64]
+    L.gfs_checksum.argtypes = [vp, vp, u64, u64, C.POINTER(u64)]
+    L.gfs_verify_dst.argtypes = [vp, C.POINTER(GfsProgram), vp, u64, C.POINTER(i64)]
+    L.gfs_gen_file.argtypes = [C.c_char_p, i64, i64, i32]
+    L.gfs_last_error.restype = C.c_char_p
+    L.gfs_stat_name.restype = C.c_char_p
+    L.gfs_stat_name.argtypes = [i32]
+    L.gfs_resident_ctas.argtypes = [vp]
+    for name in ("gfs_create", "gfs_gopen", "gfs_gclose", "gfs_file_size", "gfs_run",
+                 "gfs_log_len", "gfs_log_copy", "gfs_checksum", "gfs_verify_dst", "gfs_gen_file"):
+        getattr(L, name).restype = i32
+    _lib = L
+    return L
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        msg = load().gfs_last_error().decode(errors="replace")
+        raise GfsError(f"{what}: {msg} (code {rc})")
+
+
+def stat_names() -> list[str]:
+    global _nstats
+    L = load()
+    if _nstats is None:
+        _nstats = [L.gfs_stat_name(i).decode() for i in range(L.gfs_stat_count())]
+    return _nstats
+
+
+def gen_file(path: str, content_id: int, size: int, threads: int | None = None) -> None:
+    L = load()
+    check(L.gfs_gen_file(os.fsencode(path), content_id, size, threads or os.cpu_count() or 4),
+          f"gfs_gen_file({path})")

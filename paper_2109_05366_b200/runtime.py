@@ -1,0 +1,328 @@
+"""Python front end of the B200 file layer: gopen / gread / gclose and the drop-in
+``Simulation(cfg, seed).run()``.
+
+``GpuFS`` owns one libgfs context (one GPU, its HBM page cache, its pinned RPC ring
+and its I/O daemon threads).  ``Simulation`` mirrors the reference's outer API
+(gpuiosim/simulation.py:98-242): same constructor, ``run()`` returns a
+``MetricsReport`` with the reference's CSV columns, and after the run the object
+exposes ``metrics`` (counters, and ``deliveries`` when
+``metrics.log_deliveries`` is set before ``run`` — metrics.py:44-46),
+``recorded`` (the RPC trace, rpc.py:196-197) and ``cache.victim_log``
+(gpu_cache.py:88), so reference-style parity checks run unchanged.
+
+PyTorch is used only for plumbing: user buffers are ``torch.uint8`` CUDA tensors
+whose ``data_ptr()`` crosses the C ABI.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import native
+from .config import ExperimentConfig
+from .errors import GfsError
+from .metrics import Metrics, MetricsReport, build_report
+from .rng import SeededRng
+from .workloads import (ProgramTable, TraceRecord, WorkloadSpec, build_workload,
+                        dispatch_order, save_trace)
+
+O_RDONLY, O_RDWR = native.O_RDONLY, native.O_RDWR
+
+
+def native_config(cfg: ExperimentConfig, max_request_bytes: int = 0) -> native.GfsConfig:
+    c = native.GfsConfig()
+    if cfg["gpufs.policy"] not in native.POLICY:
+        raise GfsError(f"unknown gpufs.policy {cfg['gpufs.policy']!r}")
+    c.page_size = cfg["gpufs.page_size"]
+    c.cache_bytes = cfg["gpufs.cache_bytes"]
+    c.prefetch_bytes = cfg["gpufs.prefetch_bytes"]
+    c.staging_bytes = cfg["rpc.staging_bytes"]
+    c.ra_max_bytes = cfg["io.ra_max_bytes"]
+    c.max_request_bytes = max_request_bytes or cfg["workload.request_bytes"]
+    c.policy = native.POLICY[cfg["gpufs.policy"]]
+    c.resident_limit = cfg.resident_limit()
+    c.readahead = native.READAHEAD[cfg["io.readahead"]]
+    c.transfer = native.TRANSFER[cfg["io.transfer"]]
+    c.io_workers = cfg.io_workers()
+    c.io_direct = int(bool(cfg["io.direct"]))
+    c.device = cfg["gpu.device"]
+    c.cta_threads = cfg["gpu.cta_threads"]
+    c.max_ctas = 0
+    c.raw_mode = int(bool(cfg["mode.gpu_cache_disabled"]))
+    c.pcie_disabled = int(bool(cfg["mode.pcie_disabled"]))
+    c.log = int(bool(cfg["mode.deterministic"]))
+    c.verify = int(bool(cfg["mode.verify"]))
+    return c
+
+
+@dataclass
+class RunResult:
+    stats: dict
+    deliveries: np.ndarray | None = None
+    rpcs: np.ndarray | None = None
+    victims: np.ndarray | None = None
+    windows: np.ndarray | None = None
+    extra: dict = field(default_factory=dict)
+
+    @property
+    def seconds(self) -> float:
+        return self.stats["kernel_ns"] / 1e9
+
+    @property
+    def gbps(self) -> float:
+        ns = self.stats["kernel_ns"]
+        return self.stats["user_bytes"] / ns if ns else 0.0
+
+
+def _ptr(a: np.ndarray, ctype):
+    return a.ctypes.data_as(C.POINTER(ctype))
+
+
+class GpuFS:
+    """One GPU's file layer: HBM page cache + RPC ring + host I/O daemon."""
+
+    def __init__(self, cfg: ExperimentConfig, max_request_bytes: int = 0):
+        self.cfg = cfg
+        self._lib = native.load()
+        self._ncfg = native_config(cfg, max_request_bytes)
+        h = C.c_void_p()
+        native.check(self._lib.gfs_create(C.byref(self._ncfg), C.byref(h)), "gfs_create")
+        self._h = h
+        self.files: dict[int, dict] = {}
+
+    # -- lifecycle ----------------------------------------------------------
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) and self._h.value:
+            self._lib.gfs_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def resident_ctas(self) -> int:
+        return self._lib.gfs_resident_ctas(self._h)
+
+    # -- files ----------------------------------------------------------------
+
+    def gopen(self, path: str, flags: int = O_RDONLY, content_id: int = -1) -> int:
+        fid = C.c_int()
+        native.check(self._lib.gfs_gopen(self._h, os.fsencode(path), flags, content_id,
+                                         C.byref(fid)), f"gopen({path})")
+        size = C.c_int64()
+        native.check(self._lib.gfs_file_size(self._h, fid.value, C.byref(size)), "gfs_file_size")
+        self.files[fid.value] = {"path": path, "size": size.value,
+                                 "read_only": not (flags & O_RDWR), "content_id": content_id}
+        return fid.value
+
+    def gclose(self, fid: int) -> None:
+        native.check(self._lib.gfs_gclose(self._h, fid), f"gclose({fid})")
+        self.files.pop(fid, None)
+
+    # -- the hot path ---------------------------------------------------------
+
+    def _program(self, table: ProgramTable, request_bytes: int, order: np.ndarray):
+        p = native.GfsProgram()
+        p.n_tb = table.n_tb
+        p.request_bytes = request_bytes
+        segs = np.ascontiguousarray(table.segs.reshape(-1), dtype=np.int64)
+        if segs.size == 0:
+            segs = np.zeros(3, np.int64)
+        keep = (segs, np.ascontiguousarray(table.prog_off), np.ascontiguousarray(table.dst_off),
+                np.ascontiguousarray(order, dtype=np.int32))
+        p.segs = _ptr(keep[0], C.c_int64)
+        p.prog_off = _ptr(keep[1], C.c_int64)
+        p.dst_off = _ptr(keep[2], C.c_int64)
+        p.order = _ptr(keep[3], C.c_int32)
+        return p, keep
+
+    def run(self, table: ProgramTable, request_bytes: int, dst=None, order=None) -> RunResult:
+        """All TBs' gread loops (gpu_exec.py:95-239); dst = uint8 CUDA tensor or None."""
+        if order is None:
+            order = np.arange(table.n_tb, dtype=np.int32)
+        prog, keep = self._program(table, request_bytes, order)
+        dst_ptr, dst_bytes = None, 0
+        if dst is not None:
+            if not dst.is_cuda or dst.numel() * dst.element_size() < table.dst_bytes:
+                raise GfsError("dst must be a CUDA tensor of at least the program's bytes")
+            dst_ptr, dst_bytes = dst.data_ptr(), dst.numel() * dst.element_size()
+        names = native.stat_names()
+        out = (C.c_int64 * len(names))()
+        native.check(self._lib.gfs_run(self._h, C.byref(prog), dst_ptr, dst_bytes, out), "gfs_run")
+        del keep
+        res = RunResult(stats=dict(zip(names, list(out))))
+        if self._ncfg.log:
+            res.deliveries = self.log(native.LOG_DELIVERIES)
+            res.rpcs = self.log(native.LOG_RPCS)
+            res.victims = self.log(native.LOG_VICTIMS)
+            res.windows = self.log(native.LOG_WINDOWS)
+        return res
+
+    def gread(self, fid: int, offset: int, size: int, dst=None) -> RunResult:
+        """One threadblock's gread of [offset, offset+size) (gpu_exec.py:107-129)."""
+        table = ProgramTable.from_programs([[(fid, offset, size)]])
+        return self.run(table, size, dst)
+
+    def log(self, kind: int) -> np.ndarray:
+        n = C.c_int64()
+        native.check(self._lib.gfs_log_len(self._h, kind, C.byref(n)), "gfs_log_len")
+        w = native.LOG_WIDTH[kind]
+        arr = np.zeros((n.value, w), dtype=np.int64)
+        if n.value:
+            native.check(self._lib.gfs_log_copy(self._h, kind, _ptr(arr, C.c_int64), n.value),
+                         "gfs_log_copy")
+        return arr
+
+    # -- consumers ----------------------------------------------------------------
+
+    def checksum(self, buf, nbytes: int | None = None, word_base: int = 0) -> int:
+        n = buf.numel() * buf.element_size() if nbytes is None else nbytes
+        v = C.c_uint64()
+        native.check(self._lib.gfs_checksum(self._h, buf.data_ptr(), n, word_base, C.byref(v)),
+                     "gfs_checksum")
+        return v.value
+
+    def verify(self, table: ProgramTable, dst) -> int:
+        prog, keep = self._program(table, 1, np.arange(table.n_tb, dtype=np.int32))
+        v = C.c_int64()
+        native.check(self._lib.gfs_verify_dst(self._h, C.byref(prog), dst.data_ptr(),
+                                              dst.numel() * dst.element_size(), C.byref(v)),
+                     "gfs_verify_dst")
+        del keep
+        return v.value
+
+
+# ----------------------------------------------------------------- synthetic files
+
+SYNTH_VERSION = "W1"  # content law W(f, i) = mix64(page_tag(f, i >> 9) ^ i)
+
+
+def synth_dir(cfg: ExperimentConfig) -> str:
+    if cfg["io.dir"]:
+        return cfg["io.dir"]
+    return "/dev/shm" if cfg["mode.ramfs"] else "/tmp"
+
+
+def ensure_synthetic(directory: str, content_id: int, size: int) -> str:
+    """Path of synthetic file `content_id` of `size` bytes, generating it if needed."""
+    os.makedirs(directory, exist_ok=True)
+    path = os.path.join(directory, f"gfs_synth_c{content_id}_{size}.bin")
+    stamp = path + ".ok"
+    if os.path.exists(path) and os.path.exists(stamp) and os.path.getsize(path) == size:
+        with open(stamp) as fh:
+            if fh.read().strip() == SYNTH_VERSION:
+                return path
+    native.gen_file(path, content_id, size)
+    with open(stamp, "w") as fh:
+        fh.write(SYNTH_VERSION)
+    return path
+
+
+def open_workload_files(fs: GpuFS, cfg: ExperimentConfig, workload: WorkloadSpec) -> list[int]:
+    """gopen every workload file: real paths from io.paths, else synthetic files."""
+    paths = [p for p in cfg["io.paths"].split(",") if p] if cfg["io.paths"] else []
+    fids = []
+    for f in range(len(workload.files)):
+        flags = O_RDONLY if workload.read_only[f] else O_RDWR
+        if paths:
+            fids.append(fs.gopen(paths[f], flags, -1))
+        else:
+            path = ensure_synthetic(synth_dir(cfg), f, workload.files[f])
+            fids.append(fs.gopen(path, flags, f))
+    if fids != list(range(len(fids))):
+        raise GfsError("file ids must be assigned densely from 0 on a fresh GpuFS")
+    return fids
+
+
+# ----------------------------------------------------------------- drop-in Simulation
+
+class _CacheView:
+    def __init__(self):
+        self.victim_log: list = []
+
+
+class Simulation:
+    """Drop-in for gpuiosim.simulation.Simulation on the B200.
+
+    Simulation(cfg, seed, label, rep).run() -> MetricsReport.  Real files (io.paths)
+    or synthetic files (io.dir) are read through the GPU page cache into a device
+    user buffer; counters, logs and the verified byte checksum are kept on the object.
+    """
+
+    def __init__(self, cfg: ExperimentConfig, seed: int, label: str = "run", rep: int = 0):
+        if cfg["mode.replay_trace"]:
+            raise GfsError("mode.replay_trace drives the host path only; "
+                           "not part of the B200 gread path (DESIGN.md scope)")
+        self.cfg = cfg
+        self.seed = seed
+        self.label = label
+        self.rep = rep
+        self.workload = build_workload(cfg, SeededRng(seed))
+        self.metrics = Metrics()
+        self.cache = _CacheView()
+        self.recorded: list | None = None
+        self.result: RunResult | None = None
+        self.checksum: int | None = None
+        self.mismatched_words: int | None = None
+
+    def run(self, keep_output: bool = False) -> MetricsReport:
+        import torch
+        cfg = self.cfg
+        wl = self.workload
+        log = bool(cfg["mode.deterministic"] or self.metrics.log_deliveries
+                   or cfg["workload.record_trace"])
+        run_cfg = cfg.copy_with({"mode.deterministic": log}) if log != cfg["mode.deterministic"] else cfg
+        table = ProgramTable.from_programs(wl.programs)
+        order = dispatch_order(table.n_tb, cfg["gpu.dispatch_order"], self.seed)
+        dev = torch.device("cuda", cfg["gpu.device"])
+        with GpuFS(run_cfg, max_request_bytes=wl.request_bytes) as fs:
+            open_workload_files(fs, cfg, wl)
+            dst = torch.empty(max(table.dst_bytes, 1), dtype=torch.uint8, device=dev)
+            res = fs.run(table, wl.request_bytes, dst, order)
+            if cfg["mode.verify"] and not cfg["io.paths"]:
+                self.mismatched_words = fs.verify(table, dst)
+                res.stats["tag_mismatches"] += int(self.mismatched_words > 0)
+            self.checksum = fs.checksum(dst, table.dst_bytes)
+            if keep_output:
+                self.output = dst
+        self.result = res
+        self.metrics = Metrics(res.stats, log_deliveries=self.metrics.log_deliveries)
+        if log:
+            self.metrics.deliveries = [tuple(r) for r in res.deliveries.tolist()]
+            self.cache.victim_log = [tuple(r) for r in res.victims.tolist()]
+            self.recorded = [TraceRecord(*r) for r in res.rpcs.tolist()]
+            if res.windows is not None:
+                self.metrics.window_history = [int(w) for w in res.windows[:, 1]]
+            if cfg["workload.record_trace"]:
+                save_trace(cfg["workload.record_trace"], self.recorded)
+        self._verify(res.stats)
+        return build_report(self.label, wl.name, self.seed, self.rep, res.stats,
+                            self.metrics.window_history)
+
+    def _verify(self, st: dict) -> None:
+        """Post-run invariants of gpuiosim/simulation.py:246-264 on real counters."""
+        wl = self.workload
+        if st["tag_mismatches"] or st.get("word_mismatches"):
+            raise GfsError(f"{st['tag_mismatches']} pages delivered with wrong content")
+        in_bounds = all(off + ln <= wl.files[fid] for prog in wl.programs for fid, off, ln in prog)
+        if in_bounds and st["user_bytes"] != wl.total_bytes:
+            raise GfsError(f"delivered {st['user_bytes']} of {wl.total_bytes} bytes")
+        if st["storage_bytes"] < wl.unique_bytes:
+            raise GfsError("storage read less than the unique workload bytes")
+        if not self.cfg["mode.pcie_disabled"]:
+            if st["pcie_bytes"] < st["user_bytes"] - st["cache_hit_user_bytes"]:
+                raise GfsError("PCIe moved less than the delivered bytes")

@@ -1,0 +1,160 @@
+"""Device parity: the B200 gread path against the reference's golden fixtures and the
+CPU oracle, through the public API and the C ABI.  Runs only with a GPU (-m gpu)."""
+
+import os
+
+import numpy as np
+import pytest
+
+import golden_util as gu
+import oracle as orc
+from paper_2109_05366_b200 import rng as grng
+from paper_2109_05366_b200.config import ExperimentConfig
+from paper_2109_05366_b200.errors import GfsError
+from paper_2109_05366_b200.workloads import ProgramTable, build_workload
+
+pytestmark = pytest.mark.gpu
+
+KiB, MiB = 1 << 10, 1 << 20
+
+
+@pytest.fixture(scope="module")
+def synth_dir(tmp_path_factory):
+    d = "/dev/shm/gfs_test" if os.path.isdir("/dev/shm") else str(tmp_path_factory.mktemp("synth"))
+    os.makedirs(d, exist_ok=True)
+    return d
+
+
+def run_sim(overrides, seed, synth_dir, **extra):
+    from paper_2109_05366_b200.runtime import Simulation
+    cfg = ExperimentConfig({**overrides, "io.dir": synth_dir, "mode.deterministic": True,
+                            "io.workers": 8, **extra})
+    sim = Simulation(cfg, seed)
+    sim.metrics.log_deliveries = True
+    rep = sim.run()
+    return sim, rep
+
+
+def oracle_checksum(cfg, seed):
+    wl = build_workload(cfg)
+    res = orc.run_oracle(cfg, wl, source=orc.SRC_SYNTH, materialize_dst=True, log=False)
+    return res.checksum, res
+
+
+@pytest.mark.parametrize("name", gu.case_names())
+@pytest.mark.parametrize("transfer", ["zerocopy", "dma"])
+def test_golden_case_on_device(name, transfer, synth_dir):
+    g = gu.load(name)
+    sim, rep = run_sim(g["overrides"], g["seed"], synth_dir, **{"io.transfer": transfer})
+    st = sim.result.stats
+    errs = gu.compare(g, st, sim.result.deliveries, sim.result.rpcs, sim.result.victims)
+    assert not errs, f"{name}/{transfer}: " + "; ".join(errs)
+    assert st["word_mismatches"] == 0 and sim.mismatched_words == 0
+    want, _ = oracle_checksum(gu.config_of(g, seed=g["seed"]), g["seed"])
+    assert sim.checksum == want
+    assert rep["user_bytes"] == g["counters"]["user_bytes"]
+
+
+@pytest.mark.parametrize("policy", ["per-tb-lra", "global-lru-dealloc"])
+@pytest.mark.parametrize("readahead", ["static", "adaptive"])
+def test_pressure_many_waves_vs_oracle(policy, readahead, synth_dir):
+    """File 4x the cache, n_tb > resident CTAs (retired-frame reclaim is exercised);
+    counts, per-TB deliveries and RPC traces must equal the oracle's."""
+    over = {"workload.n_tb": 96, "workload.file_bytes": 96 * MiB, "workload.request_bytes": 64 * KiB,
+            "gpufs.page_size": 4 * KiB, "gpufs.prefetch_bytes": 60 * KiB,
+            "gpufs.cache_bytes": 24 * MiB, "gpufs.policy": policy, "gpu.sm_count": 10,
+            "gpu.threads_per_tb": 512, "io.readahead": readahead, "io.ra_max_bytes": 512 * KiB}
+    sim, _ = run_sim(over, 42, synth_dir)
+    cfg = ExperimentConfig({**over})
+    want_sum, ref = oracle_checksum(cfg, 42)
+    ref_log = orc.run_oracle(cfg, build_workload(cfg))
+    st = sim.result.stats
+    for k in ("user_bytes", "greads", "pc_misses", "pc_hits", "pb_hits", "pb_misses", "rpc_count",
+              "rpc_requested_bytes", "pc_allocs", "pc_evictions", "pc_remaps", "victims",
+              "pb_filled_bytes", "pb_discarded_bytes", "pcie_bytes"):
+        assert st[k] == ref_log.stats[k], k
+    assert np.array_equal(gu.by_tb(sim.result.deliveries), gu.by_tb(ref_log.deliveries))
+    assert np.array_equal(gu.by_tb(sim.result.rpcs), gu.by_tb(ref_log.rpcs))
+    if readahead == "adaptive":
+        assert np.array_equal(gu.by_tb(sim.result.windows), gu.by_tb(ref_log.windows))
+        assert st["rpc_count"] < 96 * (1 * MiB // (64 * KiB))
+    assert sim.checksum == want_sum
+    assert st["word_mismatches"] == 0
+
+
+def test_adaptive_window_law_single_stream(synth_dir):
+    over = {"workload.n_tb": 1, "workload.file_bytes": 8 * MiB, "gpufs.prefetch_bytes": 60 * KiB,
+            "io.readahead": "adaptive", "io.ra_max_bytes": 1 * MiB, "gpufs.cache_bytes": 16 * MiB}
+    sim, rep = run_sim(over, 1, synth_dir)
+    w = [int(x) for x in sim.result.windows[:, 1]]
+    assert w[:5] == [64 * KiB, 128 * KiB, 256 * KiB, 512 * KiB, 1 * MiB]
+    assert set(w[4:]) == {1 * MiB}
+    assert rep["ra_max_window_bytes"] == 1 * MiB
+
+
+def test_gread_api_offsets_and_eof(synth_dir):
+    from paper_2109_05366_b200.runtime import GpuFS, ensure_synthetic
+    import torch
+    size = 3 * MiB + 1000
+    path = ensure_synthetic(synth_dir, 5, size)
+    cfg = ExperimentConfig({"gpufs.cache_bytes": 8 * MiB, "gpufs.prefetch_bytes": 28 * KiB,
+                            "io.workers": 4})
+    with GpuFS(cfg, max_request_bytes=1 * MiB) as fs:
+        fid = fs.gopen(path, content_id=5)
+        dst = torch.zeros(1 * MiB, dtype=torch.uint8, device="cuda")
+        # unaligned offset inside the file
+        r = fs.gread(fid, 12345, 100_000, dst)
+        assert r.stats["user_bytes"] == 100_000
+        assert dst[:100_000].cpu().numpy().tobytes() == grng.content(5, 12345, 100_000)
+        # read crossing EOF: short read
+        r = fs.gread(fid, size - 5000, 64 * KiB, dst)
+        assert r.stats["user_bytes"] == 5000
+        assert dst[:5000].cpu().numpy().tobytes() == grng.content(5, size - 5000, 5000)
+        # read starting past EOF: zero bytes
+        r = fs.gread(fid, size + 4096 * 3, 4096, dst)
+        assert r.stats["user_bytes"] == 0
+        fs.gclose(fid)
+
+
+def test_consume_only_and_raw_mode(synth_dir):
+    from paper_2109_05366_b200.runtime import GpuFS, ensure_synthetic
+    import torch
+    size = 8 * MiB
+    path = ensure_synthetic(synth_dir, 0, size)
+    table = ProgramTable.from_programs([[(0, t * MiB, MiB)] for t in range(8)])
+    cfg = ExperimentConfig({"gpufs.cache_bytes": 16 * MiB, "gpufs.prefetch_bytes": 60 * KiB})
+    with GpuFS(cfg) as fs:
+        fs.gopen(path, content_id=0)
+        r = fs.run(table, 64 * KiB, None)
+        assert r.stats["user_bytes"] == size and r.stats["word_mismatches"] == 0
+    raw = ExperimentConfig({"mode.gpu_cache_disabled": True, "workload.request_bytes": 256 * KiB})
+    with GpuFS(raw, max_request_bytes=256 * KiB) as fs:
+        fs.gopen(path, content_id=0)
+        dst = torch.empty(size, dtype=torch.uint8, device="cuda")
+        r = fs.run(table, 256 * KiB, dst)
+        assert r.stats["user_bytes"] == size and r.stats["rpc_count"] == 32
+        assert fs.verify(table, dst) == 0
+        assert fs.checksum(dst) == grng.checksum(grng.content(0, 0, size))
+
+
+def test_errors_are_loud(synth_dir):
+    from paper_2109_05366_b200.runtime import GpuFS
+    cfg = ExperimentConfig({"gpufs.cache_bytes": 4 * 4096, "gpufs.policy": "per-tb-lra",
+                            "gpu.sm_count": 148, "gpu.threads_per_tb": 512})
+    with pytest.raises(GfsError):
+        GpuFS(cfg)  # quota floor(4 / 592) = 0 (gpu_cache.py:67-71)
+    with GpuFS(ExperimentConfig({"gpufs.cache_bytes": 1 * MiB})) as fs:
+        with pytest.raises(GfsError):
+            fs.gopen("/nonexistent/file.bin")
+        with pytest.raises(GfsError):
+            fs.run(ProgramTable.from_programs([[(3, 0, 4096)]]), 4096, None)  # unopened file
+
+
+def test_checksum_kernel_matches_numpy():
+    import torch
+    from paper_2109_05366_b200.runtime import GpuFS
+    data = grng.content(2, 100, 1_000_003)
+    t = torch.frombuffer(bytearray(data), dtype=torch.uint8).cuda()
+    with GpuFS(ExperimentConfig({"gpufs.cache_bytes": 1 * MiB})) as fs:
+        assert fs.checksum(t) == grng.checksum(data)
+        assert fs.checksum(t, word_base=9) == grng.checksum(data, 9)
