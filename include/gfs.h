@@ -134,6 +134,17 @@ int gfs_verify_dst(gfs_ctx* ctx, const gfs_program* prog, const void* dev_buf, u
 /* ---- synthetic files (K6): write W(content_id, i) words, multi-threaded ---- */
 int gfs_gen_file(const char* path, int64_t content_id, int64_t size, int threads);
 
+/* ---- comparison arms and roofline probes (bench.py; not on the gread path) ---- */
+/* parallel sequential read of [offset, offset+size) of path; wall seconds */
+int gfs_bench_storage(const char* path, int64_t offset, int64_t size, int threads, int64_t chunk,
+                      int direct, double* seconds);
+/* best-of-reps pinned host -> HBM cudaMemcpyAsync of `bytes`; seconds */
+int gfs_bench_h2d(int device, int64_t bytes, int reps, double* best_seconds);
+/* CPU I/O baseline: threads pread() into pinned buffers + cudaMemcpy into dst_dev
+ * (sync = 1: blocking cudaMemcpy per chunk, the paper's CPU arm); wall seconds */
+int gfs_bench_read_memcpy(const char* path, int64_t offset, int64_t size, void* dst_dev, int device,
+                          int threads, int64_t chunk, int direct, int sync, double* seconds);
+
 /* ---- introspection ---- */
 const char* gfs_last_error(void);
 int gfs_abi_version(void);

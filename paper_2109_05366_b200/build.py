@@ -18,7 +18,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OUT_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(OUT_DIR, "libgfs.so")
-SOURCES = [os.path.join(CSRC, "gfs_host.cpp"), os.path.join(CSRC, "gfs_kernels.cu")]
+SOURCES = [os.path.join(CSRC, "gfs_host.cpp"), os.path.join(CSRC, "gfs_baseline.cpp"),
+           os.path.join(CSRC, "gfs_kernels.cu")]
 HEADERS = [os.path.join(CSRC, "gfs_shared.h"), os.path.join(ROOT, "include", "gfs.h")]
 GENCODE = "arch=compute_100a,code=sm_100a"
 

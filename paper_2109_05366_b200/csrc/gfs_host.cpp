@@ -142,6 +142,7 @@ struct gfs_ctx {
   unsigned long long* d_cta_wait = nullptr;
   long long* d_stats = nullptr;
   unsigned long long* d_scratch = nullptr;
+  unsigned long long* h_served = nullptr;  // mapped: requests completed by the daemon
   DevBuf<int64_t> d_segs, d_prog_off, d_dst_off, d_seg_dst;
   DevBuf<int32_t> d_order;
   DevBuf<DevFile> d_files;
@@ -162,7 +163,6 @@ struct gfs_ctx {
   std::atomic<uint64_t> req_head{0};
   std::atomic<bool> stop{false};
   std::atomic<int> worker_error{0};
-  std::atomic<uint64_t> served{0};
   bool has_run = false;
   // driver entry point resolved through cudart (libgfs does not link libcuda, so it
   // loads on machines without a driver; CUDA calls then fail loudly)
@@ -231,6 +231,8 @@ static void worker_main(gfs_ctx* ctx, int wid) {
       n = do_pread(ctx, ctx->files[fid], off, size, stg);
     }
     if (n < 0) ctx->worker_error.store((int)-n);
+    // count it before completing: a launch that starts after this completion must see it
+    __atomic_fetch_add(ctx->h_served, 1ull, __ATOMIC_SEQ_CST);
     if (ctx->cfg.transfer == GFS_XFER_DMA) {
       if (n > 0)
         cudaMemcpyAsync(ctx->d_landing + (int64_t)slot * ctx->slot_bytes, stg, (size_t)n,
@@ -242,7 +244,6 @@ static void worker_main(gfs_ctx* ctx, int wid) {
       r->nbytes = n;
       __atomic_store_n(&r->seq, seq, __ATOMIC_RELEASE);
     }
-    ctx->served.fetch_add(1, std::memory_order_relaxed);
   }
 }
 
@@ -277,7 +278,7 @@ static void free_all(gfs_ctx* ctx) {
   ctx->d_order.release();
   ctx->d_files.release();
   for (auto& l : ctx->d_logs) l.release();
-  void* host[] = {ctx->h_ring, ctx->h_resp, ctx->h_staging};
+  void* host[] = {ctx->h_ring, ctx->h_resp, ctx->h_staging, ctx->h_served};
   for (void* p : host)
     if (p) cudaFreeHost(p);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
@@ -376,6 +377,8 @@ extern "C" int gfs_create(const gfs_config* cfg_in, gfs_ctx** out) {
                     cudaHostAllocMapped | cudaHostAllocPortable));
   memset(ctx->h_ring, 0, (size_t)ctx->ring_size * sizeof(RpcReq));
   memset(ctx->h_resp, 0, (size_t)ctx->n_ctas * sizeof(RpcResp));
+  TRY(cudaHostAlloc(&ctx->h_served, 64, cudaHostAllocMapped | cudaHostAllocPortable));
+  memset(ctx->h_served, 0, 64);
   if (cfg.transfer == GFS_XFER_DMA) {
     TRY(cudaMalloc(&ctx->d_landing, (size_t)(ctx->n_ctas * ctx->slot_bytes)));
     TRY(cudaMalloc(&ctx->d_doorbell, (size_t)ctx->n_ctas * 8));
@@ -615,6 +618,7 @@ extern "C" int gfs_run(gfs_ctx* ctx, const gfs_program* prog, void* dst, uint64_
   c.recycled = ctx->d_recycled;
   c.g = ctx->d_g;
   c.ring = ctx->h_ring;
+  c.host_served = ctx->h_served;
   c.resp = ctx->h_resp;
   c.staging = ctx->h_staging;
   c.landing = ctx->d_landing;
@@ -796,3 +800,6 @@ extern "C" const char* gfs_last_error(void) { return g_err.c_str(); }
 extern "C" int gfs_abi_version(void) { return GFS_ABI_VERSION; }
 extern "C" int gfs_stat_count(void) { return GFS_NSTATS; }
 extern "C" const char* gfs_stat_name(int i) { return (i >= 0 && i < GFS_NSTATS) ? kStatNames[i] : nullptr; }
+
+// lets the baseline translation unit report through the same thread-local error slot
+extern "C" int gfs_internal_fail(int code, const char* msg) { return fail(code, "%s", msg); }

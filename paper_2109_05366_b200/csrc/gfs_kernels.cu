@@ -432,7 +432,7 @@ __device__ __forceinline__ void account_transfer(const DevCtx& c, Smem& s, int64
 __device__ int64_t rpc_call(const DevCtx& c, Smem& s, int64_t fid, int64_t off, int64_t size) {
   const unsigned slot = blockIdx.x;
   const unsigned long long Q = (unsigned long long)c.ring_mask + 1;
-  unsigned long long pos = atomicAdd(&c.g->req_tail, 1ull);
+  unsigned long long pos = c.g->req_base + atomicAdd(&c.g->req_local, 1ull);
   uint64_t t0 = globaltimer();
   if (pos >= Q) {  // the entry Q positions back must have been taken by a worker
     unsigned long long j = pos - Q;
@@ -817,8 +817,18 @@ template <int BS>
 __global__ void __launch_bounds__(BS, 1024 / BS) gread_driver(DevCtx c) {
   __shared__ Smem s;
   const int tid = threadIdx.x;
-  if (tid == 0)
+  if (tid == 0) {
     for (int i = 0; i < GFS_NSTATS; i++) s.st[i] = 0;
+    // ring base for this launch: the daemon's completed-request count
+    if (atomicCAS(&c.g->base_state, 0, 1) == 0) {
+      c.g->req_base = ld_acquire_sys64(c.host_served);
+      __threadfence();
+      atomicExch(&c.g->base_state, 2);
+    } else {
+      while (*(volatile int*)&c.g->base_state != 2) __nanosleep(64);
+      __threadfence();
+    }
+  }
   int bad_words = 0;
   for (;;) {
     if (tid == 0) {

@@ -48,7 +48,10 @@ struct DevGlobals {
   unsigned long long fresh_next;   // never-used frames handed out in order
   unsigned long long ret_head, ret_tail;  // retired FIFO (per-tb-lra)
   unsigned long long g_head, g_tail;      // global FIFO (global-lru-dealloc)
-  unsigned long long req_tail;     // request ring producer counter
+  unsigned long long req_local;    // requests produced by this launch
+  unsigned long long req_base;     // ring position of this launch's first request
+  int base_state;                  // 0 = unset, 1 = being set, 2 = ready
+  int pad0;
   unsigned long long log_n[4];     // log record counts
   unsigned long long recycled_n;   // released (EOF) frames stack depth
   int lock;                        // global policy structural lock
@@ -97,6 +100,11 @@ struct DevCtx {
   DevGlobals* g;
   // RPC (mapped pinned host memory, device-usable pointers)
   RpcReq* ring;
+  // Requests completed by the daemon so far (mapped host memory).  Read once per launch
+  // as the ring base: every earlier request is complete when a launch starts, so the
+  // daemon's next expected position equals it — also under profiler kernel replay,
+  // which restores device memory but not the daemon's progress.
+  const unsigned long long* host_served;
   RpcResp* resp;
   uint8_t* staging;          // [n_ctas][slot_bytes] (zerocopy span buffers)
   // DMA mode (device)

@@ -26,7 +26,7 @@ LOG_WIDTH = {LOG_DELIVERIES: 3, LOG_RPCS: 4, LOG_VICTIMS: 3, LOG_WINDOWS: 2}
 EXPORTS = ["gfs_create", "gfs_destroy", "gfs_gopen", "gfs_gclose", "gfs_file_size", "gfs_run",
            "gfs_log_len", "gfs_log_copy", "gfs_checksum", "gfs_verify_dst", "gfs_gen_file",
            "gfs_last_error", "gfs_abi_version", "gfs_stat_count", "gfs_stat_name",
-           "gfs_resident_ctas"]
+           "gfs_resident_ctas", "gfs_bench_storage", "gfs_bench_h2d", "gfs_bench_read_memcpy"]
 
 
 class GfsConfig(C.Structure):
@@ -79,8 +79,13 @@ def load(path: str = LIB_PATH):
     L.gfs_stat_name.restype = C.c_char_p
     L.gfs_stat_name.argtypes = [i32]
     L.gfs_resident_ctas.argtypes = [vp]
+    dp = C.POINTER(C.c_double)
+    L.gfs_bench_storage.argtypes = [C.c_char_p, i64, i64, i32, i64, i32, dp]
+    L.gfs_bench_h2d.argtypes = [i32, i64, i32, dp]
+    L.gfs_bench_read_memcpy.argtypes = [C.c_char_p, i64, i64, vp, i32, i32, i64, i32, i32, dp]
     for name in ("gfs_create", "gfs_gopen", "gfs_gclose", "gfs_file_size", "gfs_run",
-                 "gfs_log_len", "gfs_log_copy", "gfs_checksum", "gfs_verify_dst", "gfs_gen_file"):
+                 "gfs_log_len", "gfs_log_copy", "gfs_checksum", "gfs_verify_dst", "gfs_gen_file",
+                 "gfs_bench_storage", "gfs_bench_h2d", "gfs_bench_read_memcpy"):
         getattr(L, name).restype = i32
     _lib = L
     return L
@@ -104,3 +109,30 @@ def gen_file(path: str, content_id: int, size: int, threads: int | None = None) 
     L = load()
     check(L.gfs_gen_file(os.fsencode(path), content_id, size, threads or os.cpu_count() or 4),
           f"gfs_gen_file({path})")
+
+
+def bench_storage(path: str, offset: int, size: int, threads: int, chunk: int, direct: bool) -> float:
+    """Seconds to read [offset, offset+size) of path with `threads` parallel readers."""
+    L = load()
+    sec = C.c_double()
+    check(L.gfs_bench_storage(os.fsencode(path), offset, size, threads, chunk, int(direct),
+                              C.byref(sec)), "gfs_bench_storage")
+    return sec.value
+
+
+def bench_h2d(device: int, nbytes: int, reps: int = 5) -> float:
+    """Best seconds of a pinned host->HBM copy of nbytes."""
+    L = load()
+    sec = C.c_double()
+    check(L.gfs_bench_h2d(device, nbytes, reps, C.byref(sec)), "gfs_bench_h2d")
+    return sec.value
+
+
+def bench_read_memcpy(path: str, offset: int, size: int, dst_ptr: int, device: int, threads: int,
+                      chunk: int, direct: bool, sync: bool) -> float:
+    """Seconds for the CPU read()+cudaMemcpy baseline over [offset, offset+size)."""
+    L = load()
+    sec = C.c_double()
+    check(L.gfs_bench_read_memcpy(os.fsencode(path), offset, size, dst_ptr, device, threads, chunk,
+                                  int(direct), int(sync), C.byref(sec)), "gfs_bench_read_memcpy")
+    return sec.value

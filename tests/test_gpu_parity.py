@@ -88,7 +88,9 @@ def test_adaptive_window_law_single_stream(synth_dir):
     sim, rep = run_sim(over, 1, synth_dir)
     w = [int(x) for x in sim.result.windows[:, 1]]
     assert w[:5] == [64 * KiB, 128 * KiB, 256 * KiB, 512 * KiB, 1 * MiB]
-    assert set(w[4:]) == {1 * MiB}
+    # capped at ra_max, the last window clamped to the end of the TB's segment
+    assert set(w[4:-1]) == {1 * MiB} and w[-1] == 8 * MiB - 960 * KiB - 7 * MiB
+    assert sum(w) == 8 * MiB
     assert rep["ra_max_window_bytes"] == 1 * MiB
 
 
