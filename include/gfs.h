@@ -86,7 +86,8 @@ typedef struct gfs_program {
   X(pc_hit_pending) X(pc_misses) X(pc_allocs) X(pc_evictions) X(pc_remaps) X(pb_hits)        \
   X(pb_misses) X(pb_filled_bytes) X(pb_consumed_bytes) X(pb_discarded_bytes) X(rpc_count)    \
   X(rpc_requested_bytes) X(slot_collisions) X(preads) X(pread_bytes) X(storage_bytes)       \
-  X(pcie_bytes) X(pcie_transfers) X(victims) X(kernel_ns) X(wall_ns) X(ctas) X(word_mismatches)
+  X(pcie_bytes) X(pcie_transfers) X(victims) X(kernel_ns) X(wall_ns) X(ctas) X(word_mismatches) \
+  X(wait_ns) X(meta_ns) X(copy_ns)
 
 enum {
 #define GFS_X(name) GFS_STAT_##name,

@@ -138,8 +138,7 @@ struct gfs_ctx {
   DevGlobals* d_g = nullptr;
   uint8_t* d_landing = nullptr;
   unsigned long long* d_doorbell = nullptr;
-  int32_t* d_ring_owner = nullptr;
-  unsigned long long* d_cta_wait = nullptr;
+  unsigned long long* d_done_pos = nullptr;
   long long* d_stats = nullptr;
   unsigned long long* d_scratch = nullptr;
   unsigned long long* h_served = nullptr;  // mapped: requests completed by the daemon
@@ -234,11 +233,17 @@ static void worker_main(gfs_ctx* ctx, int wid) {
     // count it before completing: a launch that starts after this completion must see it
     __atomic_fetch_add(ctx->h_served, 1ull, __ATOMIC_SEQ_CST);
     if (ctx->cfg.transfer == GFS_XFER_DMA) {
+      cudaError_t ce = cudaSuccess;
       if (n > 0)
-        cudaMemcpyAsync(ctx->d_landing + (int64_t)slot * ctx->slot_bytes, stg, (size_t)n,
-                        cudaMemcpyHostToDevice, st);
+        ce = cudaMemcpyAsync(ctx->d_landing + (int64_t)slot * ctx->slot_bytes, stg, (size_t)n,
+                             cudaMemcpyHostToDevice, st);
+      if (ce != cudaSuccess) {
+        ctx->worker_error.store(EIO);
+        n = -EIO;
+      }
       uint64_t v = ((uint64_t)(n < 0 ? 0xFFFFFFFFull : (uint64_t)n) << 32) | seq;
-      ctx->write_value64((CUstream)st, (CUdeviceptr)(ctx->d_doorbell + slot), (cuuint64_t)v, 0);
+      CUresult cr = ctx->write_value64((CUstream)st, (CUdeviceptr)(ctx->d_doorbell + slot), (cuuint64_t)v, 0);
+      if (cr != CUDA_SUCCESS) ctx->worker_error.store(EIO);
     } else {
       RpcResp* r = &ctx->h_resp[slot];
       r->nbytes = n;
@@ -268,7 +273,7 @@ static void free_all(gfs_ctx* ctx) {
     if (s) cudaStreamDestroy(s);
   void* dev[] = {ctx->d_frames, ctx->d_fkey, ctx->d_fstate, ctx->d_own_q, ctx->d_retired,
                  ctx->d_gfifo, ctx->d_recycled, ctx->d_g, ctx->d_landing, ctx->d_doorbell,
-                 ctx->d_ring_owner, ctx->d_cta_wait, ctx->d_stats, ctx->d_scratch};
+                 ctx->d_done_pos, ctx->d_stats, ctx->d_scratch};
   for (void* p : dev)
     if (p) cudaFree(p);
   ctx->d_segs.release();
@@ -365,8 +370,7 @@ extern "C" int gfs_create(const gfs_config* cfg_in, gfs_ctx** out) {
       TRY(cudaMalloc(&ctx->d_gfifo, (size_t)ctx->gfifo_cap * 4));
   }
   TRY(cudaMalloc(&ctx->d_g, sizeof(DevGlobals)));
-  TRY(cudaMalloc(&ctx->d_ring_owner, (size_t)ctx->ring_size * 4));
-  TRY(cudaMalloc(&ctx->d_cta_wait, (size_t)ctx->n_ctas * 8));
+  TRY(cudaMalloc(&ctx->d_done_pos, (size_t)ctx->ring_size * 8));
   TRY(cudaMalloc(&ctx->d_stats, (size_t)ctx->n_ctas * GFS_NSTATS * 8));
   TRY(cudaMalloc(&ctx->d_scratch, 64));
   TRY(cudaHostAlloc(&ctx->h_ring, (size_t)ctx->ring_size * sizeof(RpcReq),
@@ -576,9 +580,8 @@ extern "C" int gfs_run(gfs_ctx* ctx, const gfs_program* prog, void* dst, uint64_
     if (ctx->d_gfifo) CUDA_TRY(cudaMemsetAsync(ctx->d_gfifo, 0, (size_t)ctx->gfifo_cap * 4, ctx->stream));
   }
   CUDA_TRY(cudaMemsetAsync(ctx->d_g, 0, sizeof(DevGlobals), ctx->stream));
-  CUDA_TRY(cudaMemsetAsync(ctx->d_cta_wait, 0, (size_t)ctx->n_ctas * 8, ctx->stream));
   CUDA_TRY(cudaMemsetAsync(ctx->d_stats, 0, (size_t)ctx->n_ctas * GFS_NSTATS * 8, ctx->stream));
-  CUDA_TRY(cudaMemsetAsync(ctx->d_ring_owner, 0, (size_t)ctx->ring_size * 4, ctx->stream));
+  CUDA_TRY(cudaMemsetAsync(ctx->d_done_pos, 0, (size_t)ctx->ring_size * 8, ctx->stream));
 
   DevCtx c{};
   c.page_size = cfg.page_size;
@@ -623,8 +626,7 @@ extern "C" int gfs_run(gfs_ctx* ctx, const gfs_program* prog, void* dst, uint64_
   c.staging = ctx->h_staging;
   c.landing = ctx->d_landing;
   c.doorbell = ctx->d_doorbell;
-  c.ring_owner = ctx->d_ring_owner;
-  c.cta_wait = ctx->d_cta_wait;
+  c.done_pos = ctx->d_done_pos;
   c.stats = ctx->d_stats;
   for (int k = 0; k < 4; k++) {
     c.logs[k] = ctx->d_logs[k].p;

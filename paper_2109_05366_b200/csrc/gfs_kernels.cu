@@ -94,6 +94,7 @@ struct Smem {
   int64_t src_off;  // offset of the page inside the span buffer
   int64_t k;        // dispatcher ticket
   int any_bad;
+  uint64_t t_copy0;
   // TB state (thread 0)
   int tb;
   int64_t own_head, own_len;
@@ -432,18 +433,16 @@ __device__ __forceinline__ void account_transfer(const DevCtx& c, Smem& s, int64
 __device__ int64_t rpc_call(const DevCtx& c, Smem& s, int64_t fid, int64_t off, int64_t size) {
   const unsigned slot = blockIdx.x;
   const unsigned long long Q = (unsigned long long)c.ring_mask + 1;
-  unsigned long long pos = c.g->req_base + atomicAdd(&c.g->req_local, 1ull);
+  const unsigned long long local = atomicAdd(&c.g->req_local, 1ull);
+  const unsigned long long pos = c.g->req_base + local;
   uint64_t t0 = globaltimer();
-  if (pos >= Q) {  // the entry Q positions back must have been taken by a worker
-    unsigned long long j = pos - Q;
-    int owner = *(volatile int32_t*)&c.ring_owner[j & c.ring_mask];
-    while (ld_volatile_u64(&c.cta_wait[owner]) == j + 1) {
+  if (local >= Q) {  // ring position pos - Q (same entry) must have completed, i.e. been read
+    const unsigned long long need = pos - Q + 1;
+    while (ld_volatile_u64(&c.done_pos[pos & c.ring_mask]) < need) {
       if (!keep_waiting(c, t0, 20)) return -1;
-      __nanosleep(500);
+      __nanosleep(200);
     }
   }
-  c.ring_owner[pos & c.ring_mask] = (int32_t)slot;
-  *(volatile unsigned long long*)&c.cta_wait[slot] = pos + 1;
   __threadfence();
   RpcReq* e = &c.ring[pos & c.ring_mask];
   volatile RpcReq* ve = e;
@@ -455,6 +454,7 @@ __device__ int64_t rpc_call(const DevCtx& c, Smem& s, int64_t fid, int64_t off, 
   const uint32_t seq = (uint32_t)(pos + 1);
   __threadfence_system();
   st_release_sys(&e->seq, seq);
+  const uint64_t tw = globaltimer();
   int64_t n;
   if (c.transfer == GFS_XFER_DMA) {
     const unsigned long long* bell = &c.doorbell[slot];
@@ -465,7 +465,10 @@ __device__ int64_t rpc_call(const DevCtx& c, Smem& s, int64_t fid, int64_t off, 
         if (n == 0xFFFFFFFFll) n = -1;
         break;
       }
-      if (!keep_waiting(c, t0, 21)) return -1;
+      if (!keep_waiting(c, t0, 21)) {
+        c.g->error_arg = ((unsigned long long)slot << 32) | seq;
+        return -1;
+      }
       __nanosleep(256);
     }
   } else {
@@ -476,11 +479,15 @@ __device__ int64_t rpc_call(const DevCtx& c, Smem& s, int64_t fid, int64_t off, 
         n = *(volatile const int64_t*)&r->nbytes;
         break;
       }
-      if (!keep_waiting(c, t0, 22)) return -1;
+      if (!keep_waiting(c, t0, 22)) {
+        c.g->error_arg = ((unsigned long long)slot << 32) | seq;
+        return -1;
+      }
       __nanosleep(4000);
     }
   }
-  *(volatile unsigned long long*)&c.cta_wait[slot] = 0;
+  atomicMax(&c.done_pos[pos & c.ring_mask], pos + 1);
+  ST(wait_ns) += (long long)(globaltimer() - tw);
   if (n < 0) {
     set_error(c, ERR_IO, (int)fid, (unsigned long long)off);
     return -1;
@@ -628,6 +635,7 @@ __device__ int64_t gread(const DevCtx& c, Smem& s, int64_t fid, int64_t offset, 
       ST(pc_lookups)++;
       bool pending = false;
       uint64_t t0 = globaltimer();
+      const long long wait0 = ST(wait_ns);
       uint32_t f = PT_EMPTY;
       bool miss = false;
       for (;;) {
@@ -692,6 +700,9 @@ __device__ int64_t gread(const DevCtx& c, Smem& s, int64_t fid, int64_t offset, 
       if (has_error(c)) act = A_ABORT;
       s.act = act;
       s.frame = f;
+      const uint64_t t1 = globaltimer();
+      ST(meta_ns) += (long long)(t1 - t0) - (ST(wait_ns) - wait0);
+      s.t_copy0 = t1;
     }
     __syncthreads();
     const int act = s.act;
@@ -739,6 +750,7 @@ __device__ int64_t gread(const DevCtx& c, Smem& s, int64_t fid, int64_t offset, 
       __syncthreads();
     }
     if (tid == 0) {  // install (gpu_cache.py:181-189): data first, then VALID, then the PTE
+      ST(copy_ns) += (long long)(globaltimer() - s.t_copy0);
       __threadfence();
       atomicOr(&c.fstate[f], FR_VALID);
       st_release_gpu(&pt[page], f);

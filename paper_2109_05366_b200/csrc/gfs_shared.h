@@ -111,8 +111,7 @@ struct DevCtx {
   uint8_t* landing;          // [n_ctas][slot_bytes]
   unsigned long long* doorbell; // [n_ctas] (nbytes << 32 | seq), written by cuStreamWriteValue64
   // ring reuse guard (device)
-  int32_t* ring_owner;       // [ring_mask + 1]
-  unsigned long long* cta_wait;  // [n_ctas]: ring position the CTA waits on (+1), 0 = none
+  unsigned long long* done_pos;  // [ring_mask + 1]: last completed ring position + 1 per entry
   // counters (device): [n_ctas][GFS_NSTATS]
   long long* stats;
   // logs (device): [cap][width]
