@@ -103,6 +103,17 @@ struct Smem {
   int64_t ra_win, ra_next_fid, ra_next_page;
   int pending_seen;
   long long st[GFS_NSTATS];
+  // batched page walk (gread_batch): one entry per page of the batch
+  struct {
+    int n_empty, k, status, nvict, nret, ret_lane0, own_lane0;
+    int64_t rpc_n;
+    unsigned long long ret_pos;
+    int64_t own_head0, own_tail0;
+    uint32_t frame[32];
+    int32_t nb[32];
+    int64_t src_off[32];
+    int32_t vict[32];  // 1 = frame must be evicted before reuse
+  } b;
   int32_t pb_nb[MAX_PB_ENTRIES];
 };
 
@@ -162,6 +173,15 @@ __device__ bool try_evict(const DevCtx& c, Smem& s, uint32_t v) {
   log_rec(c, GFS_LOG_VICTIMS, s.tb, vfid, vpage, 0);
   ST(victims)++;
   return true;
+}
+
+// Lane-safe variant (no smem counters, no log): returns the victim's key, or ~0 if the
+// frame is referenced / not valid right now.
+__device__ unsigned long long try_unmap(const DevCtx& c, uint32_t v) {
+  if (atomicCAS(&c.fstate[v], FR_VALID, 0u) != FR_VALID) return ~0ull;
+  unsigned long long key = c.fkey[v];
+  atomicCAS(&c.files[key >> 40].pt[key & ((1ull << 40) - 1)], v, PT_EMPTY);
+  return key;
 }
 
 __device__ bool evict_spin(const DevCtx& c, Smem& s, uint32_t v) {
@@ -387,30 +407,38 @@ __device__ int64_t pb_take(Smem& s, int64_t fid, int64_t page) {
 }
 
 // request_span (prefetcher.py:13-25) + the adaptive window (io.readahead=adaptive)
-__device__ int64_t rpc_span(const DevCtx& c, Smem& s, int64_t fid, int64_t page, int64_t seg_end) {
+// Pure part of request_span: the span an RPC at `page` would have, and the adaptive
+// window it implies (no state change).
+__device__ int64_t span_peek(const DevCtx& c, const Smem& s, int64_t fid, int64_t page,
+                             int64_t seg_end, int64_t* new_win) {
   const DevFile& F = c.files[fid];
   const int64_t pg = c.page_size;
-  int64_t off = page * pg;
+  const int64_t off = page * pg;
+  *new_win = s.ra_win;
   if (off >= F.size) return 0;
-  bool ro = F.read_only != 0;
+  const bool ro = F.read_only != 0;
   int64_t want = (ro && c.prefetch_bytes > 0) ? pg + c.prefetch_bytes : pg;
-  bool adaptive = c.readahead == GFS_RA_ADAPTIVE && ro;
-  if (adaptive) {
-    int64_t base = pg + c.prefetch_bytes;
-    if (s.ra_win > 0 && fid == s.ra_next_fid && page == s.ra_next_page) {
-      s.ra_win = 2 * s.ra_win < c.ra_max_bytes ? 2 * s.ra_win : c.ra_max_bytes;
-    } else {
-      s.ra_win = base;
-    }
-    want = s.ra_win;
-    int64_t seg_lim = (seg_end + pg - 1) / pg * pg - off;  // stay inside this TB's segment
+  if (c.readahead == GFS_RA_ADAPTIVE && ro) {
+    const int64_t base = pg + c.prefetch_bytes;
+    int64_t win = base;
+    if (s.ra_win > 0 && fid == s.ra_next_fid && page == s.ra_next_page)
+      win = 2 * s.ra_win < c.ra_max_bytes ? 2 * s.ra_win : c.ra_max_bytes;
+    *new_win = win;
+    want = win;
+    const int64_t seg_lim = (seg_end + pg - 1) / pg * pg - off;  // stay inside this TB's segment
     if (want > seg_lim) want = seg_lim;
     if (want < pg) want = pg;
   }
-  int64_t span = want < F.size - off ? want : F.size - off;
-  if (adaptive) {
+  return want < F.size - off ? want : F.size - off;
+}
+
+__device__ int64_t rpc_span(const DevCtx& c, Smem& s, int64_t fid, int64_t page, int64_t seg_end) {
+  int64_t win;
+  const int64_t span = span_peek(c, s, fid, page, seg_end, &win);
+  if (span > 0 && c.readahead == GFS_RA_ADAPTIVE && c.files[fid].read_only) {
+    s.ra_win = win;
     s.ra_next_fid = fid;
-    s.ra_next_page = page + (span + pg - 1) / pg;
+    s.ra_next_page = page + (span + c.page_size - 1) / c.page_size;
     log_rec(c, GFS_LOG_WINDOWS, s.tb, span, 0, 0);
   }
   return span;
@@ -580,6 +608,416 @@ __device__ int copy_page_in(uint8_t* frame, uint8_t* dst_whole, const uint8_t* s
   return bad;
 }
 
+// ------------------------------------------------------------ batched page walk
+//
+// The cold sequential case — a run of pages none of which is cached — is walked as one
+// batch instead of page by page: warp 0 looks up and claims up to 32 pages at once, thread
+// 0 plans the frame allocations for all of them in page order (the reference's sequence
+// of allocation decisions, gpu_cache.py:104-179), warp 0 evicts the victims in parallel,
+// the whole CTA copies every page span buffer -> frame (+ user buffer) in one pass, and
+// warp 0 installs them.  Every counter, log record and victim is the same as the
+// per-page walk would produce for the same TB; only pages that are hits, in flight or
+// raced by another TB take the per-page path.
+
+__device__ __forceinline__ bool pb_has(const Smem& s, int64_t fid, int64_t page) {
+  const int64_t i = page - s.pb_base;
+  return s.pb_count > 0 && fid == s.pb_fid && i >= 1 && i <= s.pb_count && s.pb_nb[i] > 0;
+}
+
+// Reserve n consecutive log records (one atomic); ~0 when logging is off / full.
+__device__ unsigned long long log_reserve(const DevCtx& c, int kind, int n) {
+  if (!c.log || n <= 0) return ~0ull;
+  unsigned long long b = atomicAdd(&c.g->log_n[kind], (unsigned long long)n);
+  if (b + n > c.log_cap[kind]) {
+    set_error(c, ERR_LOG_OVERFLOW, kind, b);
+    return ~0ull;
+  }
+  return b;
+}
+
+__device__ __forceinline__ void log_put3(const DevCtx& c, int kind, unsigned long long i, long long a,
+                                         long long b, long long d) {
+  long long* r = c.logs[kind] + i * 3;
+  r[0] = a;
+  r[1] = b;
+  r[2] = d;
+}
+
+// per-tb-lra plan for k pages (thread 0); returns how many pages get a frame now.  Fresh
+// frames first, then retired frames of finished TBs, then the TB's own oldest frames —
+// the latter only while they predate this batch (so a batch never recycles itself).
+__device__ int plan_per_tb(const DevCtx& c, Smem& s, int k) {
+  const int64_t len0 = s.own_len;
+  const int a = (int)min((int64_t)k, max((int64_t)0, c.quota - len0));
+  int g = 0;
+  if (a > 0 && ld_volatile_u64(&c.g->fresh_next) < (unsigned long long)c.nframes) {
+    unsigned long long old = atomicAdd(&c.g->fresh_next, (unsigned long long)a);
+    if (old < (unsigned long long)c.nframes)
+      g = (int)min((unsigned long long)a, (unsigned long long)c.nframes - old);
+    for (int j = 0; j < g; j++) s.b.frame[j] = (uint32_t)(old + j);
+  }
+  while (g < a) {  // frames released at EOF (rare)
+    uint32_t f = take_recycled(c);
+    if (f == PT_EMPTY) break;
+    s.b.frame[g++] = f;
+  }
+  for (int j = 0; j < g; j++) s.b.vict[j] = 0;
+  int r = 0;
+  while (g + r < a) {  // retired frames, oldest first: one contiguous range
+    unsigned long long h = ld_volatile_u64(&c.g->ret_head), t = ld_volatile_u64(&c.g->ret_tail);
+    if (h >= t) break;
+    unsigned long long take = t - h < (unsigned long long)(a - g) ? t - h : (unsigned long long)(a - g);
+    if (atomicCAS(&c.g->ret_head, h, h + take) == h) {
+      s.b.ret_pos = h;
+      r = (int)take;
+    }
+  }
+  int hd = k - g - r;  // own-head remaps
+  if (hd > len0) hd = (int)len0;
+  const int kk = g + r + hd;
+  for (int j = g; j < kk; j++) s.b.vict[j] = 1;
+  s.b.nret = r;
+  s.b.ret_lane0 = g;
+  s.b.own_lane0 = g + r;
+  s.b.own_head0 = s.own_head;
+  s.b.own_tail0 = s.own_head + len0;
+  s.b.nvict = r + hd;
+  s.own_head += hd;
+  s.own_len = len0 + g + r;
+  ST(pc_allocs) += g;
+  ST(pc_remaps) += r + hd;
+  return kk;
+}
+
+// global-lru-dealloc plan for k pages (thread 0).  Fresh frames lock-free; victims are the
+// first valid, unreferenced frames of the global allocation-order FIFO, taken under the
+// global lock (gpu_cache.py:126-147).  Victims are unmapped here (vict = 0 afterwards).
+__device__ int plan_global(const DevCtx& c, Smem& s, int k) {
+  int g = 0;
+  if (ld_volatile_u64(&c.g->fresh_next) < (unsigned long long)c.nframes) {
+    unsigned long long old = atomicAdd(&c.g->fresh_next, (unsigned long long)k);
+    if (old < (unsigned long long)c.nframes)
+      g = (int)min((unsigned long long)k, (unsigned long long)c.nframes - old);
+    for (int j = 0; j < g; j++) s.b.frame[j] = (uint32_t)(old + j);
+  }
+  while (g < k) {
+    uint32_t f = take_recycled(c);
+    if (f == PT_EMPTY) break;
+    s.b.frame[g++] = f;
+  }
+  if (g > 0) {
+    unsigned long long pos = atomicAdd(&c.g->g_tail, (unsigned long long)g);
+    if (pos + g - ld_volatile_u64(&c.g->g_head) >= (unsigned long long)c.gfifo_cap) {
+      set_error(c, ERR_FIFO_OVERFLOW, 0, pos);
+      return 0;
+    }
+    for (int j = 0; j < g; j++) st_release_gpu(&c.gfifo[(pos + j) % c.gfifo_cap], s.b.frame[j] + 1);
+    s.last_gfifo_pos = (long long)(pos + g - 1);
+  }
+  ST(pc_allocs) += g;
+  int found = 0;
+  if (g < k) {
+    uint64_t t0 = globaltimer();
+    while (atomicCAS(&c.g->lock, 0, 1) != 0) {
+      if (!keep_waiting(c, t0, 15)) return 0;
+      __nanosleep(64);
+    }
+    __threadfence();
+    unsigned long long head = c.g->g_head;
+    const unsigned long long tail = ld_volatile_u64(&c.g->g_tail);
+    for (unsigned long long p = head; p < tail && g + found < k; p++) {
+      uint32_t* e = &c.gfifo[p % c.gfifo_cap];
+      uint32_t val;
+      while ((val = ld_acquire_gpu(e)) == 0) {  // reserved, not yet written
+        if (!keep_waiting(c, t0, 16)) break;
+      }
+      if (val == 0) break;
+      if (val == RING_TOMB) continue;
+      unsigned long long key = try_unmap(c, val - 1);
+      if (key == ~0ull) continue;  // in flight or referenced: skipped (gpu_cache.py:133-137)
+      *e = RING_TOMB;
+      s.b.frame[g + found] = val - 1;
+      log_rec(c, GFS_LOG_VICTIMS, s.tb, (long long)(key >> 40), (long long)(key & ((1ull << 40) - 1)), 0);
+      found++;
+    }
+    while (head < tail && *(volatile uint32_t*)&c.gfifo[head % c.gfifo_cap] == RING_TOMB) {
+      c.gfifo[head % c.gfifo_cap] = 0;
+      head++;
+    }
+    c.g->g_head = head;
+    __threadfence();
+    atomicExch(&c.g->lock, 0);
+    if (found > 0) {
+      unsigned long long pos = atomicAdd(&c.g->g_tail, (unsigned long long)found);
+      for (int j = 0; j < found; j++)
+        st_release_gpu(&c.gfifo[(pos + j) % c.gfifo_cap], s.b.frame[g + j] + 1);
+      s.last_gfifo_pos = (long long)(pos + found - 1);
+    }
+    ST(pc_evictions) += found;
+    ST(pc_allocs) += found;
+    ST(victims) += found;
+  }
+  for (int j = 0; j < g + found; j++) s.b.vict[j] = 0;
+  s.b.nvict = 0;
+  return g + found;
+}
+
+// One batch of cold pages starting at g_pos (all threads).  Returns delivered bytes,
+// 0 = not applicable (the caller takes the per-page path), -1 = abort.
+template <int BS>
+__device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_pos, int64_t g_end,
+                               int64_t seg_end, uint8_t* d0, int& bad_words, const uint8_t* span_buf) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  const bool w0 = tid < 32;
+  const DevFile& F = c.files[fid];
+  const int64_t pg = c.page_size, fs = F.size;
+  const int64_t p0 = g_pos / pg;
+  const int64_t lim = g_end < fs ? g_end : fs;
+  int nmax = (int)min((int64_t)32, (lim + pg - 1) / pg - p0);
+  if (c.policy == GFS_POLICY_GLOBAL_LRU) nmax = (int)min((int64_t)nmax, max((int64_t)1, c.nframes / 4));
+  uint32_t* pt = F.pt;
+  uint64_t t_start = 0;
+  if (tid == 0) t_start = globaltimer();
+
+  // (A) warp 0: look up and claim the leading run of uncached pages
+  if (w0) {
+    bool ok = lane < nmax && ld_acquire_gpu(&pt[p0 + lane]) == PT_EMPTY;
+    unsigned m = __ballot_sync(0xffffffffu, ok);
+    int run = (~m == 0u) ? 32 : __ffs(~m) - 1;
+    ok = lane < run && atomicCAS(&pt[p0 + lane], PT_EMPTY, PT_CLAIMED) == PT_EMPTY;
+    unsigned got = __ballot_sync(0xffffffffu, ok);
+    int kc = (~got == 0u) ? 32 : __ffs(~got) - 1;
+    if (ok && lane >= kc) st_release_gpu(&pt[p0 + lane], PT_EMPTY);  // beyond a raced page
+    if (lane == 0) s.b.n_empty = kc;
+  }
+  __syncthreads();
+  const int kc = s.b.n_empty;
+  if (kc < 1) return 0;
+
+  // (B) thread 0: how many of them this batch can serve, and their frames
+  if (tid == 0) {
+    int kp = 1;
+    if (pb_has(s, fid, p0)) {
+      while (kp < kc && pb_has(s, fid, p0 + kp)) kp++;
+    } else {
+      int64_t win;
+      const int64_t span = span_peek(c, s, fid, p0, seg_end, &win);
+      int64_t m = (span + pg - 1) / pg;                        // pages the RPC brings
+      if (m - 1 > c.pb_cap_bytes / pg) m = 1 + c.pb_cap_bytes / pg;  // private-buffer room
+      kp = (int)min((int64_t)kc, max((int64_t)1, m));
+    }
+    int kk = c.policy == GFS_POLICY_GLOBAL_LRU ? plan_global(c, s, kp) : plan_per_tb(c, s, kp);
+    if (has_error(c)) kk = 0;
+    s.b.k = kk;
+  }
+  __syncthreads();
+  const int kk = s.b.k;
+  if (w0 && lane < kc && lane >= kk) st_release_gpu(&pt[p0 + lane], PT_EMPTY);  // not this batch
+  if (kk < 1) {
+    __syncthreads();
+    return has_error(c) ? -1 : 0;
+  }
+
+  // (C) warp 0: victims (own-head / retired frames) and the own-queue update
+  if (w0 && c.policy == GFS_POLICY_PER_TB_LRA) {
+    const unsigned long long cap = 2ull * (unsigned long long)c.nframes;
+    uint32_t f = PT_EMPTY;
+    bool abort = false;
+    if (lane < kk && s.b.vict[lane]) {
+      if (lane < s.b.own_lane0) {  // retired range
+        uint32_t* e = &c.retired[(s.b.ret_pos + (lane - s.b.ret_lane0)) % cap];
+        uint64_t t0 = globaltimer();
+        uint32_t v;
+        while ((v = ld_acquire_gpu(e)) == 0) {
+          if (!keep_waiting(c, t0, 11)) break;
+        }
+        *e = 0;
+        f = v - 1;
+        abort = v == 0;
+      } else {  // own oldest frames
+        f = c.own_q[(int64_t)blockIdx.x * c.quota + (s.b.own_head0 + (lane - s.b.own_lane0)) % c.quota];
+      }
+    }
+    __syncwarp();
+    if (lane < kk && s.b.vict[lane]) {
+      if (!abort) s.b.frame[lane] = f;
+      unsigned long long key = ~0ull;
+      uint64_t t0 = globaltimer();
+      while (!abort && (key = try_unmap(c, f)) == ~0ull) {  // wait out transient readers
+        if (!keep_waiting(c, t0, 10)) {
+          abort = true;
+          break;
+        }
+        __nanosleep(100);
+      }
+      s.b.src_off[lane] = (long long)key;  // scratch: victim key for the log below
+    }
+    __syncwarp();
+    const int nv = s.b.nvict;
+    unsigned long long base = 0;
+    if (lane == 0) base = log_reserve(c, GFS_LOG_VICTIMS, nv);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (base != ~0ull && lane < kk && s.b.vict[lane]) {
+      const unsigned long long key = (unsigned long long)s.b.src_off[lane];
+      log_put3(c, GFS_LOG_VICTIMS, base + (lane - s.b.ret_lane0), s.tb, (long long)(key >> 40),
+               (long long)(key & ((1ull << 40) - 1)));
+    }
+    if (lane == 0) ST(victims) += nv;
+    if (lane < kk)  // pushes at the tail, in page order
+      c.own_q[(int64_t)blockIdx.x * c.quota + (s.b.own_tail0 + lane) % c.quota] = s.b.frame[lane];
+  }
+  __syncthreads();
+  if (has_error(c)) return -1;
+
+  // (D) thread 0: lookups/misses, the private-buffer walk and the RPC (prefetcher.py)
+  if (tid == 0) {
+    int status = 0;
+    for (int j = 0; j < kk; j++) {
+      ST(pc_lookups)++;
+      ST(pc_misses)++;
+      const int64_t page = p0 + j;
+      int64_t nb = pb_take(s, fid, page);
+      if (nb > 0) {
+        s.b.nb[j] = (int32_t)nb;
+        s.b.src_off[j] = (page - s.pb_base) * pg;
+        continue;
+      }
+      if (j > 0) {  // planned as a private-buffer page but absent: file shrank under us
+        set_error(c, ERR_IO, (int)fid, (unsigned long long)page);
+        status = 2;
+        break;
+      }
+      const int64_t span = rpc_span(c, s, fid, page, seg_end);
+      const int64_t n = span > 0 ? rpc_call(c, s, fid, page * pg, span) : 0;
+      if (n < 0) {
+        status = 2;
+        break;
+      }
+      log_rec(c, GFS_LOG_RPCS, s.tb, fid, page * pg, span);
+      ST(rpc_count)++;
+      ST(rpc_requested_bytes) += span;
+      account_transfer(c, s, n);
+      if (n == 0) {
+        set_error(c, ERR_IO, (int)fid, (unsigned long long)page);
+        status = 2;
+        break;
+      }
+      const int64_t nb0 = n < pg ? n : pg;
+      s.b.nb[0] = (int32_t)nb0;
+      s.b.src_off[0] = 0;
+      const int64_t m = (n + pg - 1) / pg;
+      if (m > 1) pb_fill(c, s, fid, page, m, n - nb0);
+    }
+    s.b.status = status;
+    // bind frames to their pages (installed below)
+    if (status == 0)
+      for (int j = 0; j < kk; j++) c.fkey[s.b.frame[j]] = page_key(fid, p0 + j);
+    const uint64_t t1 = globaltimer();
+    ST(meta_ns) += (long long)(t1 - t_start);
+    s.t_copy0 = t1;
+  }
+  __syncthreads();
+  if (s.b.status != 0) return -1;
+
+  // (E) all threads: K1 over the whole batch — span buffer -> frames (+ user buffer)
+  const int64_t vpp = pg >> 4;  // 16-byte vectors per page
+  const int64_t nvec = (int64_t)kk * vpp;
+  const int64_t in0 = g_pos - p0 * pg;
+  const bool dst_ok = d0 != nullptr && ((((uintptr_t)d0 - (uintptr_t)in0)) & 15) == 0;
+  const bool chk = c.verify && F.content_id >= 0;
+  const int64_t cid = F.content_id;
+  int bad = 0;
+  const uint4* src4 = (const uint4*)(span_buf + s.b.src_off[0]);  // pages are consecutive
+  const bool contiguous = s.b.src_off[kk - 1] == s.b.src_off[0] + (int64_t)(kk - 1) * pg;
+  for (int64_t v0 = tid; v0 < nvec; v0 += 4 * BS) {
+    uint4 q[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const int64_t v = v0 + u * BS;
+      if (v < nvec) {
+        const int j = (int)(v / vpp);
+        const int64_t w = v - (int64_t)j * vpp;
+        const uint4* sp = contiguous ? src4 + v : (const uint4*)(span_buf + s.b.src_off[j]) + w;
+        q[u] = (w << 4) < s.b.nb[j] ? (c.transfer == GFS_XFER_DMA ? ld16<SRC_HBM>(sp) : ld16<SRC_SYS>(sp))
+                                    : make_uint4(0, 0, 0, 0);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const int64_t v = v0 + u * BS;
+      if (v >= nvec) break;
+      const int j = (int)(v / vpp);
+      const int64_t w = v - (int64_t)j * vpp;
+      const int64_t nbj = s.b.nb[j];
+      if ((w << 4) + 16 > nbj) continue;  // sub-16 B EOF tail: byte loop below
+      ((uint4*)(c.frames + (int64_t)s.b.frame[j] * pg))[w] = q[u];
+      // whole-page deliveries go straight to the user buffer in the same pass
+      const int64_t ps = (p0 + j) * pg;
+      if (dst_ok && ps >= g_pos && ps + nbj <= g_end)
+        ((uint4*)(d0 + (ps - g_pos)))[w] = q[u];
+      if (chk) {
+        const int64_t wi = (ps >> 3) + 2 * w;
+        const uint64_t lo = ((uint64_t)q[u].y << 32) | q[u].x, hi = ((uint64_t)q[u].w << 32) | q[u].z;
+        bad += (lo != word_law(cid, wi)) + (hi != word_law(cid, wi + 1));
+      }
+    }
+  }
+  for (int j = 0; j < kk; j++) {  // EOF page tails that are not a multiple of 16 bytes
+    const int64_t nbj = s.b.nb[j];
+    if ((nbj & 15) == 0) continue;
+    const uint8_t* sp = span_buf + s.b.src_off[j];
+    uint8_t* fp = c.frames + (int64_t)s.b.frame[j] * pg;
+    for (int64_t i = (nbj & ~(int64_t)15) + tid; i < nbj; i += BS) {
+      const uint8_t b = c.transfer == GFS_XFER_DMA ? ld1<SRC_HBM>(sp + i) : ld1<SRC_SYS>(sp + i);
+      fp[i] = b;
+      if (chk) {
+        const int64_t fo = (p0 + j) * pg + i;
+        bad += b != (uint8_t)(word_law(cid, fo >> 3) >> (8 * (fo & 7)));
+      }
+    }
+  }
+  bad_words += bad;
+  const int any_bad = __syncthreads_or(bad);
+  // partial deliveries (first page entered mid-page, last page cut by the request, EOF
+  // tails, misaligned user buffers) from the frames just written
+  int64_t total = 0;
+  for (int j = 0; j < kk; j++) {
+    const int64_t ps = (p0 + j) * pg, nbj = s.b.nb[j];
+    const int64_t lo = ps > g_pos ? ps : g_pos;
+    const int64_t hi = ps + nbj < g_end ? ps + nbj : g_end;
+    const int64_t want = hi - lo;
+    total += want;
+    const bool whole = dst_ok && ps >= g_pos && ps + nbj <= g_end && (nbj & 15) == 0;
+    if (d0 && !whole) copy_bytes<BS, SRC_HBM>(d0 + (lo - g_pos), c.frames + (int64_t)s.b.frame[j] * pg + (lo - ps), want);
+  }
+  __syncthreads();
+
+  // (F) warp 0: install (data, then VALID, then the page-table entry) and deliveries
+  if (w0) {
+    if (lane == 0) {
+      const uint64_t t_in = globaltimer();
+      ST(copy_ns) += (long long)(t_in - s.t_copy0);
+      s.t_copy0 = t_in;
+    }
+    __threadfence();
+    if (lane < kk) {
+      atomicOr(&c.fstate[s.b.frame[lane]], FR_VALID);
+      st_release_gpu(&pt[p0 + lane], s.b.frame[lane]);
+    }
+    unsigned long long base = 0;
+    if (lane == 0) base = log_reserve(c, GFS_LOG_DELIVERIES, kk);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (base != ~0ull && lane < kk) log_put3(c, GFS_LOG_DELIVERIES, base + lane, s.tb, fid, p0 + lane);
+    if (lane == 0) {
+      ST(user_bytes) += total;
+      if (any_bad) ST(tag_mismatches)++;
+      ST(install_ns) += (long long)(globaltimer() - s.t_copy0);
+    }
+  }
+  __syncthreads();
+  return total;
+}
+
 // ----------------------------------------------------------------- gread (all threads)
 
 // One gread of `size` bytes at `offset` of `fid` (gpu_exec.py:107-239).  `dst` is the
@@ -630,6 +1068,16 @@ __device__ int64_t gread(const DevCtx& c, Smem& s, int64_t fid, int64_t offset, 
     const int64_t in_page = g_pos - page * pg;
     const unsigned long long key = page_key(fid, page);
 
+    {  // cold run of pages: batched walk
+      const int64_t got = gread_batch<BS>(c, s, fid, g_pos, g_end, seg_end,
+                                          dst ? dst + (g_pos - offset) : nullptr, bad_words, span_buf);
+      if (got < 0) return -1;
+      if (got > 0) {
+        g_pos += got;
+        continue;
+      }
+    }
+
     if (tid == 0) {  // ---- decide (gpu_exec.py:142-199) ----
       int act = A_ABORT;
       ST(pc_lookups)++;
@@ -672,7 +1120,10 @@ __device__ int64_t gread(const DevCtx& c, Smem& s, int64_t fid, int64_t offset, 
       }
       if (miss) {
         ST(pc_misses)++;
+        const uint64_t ta = globaltimer();
+        ST(lookup_ns) += (long long)(ta - t0);
         f = c.policy == GFS_POLICY_GLOBAL_LRU ? alloc_global(c, s) : alloc_per_tb(c, s);
+        ST(alloc_ns) += (long long)(globaltimer() - ta);
         if (f != PT_EMPTY) {
           c.fkey[f] = key;
           st_release_gpu(&pt[page], f | PT_INFLIGHT);
@@ -750,7 +1201,8 @@ __device__ int64_t gread(const DevCtx& c, Smem& s, int64_t fid, int64_t offset, 
       __syncthreads();
     }
     if (tid == 0) {  // install (gpu_cache.py:181-189): data first, then VALID, then the PTE
-      ST(copy_ns) += (long long)(globaltimer() - s.t_copy0);
+      const uint64_t t_in = globaltimer();
+      ST(copy_ns) += (long long)(t_in - s.t_copy0);
       __threadfence();
       atomicOr(&c.fstate[f], FR_VALID);
       st_release_gpu(&pt[page], f);
@@ -761,6 +1213,7 @@ __device__ int64_t gread(const DevCtx& c, Smem& s, int64_t fid, int64_t offset, 
       }
       ST(user_bytes) += want;
       log_rec(c, GFS_LOG_DELIVERIES, s.tb, fid, page, 0);
+      ST(install_ns) += (long long)(globaltimer() - t_in);
     }
     g_pos += want;
     __syncthreads();
@@ -826,7 +1279,7 @@ __device__ bool run_tb(const DevCtx& c, Smem& s, int tb, int& bad_words) {
 }
 
 template <int BS>
-__global__ void __launch_bounds__(BS, 1024 / BS) gread_driver(DevCtx c) {
+__global__ void __launch_bounds__(BS, 4) gread_driver(DevCtx c) {
   __shared__ Smem s;
   const int tid = threadIdx.x;
   if (tid == 0) {
