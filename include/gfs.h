@@ -87,7 +87,8 @@ typedef struct gfs_program {
   X(pb_misses) X(pb_filled_bytes) X(pb_consumed_bytes) X(pb_discarded_bytes) X(rpc_count)    \
   X(rpc_requested_bytes) X(slot_collisions) X(preads) X(pread_bytes) X(storage_bytes)       \
   X(pcie_bytes) X(pcie_transfers) X(victims) X(kernel_ns) X(wall_ns) X(ctas) X(word_mismatches) \
-  X(wait_ns) X(meta_ns) X(copy_ns) X(lookup_ns) X(alloc_ns) X(install_ns)
+  X(wait_ns) X(meta_ns) X(copy_ns) X(lookup_ns) X(alloc_ns) X(install_ns) X(host_pread_ns) \
+  X(host_idle_ns) X(host_xfer_ns) X(host_requests) X(io_workers)
 
 enum {
 #define GFS_X(name) GFS_STAT_##name,

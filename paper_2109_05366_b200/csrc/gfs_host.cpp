@@ -159,7 +159,14 @@ struct gfs_ctx {
   // daemon
   std::vector<std::thread> workers;
   std::vector<cudaStream_t> worker_streams;
+  // DMA mode: per-worker pinned bounce buffers, few and small enough to stay resident in
+  // the host LLC (pread writes them, the copy engine reads them right after)
+  int nbounce = 0;
+  uint8_t* h_bounce = nullptr;
+  std::vector<cudaEvent_t> bounce_ev;  // [io_workers * nbounce]
   std::atomic<uint64_t> req_head{0};
+  // daemon accounting for the current run (ns summed over workers)
+  std::atomic<int64_t> t_pread{0}, t_idle{0}, t_xfer{0}, n_served{0};
   std::atomic<bool> stop{false};
   std::atomic<int> worker_error{0};
   bool has_run = false;
@@ -203,13 +210,16 @@ static int64_t do_pread(gfs_ctx* ctx, const HostFile& f, int64_t off, int64_t si
 
 static void worker_main(gfs_ctx* ctx, int wid) {
   const uint32_t mask = ctx->ring_size - 1;
-  cudaStream_t st = ctx->cfg.transfer == GFS_XFER_DMA ? ctx->worker_streams[wid] : nullptr;
-  if (st) cudaSetDevice(ctx->cfg.device);
+  const bool dma = ctx->cfg.transfer == GFS_XFER_DMA;
+  cudaStream_t st = dma ? ctx->worker_streams[wid] : nullptr;
+  if (dma) cudaSetDevice(ctx->cfg.device);
+  uint64_t nreq = 0;
   while (!ctx->stop.load(std::memory_order_relaxed)) {
     uint64_t h = ctx->req_head.fetch_add(1, std::memory_order_relaxed);
     RpcReq* e = &ctx->h_ring[h & mask];
     const uint32_t seq = (uint32_t)(h + 1);
     uint64_t spins = 0;
+    const uint64_t t_wait = now_ns();
     while (__atomic_load_n(&e->seq, __ATOMIC_ACQUIRE) != seq) {
       if (ctx->stop.load(std::memory_order_relaxed)) return;
       if (++spins < 20000) {
@@ -219,24 +229,39 @@ static void worker_main(gfs_ctx* ctx, int wid) {
         nanosleep(&ts, nullptr);
       }
     }
+    const uint64_t t0 = now_ns();
+    ctx->t_idle.fetch_add((int64_t)(t0 - t_wait), std::memory_order_relaxed);
     const int64_t off = e->offset, size = e->size;
     const int fid = e->fid, slot = e->slot;
     int64_t n;
-    uint8_t* stg = ctx->h_staging + (int64_t)slot * ctx->slot_bytes;
+    uint8_t* buf;
+    int b = 0;
+    if (dma) {  // next bounce buffer of this worker, once its previous copy has drained
+      b = wid * ctx->nbounce + (int)(nreq % (uint64_t)ctx->nbounce);
+      if (nreq >= (uint64_t)ctx->nbounce) cudaEventSynchronize(ctx->bounce_ev[b]);
+      buf = ctx->h_bounce + (int64_t)b * ctx->slot_bytes;
+    } else {
+      buf = ctx->h_staging + (int64_t)slot * ctx->slot_bytes;
+    }
+    nreq++;
     if (slot < 0 || slot >= ctx->n_ctas || fid < 0 || fid >= (int)ctx->files.size() ||
         !ctx->files[fid].open || size > ctx->slot_bytes) {
       n = -EINVAL;
     } else {
-      n = do_pread(ctx, ctx->files[fid], off, size, stg);
+      n = do_pread(ctx, ctx->files[fid], off, size, buf);
     }
+    const uint64_t t1 = now_ns();
+    ctx->t_pread.fetch_add((int64_t)(t1 - t0), std::memory_order_relaxed);
     if (n < 0) ctx->worker_error.store((int)-n);
     // count it before completing: a launch that starts after this completion must see it
     __atomic_fetch_add(ctx->h_served, 1ull, __ATOMIC_SEQ_CST);
-    if (ctx->cfg.transfer == GFS_XFER_DMA) {
+    if (dma) {
       cudaError_t ce = cudaSuccess;
-      if (n > 0)
-        ce = cudaMemcpyAsync(ctx->d_landing + (int64_t)slot * ctx->slot_bytes, stg, (size_t)n,
+      if (n > 0) {
+        ce = cudaMemcpyAsync(ctx->d_landing + (int64_t)slot * ctx->slot_bytes, buf, (size_t)n,
                              cudaMemcpyHostToDevice, st);
+        if (ce == cudaSuccess) ce = cudaEventRecord(ctx->bounce_ev[b], st);
+      }
       if (ce != cudaSuccess) {
         ctx->worker_error.store(EIO);
         n = -EIO;
@@ -244,11 +269,13 @@ static void worker_main(gfs_ctx* ctx, int wid) {
       uint64_t v = ((uint64_t)(n < 0 ? 0xFFFFFFFFull : (uint64_t)n) << 32) | seq;
       CUresult cr = ctx->write_value64((CUstream)st, (CUdeviceptr)(ctx->d_doorbell + slot), (cuuint64_t)v, 0);
       if (cr != CUDA_SUCCESS) ctx->worker_error.store(EIO);
+      ctx->t_xfer.fetch_add((int64_t)(now_ns() - t1), std::memory_order_relaxed);
     } else {
       RpcResp* r = &ctx->h_resp[slot];
       r->nbytes = n;
       __atomic_store_n(&r->seq, seq, __ATOMIC_RELEASE);
     }
+    ctx->n_served.fetch_add(1, std::memory_order_relaxed);
   }
 }
 
@@ -283,7 +310,9 @@ static void free_all(gfs_ctx* ctx) {
   ctx->d_order.release();
   ctx->d_files.release();
   for (auto& l : ctx->d_logs) l.release();
-  void* host[] = {ctx->h_ring, ctx->h_resp, ctx->h_staging, ctx->h_served};
+  for (auto ev : ctx->bounce_ev)
+    if (ev) cudaEventDestroy(ev);
+  void* host[] = {ctx->h_ring, ctx->h_resp, ctx->h_staging, ctx->h_served, ctx->h_bounce};
   for (void* p : host)
     if (p) cudaFreeHost(p);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
@@ -377,8 +406,9 @@ extern "C" int gfs_create(const gfs_config* cfg_in, gfs_ctx** out) {
                     cudaHostAllocMapped | cudaHostAllocPortable));
   TRY(cudaHostAlloc(&ctx->h_resp, (size_t)ctx->n_ctas * sizeof(RpcResp),
                     cudaHostAllocMapped | cudaHostAllocPortable));
-  TRY(cudaHostAlloc(&ctx->h_staging, (size_t)(ctx->n_ctas * ctx->slot_bytes),
-                    cudaHostAllocMapped | cudaHostAllocPortable));
+  if (cfg.transfer != GFS_XFER_DMA)
+    TRY(cudaHostAlloc(&ctx->h_staging, (size_t)(ctx->n_ctas * ctx->slot_bytes),
+                      cudaHostAllocMapped | cudaHostAllocPortable));
   memset(ctx->h_ring, 0, (size_t)ctx->ring_size * sizeof(RpcReq));
   memset(ctx->h_resp, 0, (size_t)ctx->n_ctas * sizeof(RpcResp));
   TRY(cudaHostAlloc(&ctx->h_served, 64, cudaHostAllocMapped | cudaHostAllocPortable));
@@ -395,6 +425,13 @@ extern "C" int gfs_create(const gfs_config* cfg_in, gfs_ctx** out) {
     ctx->write_value64 = (CUresult(*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int))fn;
     ctx->worker_streams.resize(cfg.io_workers, nullptr);
     for (auto& s : ctx->worker_streams) TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    // ~48 MiB of bounce buffers in total (LLC-sized), at least 2 per worker
+    ctx->nbounce = (int)std::max<int64_t>(2, (48ll << 20) / (ctx->slot_bytes * cfg.io_workers));
+    if (ctx->nbounce > 8) ctx->nbounce = 8;
+    TRY(cudaHostAlloc(&ctx->h_bounce, (size_t)(ctx->slot_bytes * cfg.io_workers * ctx->nbounce),
+                      cudaHostAllocPortable));
+    ctx->bounce_ev.resize((size_t)cfg.io_workers * ctx->nbounce, nullptr);
+    for (auto& ev : ctx->bounce_ev) TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   }
   TRY(cudaDeviceSynchronize());
 #undef TRY
@@ -633,6 +670,10 @@ extern "C" int gfs_run(gfs_ctx* ctx, const gfs_program* prog, void* dst, uint64_
     c.log_cap[k] = ctx->log_cap[k];
   }
   ctx->worker_error.store(0);
+  ctx->t_pread.store(0);
+  ctx->t_idle.store(0);
+  ctx->t_xfer.store(0);
+  ctx->n_served.store(0);
   if (prog->n_tb > 0) {
     CUDA_TRY(cudaEventRecord(ctx->ev0, ctx->stream));
     CUDA_TRY(launch_gread(c, cfg.cta_threads, ctx->stream));
@@ -659,6 +700,11 @@ extern "C" int gfs_run(gfs_ctx* ctx, const gfs_program* prog, void* dst, uint64_
     for (int k = 0; k < GFS_NSTATS; k++) out->v[k] += st[(size_t)b * GFS_NSTATS + k];
   out->v[GFS_STAT_kernel_ns] = (int64_t)((double)ms * 1e6);
   out->v[GFS_STAT_ctas] = ctx->n_ctas;
+  out->v[GFS_STAT_host_pread_ns] = ctx->t_pread.load();
+  out->v[GFS_STAT_host_idle_ns] = ctx->t_idle.load();
+  out->v[GFS_STAT_host_xfer_ns] = ctx->t_xfer.load();
+  out->v[GFS_STAT_host_requests] = ctx->n_served.load();
+  out->v[GFS_STAT_io_workers] = ctx->cfg.io_workers;
   for (int k = 0; k < 4; k++) ctx->log_n[k] = std::min(g.log_n[k], ctx->log_cap[k]);
   ctx->has_run = true;
   out->v[GFS_STAT_wall_ns] = (int64_t)(now_ns() - w0);

@@ -45,10 +45,17 @@ def main():
             st = r["stats"][-1]
             ns = st["kernel_ns"]
             cta_ns = ns * r["ctas"]
+            W = st["io_workers"]
             line = {"variant": v or "headline", "gbps": round(st["user_bytes"] / ns, 2),
-                    "rpcs": st["rpc_count"], "wait": round(st["wait_ns"] / cta_ns, 3),
-                    "meta": round(st["meta_ns"] / cta_ns, 3), "copy": round(st["copy_ns"] / cta_ns, 3),
-                    "us_per_rpc_wait": round(st["wait_ns"] / max(1, st["rpc_count"]) / 1e3, 1),
+                    "rpcs": st["rpc_count"],
+                    "cta_wait": round(st["wait_ns"] / cta_ns, 3),
+                    "cta_meta": round(st["meta_ns"] / cta_ns, 3),
+                    "cta_copy": round(st["copy_ns"] / cta_ns, 3),
+                    "us_rpc_wait": round(st["wait_ns"] / max(1, st["rpc_count"]) / 1e3, 1),
+                    "host_pread": round(st["host_pread_ns"] / (W * ns), 3),
+                    "host_xfer": round(st["host_xfer_ns"] / (W * ns), 3),
+                    "host_idle": round(st["host_idle_ns"] / (W * ns), 3),
+                    "us_pread": round(st["host_pread_ns"] / max(1, st["host_requests"]) / 1e3, 1),
                     "mism": r["mismatched_words"], "wall_s": round(time.time() - t0, 1)}
         except Exception as e:
             line = {"variant": v, "error": str(e)[:400]}
