@@ -55,7 +55,7 @@ def headline_overrides(size: int, n_gpus: int, directory: str) -> dict:
         "workload.request_bytes": 64 * KiB, "gpufs.page_size": 4 * KiB,
         "gpufs.prefetch_bytes": 60 * KiB, "gpufs.cache_bytes": 4 * GiB,
         "gpufs.policy": "per-tb-lra", "gpu.sm_count": 148, "gpu.max_threads_per_sm": 2048,
-        "gpu.threads_per_tb": 512, "io.readahead": "adaptive", "io.ra_max_bytes": 2 * MiB,
+        "gpu.threads_per_tb": 512, "io.readahead": "adaptive", "io.ra_max_bytes": 0,
         "io.transfer": "zerocopy", "io.workers": 12, "io.direct": True, "mode.ramfs": True,
         "io.dir": directory, "mode.verify": True,
     }
@@ -402,7 +402,7 @@ def main() -> None:
                    "request": cfg["workload.request_bytes"], "page": cfg["gpufs.page_size"],
                    "prefetch": cfg["gpufs.prefetch_bytes"], "cache": cfg["gpufs.cache_bytes"],
                    "policy": cfg["gpufs.policy"], "readahead": cfg["io.readahead"],
-                   "ra_max": cfg["io.ra_max_bytes"], "transfer": cfg["io.transfer"],
+                   "ra_max": cfg.ra_max(), "transfer": cfg["io.transfer"],
                    "io_workers": cfg.io_workers(), "resident_tbs": cfg.resident_limit(),
                    "resident_ctas": res["ctas"], "storage": f"tmpfs {cfg['io.dir']} O_DIRECT (ramfs)",
                    "l2": "inputs 16 GiB/GPU >> 126 MB L2; cold GPU page cache every step",

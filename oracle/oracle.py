@@ -132,7 +132,7 @@ def run_oracle(cfg, workload, *, source: int = SRC_NONE, paths=None, io_direct: 
     c.prefetch_bytes = cfg["gpufs.prefetch_bytes"]
     c.request_bytes = workload.request_bytes
     c.staging_bytes = cfg["rpc.staging_bytes"]
-    c.ra_max_bytes = cfg["io.ra_max_bytes"]
+    c.ra_max_bytes = cfg.ra_max()
     c.policy = 1 if cfg["gpufs.policy"] == "per-tb-lra" else 0
     c.resident_limit = cfg.resident_limit()
     c.raw_mode = int(bool(cfg["mode.gpu_cache_disabled"]))

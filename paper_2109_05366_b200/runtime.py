@@ -41,7 +41,7 @@ def native_config(cfg: ExperimentConfig, max_request_bytes: int = 0) -> native.G
     c.cache_bytes = cfg["gpufs.cache_bytes"]
     c.prefetch_bytes = cfg["gpufs.prefetch_bytes"]
     c.staging_bytes = cfg["rpc.staging_bytes"]
-    c.ra_max_bytes = cfg["io.ra_max_bytes"]
+    c.ra_max_bytes = cfg.ra_max()
     c.max_request_bytes = max_request_bytes or cfg["workload.request_bytes"]
     c.policy = native.POLICY[cfg["gpufs.policy"]]
     c.resident_limit = cfg.resident_limit()
