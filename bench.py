@@ -45,6 +45,7 @@ def parse():
     p.add_argument("--quick", action="store_true", help="headline only: skip comparison arms")
     p.add_argument("--set", action="append", default=[], metavar="KEY=VALUE")
     p.add_argument("--dir", default="/dev/shm")
+    p.add_argument("--no-clocks", action="store_true", help="skip nvidia-smi sampling")
     return p.parse_args()
 
 
@@ -363,7 +364,7 @@ def main() -> None:
     path = ensure_file(cfg, dist)
 
     res = run_arm(cfg, path, dist.rank, device, args.steps, args.warmup,
-                  sampler_index=device, dist=dist)
+                  sampler_index=None if args.no_clocks else device, dist=dist)
     st = res["stats"]
     kernel_s = sum(s["kernel_ns"] for s in st) / 1e9
     wall_s = sum(res["walls"])
