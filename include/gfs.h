@@ -35,9 +35,11 @@ enum { GFS_POLICY_GLOBAL_LRU = 0, GFS_POLICY_PER_TB_LRA = 1 };
 /* io.readahead: static = the reference span page+prefetch (prefetcher.py:13-25);
  * adaptive = window doubling on sequential continuation up to ra_max_bytes */
 enum { GFS_RA_STATIC = 0, GFS_RA_ADAPTIVE = 1 };
-/* io.transfer: zerocopy = SMs pull the span from mapped pinned staging;
+/* io.transfer: zerocopy = SMs pull the span from per-CTA mapped pinned staging;
+ * bounce = the daemon preads into a small (LLC-resident) per-worker pinned pool, the CTA
+ *          pulls the whole span into its HBM landing slot at once and releases the buffer;
  * dma = daemon cudaMemcpyAsync's staging -> HBM landing, doorbell after it */
-enum { GFS_XFER_ZEROCOPY = 0, GFS_XFER_DMA = 1 };
+enum { GFS_XFER_ZEROCOPY = 0, GFS_XFER_DMA = 1, GFS_XFER_BOUNCE = 2 };
 /* gopen flags: read-only files are the only ones prefetched (prefetcher.py:22-24) */
 enum { GFS_O_RDONLY = 0, GFS_O_RDWR = 2 };
 /* log kinds (deterministic mode) */

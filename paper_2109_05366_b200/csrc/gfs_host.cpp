@@ -164,6 +164,9 @@ struct gfs_ctx {
   int nbounce = 0;
   uint8_t* h_bounce = nullptr;
   std::vector<cudaEvent_t> bounce_ev;  // [io_workers * nbounce]
+  // bounce mode: the same pool, mapped; the GPU writes release words after pulling a span
+  uint32_t* h_release = nullptr;       // [io_workers * nbounce] (mapped)
+  std::vector<uint32_t> bounce_last;   // seq last stored in each buffer (0 = free)
   std::atomic<uint64_t> req_head{0};
   // daemon accounting for the current run (ns summed over workers)
   std::atomic<int64_t> t_pread{0}, t_idle{0}, t_xfer{0}, n_served{0};
@@ -211,6 +214,7 @@ static int64_t do_pread(gfs_ctx* ctx, const HostFile& f, int64_t off, int64_t si
 static void worker_main(gfs_ctx* ctx, int wid) {
   const uint32_t mask = ctx->ring_size - 1;
   const bool dma = ctx->cfg.transfer == GFS_XFER_DMA;
+  const bool bounce = ctx->cfg.transfer == GFS_XFER_BOUNCE;
   cudaStream_t st = dma ? ctx->worker_streams[wid] : nullptr;
   if (dma) cudaSetDevice(ctx->cfg.device);
   uint64_t nreq = 0;
@@ -239,6 +243,21 @@ static void worker_main(gfs_ctx* ctx, int wid) {
     if (dma) {  // next bounce buffer of this worker, once its previous copy has drained
       b = wid * ctx->nbounce + (int)(nreq % (uint64_t)ctx->nbounce);
       if (nreq >= (uint64_t)ctx->nbounce) cudaEventSynchronize(ctx->bounce_ev[b]);
+      buf = ctx->h_bounce + (int64_t)b * ctx->slot_bytes;
+    } else if (bounce) {  // next pool buffer, once the CTA that used it last pulled it out
+      b = wid * ctx->nbounce + (int)(nreq % (uint64_t)ctx->nbounce);
+      const uint32_t last = ctx->bounce_last[b];
+      uint64_t sp = 0;
+      while (last && __atomic_load_n(&ctx->h_release[b], __ATOMIC_ACQUIRE) != last) {
+        if (ctx->stop.load(std::memory_order_relaxed)) return;
+        if (++sp > 200000) {
+          timespec ts{0, 5000};
+          nanosleep(&ts, nullptr);
+        } else {
+          _mm_pause();
+        }
+      }
+      ctx->bounce_last[b] = seq;
       buf = ctx->h_bounce + (int64_t)b * ctx->slot_bytes;
     } else {
       buf = ctx->h_staging + (int64_t)slot * ctx->slot_bytes;
@@ -273,6 +292,8 @@ static void worker_main(gfs_ctx* ctx, int wid) {
     } else {
       RpcResp* r = &ctx->h_resp[slot];
       r->nbytes = n;
+      r->buf = b;
+      if (bounce && n <= 0) ctx->bounce_last[b] = 0;  // nothing to pull: buffer stays free
       __atomic_store_n(&r->seq, seq, __ATOMIC_RELEASE);
     }
     ctx->n_served.fetch_add(1, std::memory_order_relaxed);
@@ -312,7 +333,8 @@ static void free_all(gfs_ctx* ctx) {
   for (auto& l : ctx->d_logs) l.release();
   for (auto ev : ctx->bounce_ev)
     if (ev) cudaEventDestroy(ev);
-  void* host[] = {ctx->h_ring, ctx->h_resp, ctx->h_staging, ctx->h_served, ctx->h_bounce};
+  void* host[] = {ctx->h_ring, ctx->h_resp, ctx->h_staging, ctx->h_served, ctx->h_bounce,
+                  ctx->h_release};
   for (void* p : host)
     if (p) cudaFreeHost(p);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
@@ -406,9 +428,21 @@ extern "C" int gfs_create(const gfs_config* cfg_in, gfs_ctx** out) {
                     cudaHostAllocMapped | cudaHostAllocPortable));
   TRY(cudaHostAlloc(&ctx->h_resp, (size_t)ctx->n_ctas * sizeof(RpcResp),
                     cudaHostAllocMapped | cudaHostAllocPortable));
-  if (cfg.transfer != GFS_XFER_DMA)
+  if (cfg.transfer == GFS_XFER_ZEROCOPY)
     TRY(cudaHostAlloc(&ctx->h_staging, (size_t)(ctx->n_ctas * ctx->slot_bytes),
                       cudaHostAllocMapped | cudaHostAllocPortable));
+  if (cfg.transfer == GFS_XFER_BOUNCE) {
+    // ~24 MiB pool in total so it stays resident in the host LLC, 2..8 buffers per worker
+    ctx->nbounce = (int)std::max<int64_t>(2, (24ll << 20) / (ctx->slot_bytes * cfg.io_workers));
+    if (ctx->nbounce > 8) ctx->nbounce = 8;
+    const int64_t nb = (int64_t)cfg.io_workers * ctx->nbounce;
+    TRY(cudaHostAlloc(&ctx->h_bounce, (size_t)(ctx->slot_bytes * nb),
+                      cudaHostAllocMapped | cudaHostAllocPortable));
+    TRY(cudaHostAlloc(&ctx->h_release, (size_t)nb * 4, cudaHostAllocMapped | cudaHostAllocPortable));
+    memset(ctx->h_release, 0, (size_t)nb * 4);
+    ctx->bounce_last.assign((size_t)nb, 0);
+    TRY(cudaMalloc(&ctx->d_landing, (size_t)(ctx->n_ctas * ctx->slot_bytes)));
+  }
   memset(ctx->h_ring, 0, (size_t)ctx->ring_size * sizeof(RpcReq));
   memset(ctx->h_resp, 0, (size_t)ctx->n_ctas * sizeof(RpcResp));
   TRY(cudaHostAlloc(&ctx->h_served, 64, cudaHostAllocMapped | cudaHostAllocPortable));
@@ -662,6 +696,9 @@ extern "C" int gfs_run(gfs_ctx* ctx, const gfs_program* prog, void* dst, uint64_
   c.resp = ctx->h_resp;
   c.staging = ctx->h_staging;
   c.landing = ctx->d_landing;
+  c.bounce = ctx->h_bounce;
+  c.bounce_release = ctx->h_release;
+  c.bounce_bytes = ctx->slot_bytes;
   c.doorbell = ctx->d_doorbell;
   c.done_pos = ctx->d_done_pos;
   c.stats = ctx->d_stats;
@@ -686,7 +723,8 @@ extern "C" int gfs_run(gfs_ctx* ctx, const gfs_program* prog, void* dst, uint64_
     if (q == cudaSuccess) break;
     if (q != cudaErrorNotReady) return fail(GFS_ECUDA, "gread kernel failed: %s", cudaGetErrorString(q));
     if (now_ns() > deadline) return fail(GFS_ETIMEDOUT, "gread kernel did not finish in 600 s");
-    std::this_thread::sleep_for(std::chrono::microseconds(50));
+    // the daemon threads own the host cores while the kernel runs: poll lazily
+    std::this_thread::sleep_for(std::chrono::microseconds(500));
   }
   float ms = 0.f;
   if (prog->n_tb > 0) CUDA_TRY(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));

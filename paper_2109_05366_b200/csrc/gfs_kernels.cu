@@ -95,6 +95,10 @@ struct Smem {
   int64_t k;        // dispatcher ticket
   int any_bad;
   uint64_t t_copy0;
+  // bounce mode: span waiting in a host pool buffer to be pulled into the HBM landing slot
+  int64_t pull_n;
+  int32_t pull_buf;
+  uint32_t pull_seq;
   // TB state (thread 0)
   int tb;
   int64_t own_head, own_len;
@@ -505,6 +509,11 @@ __device__ int64_t rpc_call(const DevCtx& c, Smem& s, int64_t fid, int64_t off, 
     for (;;) {
       if (ld_acquire_sys(&r->seq) == seq) {
         n = *(volatile const int64_t*)&r->nbytes;
+        if (c.transfer == GFS_XFER_BOUNCE && n > 0) {  // pulled by the whole CTA (pull_span)
+          s.pull_n = n;
+          s.pull_buf = *(volatile const int32_t*)&r->buf;
+          s.pull_seq = seq;
+        }
         break;
       }
       if (!keep_waiting(c, t0, 22)) {
@@ -553,6 +562,22 @@ __device__ void copy_bytes(uint8_t* dst, const uint8_t* src, int64_t n) {
   } else {
     for (int64_t i = tid; i < n; i += BS) dst[i] = ld1<SRC>(src + i);
   }
+}
+
+// Bounce mode (all threads): pull the span the daemon left in a host pool buffer into this
+// CTA's HBM landing slot in one bulk pass, then hand the buffer back to its worker.
+template <int BS>
+__device__ void pull_span(const DevCtx& c, Smem& s) {
+  if (s.pull_n <= 0) return;
+  copy_bytes<BS, SRC_SYS>(c.landing + (int64_t)blockIdx.x * c.slot_bytes,
+                          c.bounce + (int64_t)s.pull_buf * c.bounce_bytes, s.pull_n);
+  __syncthreads();  // every load has returned: the buffer may be reused
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    st_release_sys(&c.bounce_release[s.pull_buf], s.pull_seq);
+    s.pull_n = 0;
+  }
+  __syncthreads();
 }
 
 // K1: copy a page's nb bytes from the span buffer into its frame (and, when the page is
@@ -918,6 +943,7 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
   }
   __syncthreads();
   if (s.b.status != 0) return -1;
+  pull_span<BS>(c, s);
 
   // (E) all threads: K1 over the whole batch — span buffer -> frames (+ user buffer)
   const int64_t vpp = pg >> 4;  // 16-byte vectors per page
@@ -938,7 +964,7 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
         const int j = (int)(v / vpp);
         const int64_t w = v - (int64_t)j * vpp;
         const uint4* sp = contiguous ? src4 + v : (const uint4*)(span_buf + s.b.src_off[j]) + w;
-        q[u] = (w << 4) < s.b.nb[j] ? (c.transfer == GFS_XFER_DMA ? ld16<SRC_HBM>(sp) : ld16<SRC_SYS>(sp))
+        q[u] = (w << 4) < s.b.nb[j] ? (c.transfer != GFS_XFER_ZEROCOPY ? ld16<SRC_HBM>(sp) : ld16<SRC_SYS>(sp))
                                     : make_uint4(0, 0, 0, 0);
       }
     }
@@ -968,7 +994,7 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
     const uint8_t* sp = span_buf + s.b.src_off[j];
     uint8_t* fp = c.frames + (int64_t)s.b.frame[j] * pg;
     for (int64_t i = (nbj & ~(int64_t)15) + tid; i < nbj; i += BS) {
-      const uint8_t b = c.transfer == GFS_XFER_DMA ? ld1<SRC_HBM>(sp + i) : ld1<SRC_SYS>(sp + i);
+      const uint8_t b = c.transfer != GFS_XFER_ZEROCOPY ? ld1<SRC_HBM>(sp + i) : ld1<SRC_SYS>(sp + i);
       fp[i] = b;
       if (chk) {
         const int64_t fo = (p0 + j) * pg + i;
@@ -1030,7 +1056,7 @@ __device__ int64_t gread(const DevCtx& c, Smem& s, int64_t fid, int64_t offset, 
   const int64_t pg = c.page_size;
   const DevFile& F = c.files[fid];
   const int64_t fs = F.size;
-  uint8_t* span_buf = (c.transfer == GFS_XFER_DMA ? c.landing : c.staging) +
+  uint8_t* span_buf = (c.transfer != GFS_XFER_ZEROCOPY ? c.landing : c.staging) +
                       (int64_t)blockIdx.x * c.slot_bytes;
   if (tid == 0) ST(greads)++;
 
@@ -1047,10 +1073,11 @@ __device__ int64_t gread(const DevCtx& c, Smem& s, int64_t fid, int64_t offset, 
       }
     }
     __syncthreads();
+    pull_span<BS>(c, s);
     int64_t n = s.n;
     if (n < 0) return -1;
     if (dst) {
-      if (c.transfer == GFS_XFER_DMA) copy_bytes<BS, SRC_HBM>(dst, span_buf, n);
+      if (c.transfer != GFS_XFER_ZEROCOPY) copy_bytes<BS, SRC_HBM>(dst, span_buf, n);
       else copy_bytes<BS, SRC_SYS>(dst, span_buf, n);
     }
     __syncthreads();
@@ -1156,6 +1183,7 @@ __device__ int64_t gread(const DevCtx& c, Smem& s, int64_t fid, int64_t offset, 
       s.t_copy0 = t1;
     }
     __syncthreads();
+    pull_span<BS>(c, s);
     const int act = s.act;
     const uint32_t f = s.frame;
     if (act == A_ABORT) return -1;
@@ -1189,7 +1217,7 @@ __device__ int64_t gread(const DevCtx& c, Smem& s, int64_t fid, int64_t offset, 
     }
     const bool whole = d && in_page == 0 && want == nb && (((uintptr_t)d & 15) == 0);
     const uint8_t* src = span_buf + s.src_off;
-    int bad = c.transfer == GFS_XFER_DMA
+    int bad = c.transfer != GFS_XFER_ZEROCOPY
                   ? copy_page_in<BS, SRC_HBM>(fmem, whole ? d : nullptr, src, nb, page * pg,
                                               c.verify ? F.content_id : -1)
                   : copy_page_in<BS, SRC_SYS>(fmem, whole ? d : nullptr, src, nb, page * pg,
@@ -1284,6 +1312,7 @@ __global__ void __launch_bounds__(BS, 4) gread_driver(DevCtx c) {
   const int tid = threadIdx.x;
   if (tid == 0) {
     for (int i = 0; i < GFS_NSTATS; i++) s.st[i] = 0;
+    s.pull_n = 0;
     // ring base for this launch: the daemon's completed-request count
     if (atomicCAS(&c.g->base_state, 0, 1) == 0) {
       c.g->req_base = ld_acquire_sys64(c.host_served);

@@ -31,7 +31,8 @@ struct alignas(32) RpcReq {
 struct alignas(64) RpcResp {
   int64_t nbytes;   // bytes read (EOF-clamped), < 0 = -errno
   uint32_t seq;     // request seq this answers (written last, release)
-  uint32_t pad[13];
+  int32_t buf;      // bounce mode: pool buffer holding the data
+  uint32_t pad[12];
 };
 
 struct DevFile {
@@ -110,6 +111,10 @@ struct DevCtx {
   // DMA mode (device)
   uint8_t* landing;          // [n_ctas][slot_bytes]
   unsigned long long* doorbell; // [n_ctas] (nbytes << 32 | seq), written by cuStreamWriteValue64
+  // bounce mode (mapped pinned host memory): worker pool and per-buffer release words
+  uint8_t* bounce;
+  uint32_t* bounce_release;  // [n_bounce]: seq of the request whose data was pulled out
+  int64_t bounce_bytes;
   // ring reuse guard (device)
   unsigned long long* done_pos;  // [ring_mask + 1]: last completed ring position + 1 per entry
   // counters (device): [n_ctas][GFS_NSTATS]
