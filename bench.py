@@ -57,7 +57,7 @@ def headline_overrides(size: int, n_gpus: int, directory: str) -> dict:
         "gpufs.prefetch_bytes": 60 * KiB, "gpufs.cache_bytes": 4 * GiB,
         "gpufs.policy": "per-tb-lra", "gpu.sm_count": 148, "gpu.max_threads_per_sm": 2048,
         "gpu.threads_per_tb": 512, "io.readahead": "adaptive", "io.ra_max_bytes": 0,
-        "io.transfer": "zerocopy", "io.workers": 12, "io.direct": True, "mode.ramfs": True,
+        "io.transfer": "bounce", "io.workers": 0, "io.direct": True, "mode.ramfs": True,
         "io.dir": directory, "mode.verify": True,
     }
 
@@ -452,9 +452,9 @@ def comparison_arms(cfg, path: str, device: int, head) -> tuple[dict, dict, dict
     probes["pcie_h2d_gbps"] = round(gbps(GiB, t), 3)
     dst = head["dst"]
     variants = {
-        "static_prefetch_zerocopy": {"io.readahead": "static"},
-        "adaptive_dma": {"io.transfer": "dma"},
-        "static_prefetch_dma": {"io.readahead": "static", "io.transfer": "dma"},
+        "static_prefetch_bounce": {"io.readahead": "static"},
+        "adaptive_zerocopy": {"io.transfer": "zerocopy"},
+        "adaptive_dma_1mib": {"io.transfer": "dma", "io.ra_max_bytes": 1 * MiB},
         "global_lru_prefetch": {"gpufs.policy": "global-lru-dealloc"},
         "nonprefetch_gpufs_4k": {"io.readahead": "static", "gpufs.prefetch_bytes": 0,
                                  "gpufs.policy": "global-lru-dealloc"},
