@@ -296,10 +296,14 @@ def cpu_oracle_sample(path: str, cfg, sample_bytes: int, threads: int) -> dict:
 
 
 def load_profile_summary() -> dict:
-    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
-    if os.path.exists(p):
-        with open(p) as fh:
-            return json.load(fh)
+    """Latest committed ncu --set full summary of gread_driver (profiles/rNN/)."""
+    import glob
+    paths = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_gread_summary.json")))
+    if paths:
+        with open(paths[-1]) as fh:
+            d = json.load(fh)
+        d["path"] = os.path.relpath(paths[-1], ROOT)
+        return d
     return {}
 
 
@@ -419,7 +423,11 @@ def main() -> None:
                          "peak": pk.get("hbm_gbs"), "unit": "GB/s",
                          "frac": round(gbps(hbm_alg, ms_step / 1e3) / pk["hbm_gbs"], 5)
                          if pk.get("hbm_gbs") else None,
-                         "traffic": prof.get("dram_bytes_per_launch"),
+                         "traffic": round(prof["dram_bytes_per_user_byte"] * nbytes)
+                         if prof.get("dram_bytes_per_user_byte") else None,
+                         "traffic_source": (f"{prof['path']}: dram read+write per user byte of "
+                                            f"the profiled launch x this launch's bytes")
+                         if prof else None,
                          "source": "MEASURED_PEAKS.json" if not pk.get("fallback") else "fallback"},
         "cpu_baseline": cpu_base,
         "e2e": {"value": round(gbps(total_bytes, wall_s), 3), "unit": "GB/s",
