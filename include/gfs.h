@@ -38,8 +38,10 @@ enum { GFS_RA_STATIC = 0, GFS_RA_ADAPTIVE = 1 };
 /* io.transfer: zerocopy = SMs pull the span from per-CTA mapped pinned staging;
  * bounce = the daemon preads into a small (LLC-resident) per-worker pinned pool, the CTA
  *          pulls the whole span into its HBM landing slot at once and releases the buffer;
- * dma = daemon cudaMemcpyAsync's staging -> HBM landing, doorbell after it */
-enum { GFS_XFER_ZEROCOPY = 0, GFS_XFER_DMA = 1, GFS_XFER_BOUNCE = 2 };
+ * dma = daemon cudaMemcpyAsync's staging -> HBM landing, doorbell after it;
+ * mapped = memory-resident (tmpfs) files: the daemon DMAs each span straight from the
+ *          pinned page-cache mapping into the HBM landing slot (no CPU copy) */
+enum { GFS_XFER_ZEROCOPY = 0, GFS_XFER_DMA = 1, GFS_XFER_BOUNCE = 2, GFS_XFER_MAPPED = 3 };
 /* gopen flags: read-only files are the only ones prefetched (prefetcher.py:22-24) */
 enum { GFS_O_RDONLY = 0, GFS_O_RDWR = 2 };
 /* log kinds (deterministic mode) */

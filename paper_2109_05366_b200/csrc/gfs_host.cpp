@@ -22,6 +22,7 @@
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
+#include <sys/mman.h>
 #include <sys/stat.h>
 #include <time.h>
 #include <unistd.h>
@@ -95,8 +96,17 @@ struct HostFile {
   int read_only = 1;
   int64_t content_id = -1;
   uint32_t* d_pt = nullptr;
+  uint8_t* map = nullptr;  // mapped mode: pinned read-only mapping of the whole file
   bool open = false;
 };
+
+static void unmap_file(HostFile& f) {
+  if (f.map) {
+    cudaHostUnregister(f.map);
+    munmap(f.map, (size_t)f.size);
+    f.map = nullptr;
+  }
+}
 
 template <typename T>
 struct DevBuf {  // grow-only device buffer
@@ -215,8 +225,9 @@ static void worker_main(gfs_ctx* ctx, int wid) {
   const uint32_t mask = ctx->ring_size - 1;
   const bool dma = ctx->cfg.transfer == GFS_XFER_DMA;
   const bool bounce = ctx->cfg.transfer == GFS_XFER_BOUNCE;
-  cudaStream_t st = dma ? ctx->worker_streams[wid] : nullptr;
-  if (dma) cudaSetDevice(ctx->cfg.device);
+  const bool mapped = ctx->cfg.transfer == GFS_XFER_MAPPED;
+  cudaStream_t st = (dma || mapped) ? ctx->worker_streams[wid] : nullptr;
+  if (st) cudaSetDevice(ctx->cfg.device);
   uint64_t nreq = 0;
   while (!ctx->stop.load(std::memory_order_relaxed)) {
     uint64_t h = ctx->req_head.fetch_add(1, std::memory_order_relaxed);
@@ -259,13 +270,20 @@ static void worker_main(gfs_ctx* ctx, int wid) {
       }
       ctx->bounce_last[b] = seq;
       buf = ctx->h_bounce + (int64_t)b * ctx->slot_bytes;
+    } else if (mapped) {
+      buf = nullptr;
     } else {
       buf = ctx->h_staging + (int64_t)slot * ctx->slot_bytes;
     }
     nreq++;
-    if (slot < 0 || slot >= ctx->n_ctas || fid < 0 || fid >= (int)ctx->files.size() ||
-        !ctx->files[fid].open || size > ctx->slot_bytes) {
+    const bool bad = slot < 0 || slot >= ctx->n_ctas || fid < 0 || fid >= (int)ctx->files.size() ||
+                     !ctx->files[fid].open || size > ctx->slot_bytes;
+    if (bad) {
       n = -EINVAL;
+    } else if (mapped) {  // no read at all: the span is DMA'd from the pinned file mapping
+      const HostFile& f = ctx->files[fid];
+      n = off >= f.size ? 0 : std::min(size, f.size - off);
+      buf = f.map + off;
     } else {
       n = do_pread(ctx, ctx->files[fid], off, size, buf);
     }
@@ -274,12 +292,12 @@ static void worker_main(gfs_ctx* ctx, int wid) {
     if (n < 0) ctx->worker_error.store((int)-n);
     // count it before completing: a launch that starts after this completion must see it
     __atomic_fetch_add(ctx->h_served, 1ull, __ATOMIC_SEQ_CST);
-    if (dma) {
+    if (dma || mapped) {
       cudaError_t ce = cudaSuccess;
       if (n > 0) {
         ce = cudaMemcpyAsync(ctx->d_landing + (int64_t)slot * ctx->slot_bytes, buf, (size_t)n,
                              cudaMemcpyHostToDevice, st);
-        if (ce == cudaSuccess) ce = cudaEventRecord(ctx->bounce_ev[b], st);
+        if (ce == cudaSuccess && dma) ce = cudaEventRecord(ctx->bounce_ev[b], st);
       }
       if (ce != cudaSuccess) {
         ctx->worker_error.store(EIO);
@@ -315,6 +333,7 @@ static void free_all(gfs_ctx* ctx) {
     if (f.fd_direct >= 0) close(f.fd_direct);
     if (f.fd_buffered >= 0) close(f.fd_buffered);
     if (f.d_pt) cudaFree(f.d_pt);
+    unmap_file(f);
   }
   ctx->files.clear();
   for (auto s : ctx->worker_streams)
@@ -447,7 +466,7 @@ extern "C" int gfs_create(const gfs_config* cfg_in, gfs_ctx** out) {
   memset(ctx->h_resp, 0, (size_t)ctx->n_ctas * sizeof(RpcResp));
   TRY(cudaHostAlloc(&ctx->h_served, 64, cudaHostAllocMapped | cudaHostAllocPortable));
   memset(ctx->h_served, 0, 64);
-  if (cfg.transfer == GFS_XFER_DMA) {
+  if (cfg.transfer == GFS_XFER_DMA || cfg.transfer == GFS_XFER_MAPPED) {
     TRY(cudaMalloc(&ctx->d_landing, (size_t)(ctx->n_ctas * ctx->slot_bytes)));
     TRY(cudaMalloc(&ctx->d_doorbell, (size_t)ctx->n_ctas * 8));
     TRY(cudaMemset(ctx->d_doorbell, 0, (size_t)ctx->n_ctas * 8));
@@ -459,6 +478,8 @@ extern "C" int gfs_create(const gfs_config* cfg_in, gfs_ctx** out) {
     ctx->write_value64 = (CUresult(*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int))fn;
     ctx->worker_streams.resize(cfg.io_workers, nullptr);
     for (auto& s : ctx->worker_streams) TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  }
+  if (cfg.transfer == GFS_XFER_DMA) {
     // ~48 MiB of bounce buffers in total (LLC-sized), at least 2 per worker
     ctx->nbounce = (int)std::max<int64_t>(2, (48ll << 20) / (ctx->slot_bytes * cfg.io_workers));
     if (ctx->nbounce > 8) ctx->nbounce = 8;
@@ -512,6 +533,23 @@ extern "C" int gfs_gopen(gfs_ctx* ctx, const char* path, int flags, int64_t cont
       return fail(GFS_ECUDA, "page table for %s: %s", path, cudaGetErrorString(e));
     }
   }
+  if (ctx->cfg.transfer == GFS_XFER_MAPPED && f.size > 0) {
+    // memory-resident file: pin its page-cache pages once so the daemon can DMA spans
+    // straight out of them (tmpfs/shmem allows long-term pins; disk files do not)
+    void* m = mmap(nullptr, (size_t)f.size, PROT_READ, MAP_SHARED | MAP_POPULATE, f.fd_buffered, 0);
+    cudaError_t e = m == MAP_FAILED ? cudaErrorInvalidValue
+                                    : cudaHostRegister(m, (size_t)f.size,
+                                                       cudaHostRegisterReadOnly | cudaHostRegisterPortable);
+    if (m == MAP_FAILED || e != cudaSuccess) {
+      if (m != MAP_FAILED) munmap(m, (size_t)f.size);
+      if (f.d_pt) cudaFree(f.d_pt);
+      close(f.fd_buffered);
+      if (f.fd_direct >= 0) close(f.fd_direct);
+      return fail(GFS_EIO, "io.transfer=mapped needs a memory-resident file (tmpfs); %s: %s", path,
+                  m == MAP_FAILED ? strerror(errno) : cudaGetErrorString(e));
+    }
+    f.map = (uint8_t*)m;
+  }
   f.open = true;
   ctx->files.push_back(f);
   *fid = (int)ctx->files.size() - 1;
@@ -527,6 +565,7 @@ extern "C" int gfs_gclose(gfs_ctx* ctx, int fid) {
   if (f.fd_direct >= 0) close(f.fd_direct);
   if (f.fd_buffered >= 0) close(f.fd_buffered);
   if (f.d_pt) cudaFree(f.d_pt);
+  unmap_file(f);
   f.fd_direct = f.fd_buffered = -1;
   f.d_pt = nullptr;
   f.open = false;

@@ -488,7 +488,7 @@ __device__ int64_t rpc_call(const DevCtx& c, Smem& s, int64_t fid, int64_t off, 
   st_release_sys(&e->seq, seq);
   const uint64_t tw = globaltimer();
   int64_t n;
-  if (c.transfer == GFS_XFER_DMA) {
+  if (c.transfer == GFS_XFER_DMA || c.transfer == GFS_XFER_MAPPED) {
     const unsigned long long* bell = &c.doorbell[slot];
     for (;;) {
       uint64_t v = ld_acquire_sys64(bell);
