@@ -182,6 +182,10 @@ struct gfs_ctx {
   std::atomic<int64_t> t_pread{0}, t_idle{0}, t_xfer{0}, n_served{0};
   std::atomic<bool> stop{false};
   std::atomic<int> worker_error{0};
+  // per-worker progress, for diagnosing a stalled request: last claimed ring position and
+  // phase (0 waiting for the entry, 1 reading, 2 completing, 3 completed)
+  std::atomic<uint64_t> w_pos[256];
+  std::atomic<int> w_phase[256];
   bool has_run = false;
   // driver entry point resolved through cudart (libgfs does not link libcuda, so it
   // loads on machines without a driver; CUDA calls then fail loudly)
@@ -235,6 +239,8 @@ static void worker_main(gfs_ctx* ctx, int wid) {
     const uint32_t seq = (uint32_t)(h + 1);
     uint64_t spins = 0;
     const uint64_t t_wait = now_ns();
+    ctx->w_pos[wid].store(h, std::memory_order_relaxed);
+    ctx->w_phase[wid].store(0, std::memory_order_relaxed);
     while (__atomic_load_n(&e->seq, __ATOMIC_ACQUIRE) != seq) {
       if (ctx->stop.load(std::memory_order_relaxed)) return;
       if (++spins < 20000) {
@@ -246,6 +252,7 @@ static void worker_main(gfs_ctx* ctx, int wid) {
     }
     const uint64_t t0 = now_ns();
     ctx->t_idle.fetch_add((int64_t)(t0 - t_wait), std::memory_order_relaxed);
+    ctx->w_phase[wid].store(1, std::memory_order_relaxed);
     const int64_t off = e->offset, size = e->size;
     const int fid = e->fid, slot = e->slot;
     int64_t n;
@@ -289,6 +296,7 @@ static void worker_main(gfs_ctx* ctx, int wid) {
     }
     const uint64_t t1 = now_ns();
     ctx->t_pread.fetch_add((int64_t)(t1 - t0), std::memory_order_relaxed);
+    ctx->w_phase[wid].store(2, std::memory_order_relaxed);
     if (n < 0) ctx->worker_error.store((int)-n);
     // count it before completing: a launch that starts after this completion must see it
     __atomic_fetch_add(ctx->h_served, 1ull, __ATOMIC_SEQ_CST);
@@ -315,6 +323,7 @@ static void worker_main(gfs_ctx* ctx, int wid) {
       __atomic_store_n(&r->seq, seq, __ATOMIC_RELEASE);
     }
     ctx->n_served.fetch_add(1, std::memory_order_relaxed);
+    ctx->w_phase[wid].store(3, std::memory_order_relaxed);
   }
 }
 
@@ -540,7 +549,20 @@ extern "C" int gfs_gopen(gfs_ctx* ctx, const char* path, int flags, int64_t cont
     cudaError_t e = m == MAP_FAILED ? cudaErrorInvalidValue
                                     : cudaHostRegister(m, (size_t)f.size,
                                                        cudaHostRegisterReadOnly | cudaHostRegisterPortable);
+    if (m != MAP_FAILED && e != cudaSuccess) {
+      // platforms without read-only registration: pin a shared read-write mapping of the
+      // same pages (never written through; needs write permission on the file)
+      cudaGetLastError();
+      munmap(m, (size_t)f.size);
+      int rw = open(path, O_RDWR);
+      m = rw < 0 ? MAP_FAILED
+                 : mmap(nullptr, (size_t)f.size, PROT_READ | PROT_WRITE, MAP_SHARED | MAP_POPULATE, rw, 0);
+      if (rw >= 0) close(rw);
+      e = m == MAP_FAILED ? cudaErrorInvalidValue
+                          : cudaHostRegister(m, (size_t)f.size, cudaHostRegisterPortable);
+    }
     if (m == MAP_FAILED || e != cudaSuccess) {
+      cudaGetLastError();  // do not leave a sticky error for the next launch check
       if (m != MAP_FAILED) munmap(m, (size_t)f.size);
       if (f.d_pt) cudaFree(f.d_pt);
       close(f.fd_buffered);
@@ -752,6 +774,7 @@ extern "C" int gfs_run(gfs_ctx* ctx, const gfs_program* prog, void* dst, uint64_
   ctx->n_served.store(0);
   if (prog->n_tb > 0) {
     CUDA_TRY(cudaEventRecord(ctx->ev0, ctx->stream));
+    cudaGetLastError();  // clear any stale non-sticky error before the launch check
     CUDA_TRY(launch_gread(c, cfg.cta_threads, ctx->stream));
     CUDA_TRY(cudaEventRecord(ctx->ev1, ctx->stream));
   }
@@ -793,10 +816,34 @@ extern "C" int gfs_run(gfs_ctx* ctx, const gfs_program* prog, void* dst, uint64_
                                   "private buffer overflow"};
     const char* what = g.error < 9 ? names[g.error] : "unknown";
     int werr = ctx->worker_error.load();
+    std::string diag;
+    if (g.error == ERR_TIMEOUT && (g.error_info == 21 || g.error_info == 22)) {
+      // a request never completed: say where it is (ring entry, mailbox/doorbell, workers)
+      const int slot = (int)(g.error_arg >> 32);
+      const uint32_t seq = (uint32_t)g.error_arg;
+      char b[256];
+      const RpcReq* e = &ctx->h_ring[(seq - 1) & (ctx->ring_size - 1)];
+      snprintf(b, sizeof b, "; slot %d seq %u: ring entry seq %u slot %d, mailbox seq %u", slot, seq,
+               e->seq, e->slot, slot < ctx->n_ctas ? ctx->h_resp[slot].seq : 0);
+      diag += b;
+      if (ctx->d_doorbell && slot < ctx->n_ctas) {
+        unsigned long long bell = 0;
+        cudaMemcpy(&bell, ctx->d_doorbell + slot, 8, cudaMemcpyDeviceToHost);
+        snprintf(b, sizeof b, ", doorbell seq %u n %u", (uint32_t)bell, (uint32_t)(bell >> 32));
+        diag += b;
+      }
+      snprintf(b, sizeof b, "; ring head %llu served %llu; workers",
+               (unsigned long long)ctx->req_head.load(), (unsigned long long)*ctx->h_served);
+      diag += b;
+      for (int w = 0; w < ctx->cfg.io_workers && w < 256; w++) {
+        snprintf(b, sizeof b, " %llu/%d", (unsigned long long)ctx->w_pos[w].load(), ctx->w_phase[w].load());
+        diag += b;
+      }
+    }
     return fail(g.error == ERR_IO ? GFS_EIO : (g.error == ERR_TIMEOUT ? GFS_ETIMEDOUT : GFS_EDEVICE),
-                "device error %d: %s (info %d, arg %llu)%s%s", g.error, what, g.error_info,
+                "device error %d: %s (info %d, arg %llu)%s%s%s", g.error, what, g.error_info,
                 (unsigned long long)g.error_arg, werr ? "; daemon errno: " : "",
-                werr ? strerror(werr) : "");
+                werr ? strerror(werr) : "", diag.c_str());
   }
   return GFS_OK;
 }
