@@ -39,9 +39,12 @@ enum { GFS_RA_STATIC = 0, GFS_RA_ADAPTIVE = 1 };
  * bounce = the daemon preads into a small (LLC-resident) per-worker pinned pool, the CTA
  *          pulls the whole span into its HBM landing slot at once and releases the buffer;
  * dma = daemon cudaMemcpyAsync's staging -> HBM landing, doorbell after it;
- * mapped = memory-resident (tmpfs) files: the daemon DMAs each span straight from the
- *          pinned page-cache mapping into the HBM landing slot (no CPU copy) */
-enum { GFS_XFER_ZEROCOPY = 0, GFS_XFER_DMA = 1, GFS_XFER_BOUNCE = 2, GFS_XFER_MAPPED = 3 };
+ * mapped_dma = memory-resident (tmpfs) files: the daemon DMAs each span straight from the
+ *          pinned page-cache mapping into the HBM landing slot (no CPU copy);
+ * mapped = memory-resident files: the daemon only answers the RPC, the CTA pulls the span
+ *          from the pinned page-cache mapping into its HBM landing slot itself */
+enum { GFS_XFER_ZEROCOPY = 0, GFS_XFER_DMA = 1, GFS_XFER_BOUNCE = 2, GFS_XFER_MAPPED = 3,
+       GFS_XFER_MAPPED_ZC = 4 };
 /* gopen flags: read-only files are the only ones prefetched (prefetcher.py:22-24) */
 enum { GFS_O_RDONLY = 0, GFS_O_RDWR = 2 };
 /* log kinds (deterministic mode) */

@@ -96,7 +96,8 @@ struct HostFile {
   int read_only = 1;
   int64_t content_id = -1;
   uint32_t* d_pt = nullptr;
-  uint8_t* map = nullptr;  // mapped mode: pinned read-only mapping of the whole file
+  uint8_t* map = nullptr;   // mapped modes: pinned mapping of the whole file (host address)
+  uint8_t* dmap = nullptr;  // and its device address
   bool open = false;
 };
 
@@ -229,7 +230,8 @@ static void worker_main(gfs_ctx* ctx, int wid) {
   const uint32_t mask = ctx->ring_size - 1;
   const bool dma = ctx->cfg.transfer == GFS_XFER_DMA;
   const bool bounce = ctx->cfg.transfer == GFS_XFER_BOUNCE;
-  const bool mapped = ctx->cfg.transfer == GFS_XFER_MAPPED;
+  const bool mapped = ctx->cfg.transfer == GFS_XFER_MAPPED;        // copy engine from the mapping
+  const bool mapped_zc = ctx->cfg.transfer == GFS_XFER_MAPPED_ZC;  // the CTA pulls it itself
   cudaStream_t st = (dma || mapped) ? ctx->worker_streams[wid] : nullptr;
   if (st) cudaSetDevice(ctx->cfg.device);
   uint64_t nreq = 0;
@@ -277,7 +279,7 @@ static void worker_main(gfs_ctx* ctx, int wid) {
       }
       ctx->bounce_last[b] = seq;
       buf = ctx->h_bounce + (int64_t)b * ctx->slot_bytes;
-    } else if (mapped) {
+    } else if (mapped || mapped_zc) {
       buf = nullptr;
     } else {
       buf = ctx->h_staging + (int64_t)slot * ctx->slot_bytes;
@@ -287,7 +289,7 @@ static void worker_main(gfs_ctx* ctx, int wid) {
                      !ctx->files[fid].open || size > ctx->slot_bytes;
     if (bad) {
       n = -EINVAL;
-    } else if (mapped) {  // no read at all: the span is DMA'd from the pinned file mapping
+    } else if (mapped || mapped_zc) {  // no read at all: the span comes from the pinned mapping
       const HostFile& f = ctx->files[fid];
       n = off >= f.size ? 0 : std::min(size, f.size - off);
       buf = f.map + off;
@@ -318,7 +320,7 @@ static void worker_main(gfs_ctx* ctx, int wid) {
     } else {
       RpcResp* r = &ctx->h_resp[slot];
       r->nbytes = n;
-      r->buf = b;
+      r->buf = mapped_zc ? -1 : b;
       if (bounce && n <= 0) ctx->bounce_last[b] = 0;  // nothing to pull: buffer stays free
       __atomic_store_n(&r->seq, seq, __ATOMIC_RELEASE);
     }
@@ -459,6 +461,8 @@ extern "C" int gfs_create(const gfs_config* cfg_in, gfs_ctx** out) {
   if (cfg.transfer == GFS_XFER_ZEROCOPY)
     TRY(cudaHostAlloc(&ctx->h_staging, (size_t)(ctx->n_ctas * ctx->slot_bytes),
                       cudaHostAllocMapped | cudaHostAllocPortable));
+  if (cfg.transfer == GFS_XFER_MAPPED_ZC)
+    TRY(cudaMalloc(&ctx->d_landing, (size_t)(ctx->n_ctas * ctx->slot_bytes)));
   if (cfg.transfer == GFS_XFER_BOUNCE) {
     // ~24 MiB pool in total so it stays resident in the host LLC, 2..8 buffers per worker
     ctx->nbounce = (int)std::max<int64_t>(2, (24ll << 20) / (ctx->slot_bytes * cfg.io_workers));
@@ -542,13 +546,13 @@ extern "C" int gfs_gopen(gfs_ctx* ctx, const char* path, int flags, int64_t cont
       return fail(GFS_ECUDA, "page table for %s: %s", path, cudaGetErrorString(e));
     }
   }
-  if (ctx->cfg.transfer == GFS_XFER_MAPPED && f.size > 0) {
+  if ((ctx->cfg.transfer == GFS_XFER_MAPPED || ctx->cfg.transfer == GFS_XFER_MAPPED_ZC) && f.size > 0) {
     // memory-resident file: pin its page-cache pages once so the daemon can DMA spans
     // straight out of them (tmpfs/shmem allows long-term pins; disk files do not)
     void* m = mmap(nullptr, (size_t)f.size, PROT_READ, MAP_SHARED | MAP_POPULATE, f.fd_buffered, 0);
     cudaError_t e = m == MAP_FAILED ? cudaErrorInvalidValue
                                     : cudaHostRegister(m, (size_t)f.size,
-                                                       cudaHostRegisterReadOnly | cudaHostRegisterPortable);
+                                                       cudaHostRegisterReadOnly | cudaHostRegisterPortable | cudaHostRegisterMapped);
     if (m != MAP_FAILED && e != cudaSuccess) {
       // platforms without read-only registration: pin a shared read-write mapping of the
       // same pages (never written through; needs write permission on the file)
@@ -559,7 +563,7 @@ extern "C" int gfs_gopen(gfs_ctx* ctx, const char* path, int flags, int64_t cont
                  : mmap(nullptr, (size_t)f.size, PROT_READ | PROT_WRITE, MAP_SHARED | MAP_POPULATE, rw, 0);
       if (rw >= 0) close(rw);
       e = m == MAP_FAILED ? cudaErrorInvalidValue
-                          : cudaHostRegister(m, (size_t)f.size, cudaHostRegisterPortable);
+                          : cudaHostRegister(m, (size_t)f.size, cudaHostRegisterPortable | cudaHostRegisterMapped);
     }
     if (m == MAP_FAILED || e != cudaSuccess) {
       cudaGetLastError();  // do not leave a sticky error for the next launch check
@@ -571,6 +575,12 @@ extern "C" int gfs_gopen(gfs_ctx* ctx, const char* path, int flags, int64_t cont
                   m == MAP_FAILED ? strerror(errno) : cudaGetErrorString(e));
     }
     f.map = (uint8_t*)m;
+    void* dp = nullptr;
+    if (cudaHostGetDevicePointer(&dp, m, 0) != cudaSuccess) {
+      cudaGetLastError();
+      dp = m;  // UVA: the host address is the device address
+    }
+    f.dmap = (uint8_t*)dp;
   }
   f.open = true;
   ctx->files.push_back(f);
@@ -612,6 +622,7 @@ static int upload_files(gfs_ctx* ctx) {
     df[i].npages = f.npages;
     df[i].read_only = f.read_only;
     df[i].content_id = (int32_t)f.content_id;
+    df[i].map = f.dmap;
   }
   CUDA_TRY(ctx->d_files.reserve(std::max<size_t>(df.size(), 1)));
   if (!df.empty())

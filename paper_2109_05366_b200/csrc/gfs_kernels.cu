@@ -97,8 +97,9 @@ struct Smem {
   uint64_t t_copy0;
   // bounce mode: span waiting in a host pool buffer to be pulled into the HBM landing slot
   int64_t pull_n;
-  int32_t pull_buf;
+  int32_t pull_buf;  // bounce buffer to release afterwards, -1 = none (mapped file)
   uint32_t pull_seq;
+  const uint8_t* pull_src;
   // TB state (thread 0)
   int tb;
   int64_t own_head, own_len;
@@ -512,7 +513,12 @@ __device__ int64_t rpc_call(const DevCtx& c, Smem& s, int64_t fid, int64_t off, 
         if (c.transfer == GFS_XFER_BOUNCE && n > 0) {  // pulled by the whole CTA (pull_span)
           s.pull_n = n;
           s.pull_buf = *(volatile const int32_t*)&r->buf;
+          s.pull_src = c.bounce + (int64_t)s.pull_buf * c.bounce_bytes;
           s.pull_seq = seq;
+        } else if (c.transfer == GFS_XFER_MAPPED_ZC && n > 0) {  // straight from the page cache
+          s.pull_n = n;
+          s.pull_buf = -1;
+          s.pull_src = c.files[fid].map + off;
         }
         break;
       }
@@ -569,12 +575,13 @@ __device__ void copy_bytes(uint8_t* dst, const uint8_t* src, int64_t n) {
 template <int BS>
 __device__ void pull_span(const DevCtx& c, Smem& s) {
   if (s.pull_n <= 0) return;
-  copy_bytes<BS, SRC_SYS>(c.landing + (int64_t)blockIdx.x * c.slot_bytes,
-                          c.bounce + (int64_t)s.pull_buf * c.bounce_bytes, s.pull_n);
+  copy_bytes<BS, SRC_SYS>(c.landing + (int64_t)blockIdx.x * c.slot_bytes, s.pull_src, s.pull_n);
   __syncthreads();  // every load has returned: the buffer may be reused
   if (threadIdx.x == 0) {
-    __threadfence_system();
-    st_release_sys(&c.bounce_release[s.pull_buf], s.pull_seq);
+    if (s.pull_buf >= 0) {
+      __threadfence_system();
+      st_release_sys(&c.bounce_release[s.pull_buf], s.pull_seq);
+    }
     s.pull_n = 0;
   }
   __syncthreads();

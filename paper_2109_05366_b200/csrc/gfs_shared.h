@@ -41,6 +41,7 @@ struct DevFile {
   int64_t npages;
   int32_t read_only;
   int32_t content_id; // >= 0: synthetic law W(content_id, i); -1 = unverified
+  const uint8_t* map; // mapped transfers: device pointer of the pinned file mapping
 };
 
 // Global run state in device memory (zeroed per run).

@@ -42,7 +42,7 @@ def oracle_checksum(cfg, seed):
 
 
 @pytest.mark.parametrize("name", gu.case_names())
-@pytest.mark.parametrize("transfer", ["zerocopy", "bounce", "dma", "mapped"])
+@pytest.mark.parametrize("transfer", ["zerocopy", "bounce", "dma", "mapped", "mapped_dma"])
 def test_golden_case_on_device(name, transfer, synth_dir):
     g = gu.load(name)
     sim, rep = run_sim(g["overrides"], g["seed"], synth_dir, **{"io.transfer": transfer})
