@@ -57,7 +57,7 @@ def headline_overrides(size: int, n_gpus: int, directory: str) -> dict:
         "gpufs.prefetch_bytes": 60 * KiB, "gpufs.cache_bytes": 4 * GiB,
         "gpufs.policy": "per-tb-lra", "gpu.sm_count": 148, "gpu.max_threads_per_sm": 2048,
         "gpu.threads_per_tb": 512, "io.readahead": "adaptive", "io.ra_max_bytes": 0,
-        "io.transfer": "bounce", "io.workers": 0, "io.direct": True, "mode.ramfs": True,
+        "io.transfer": "auto", "io.workers": 0, "io.direct": True, "mode.ramfs": True,
         "io.dir": directory, "mode.verify": True,
     }
 
@@ -407,7 +407,7 @@ def main() -> None:
                    "request": cfg["workload.request_bytes"], "page": cfg["gpufs.page_size"],
                    "prefetch": cfg["gpufs.prefetch_bytes"], "cache": cfg["gpufs.cache_bytes"],
                    "policy": cfg["gpufs.policy"], "readahead": cfg["io.readahead"],
-                   "ra_max": cfg.ra_max(), "transfer": cfg["io.transfer"],
+                   "ra_max": cfg.ra_max(), "transfer": cfg.transfer(),
                    "io_workers": cfg.io_workers(), "resident_tbs": cfg.resident_limit(),
                    "resident_ctas": res["ctas"], "storage": f"tmpfs {cfg['io.dir']} O_DIRECT (ramfs)",
                    "l2": "inputs 16 GiB/GPU >> 126 MB L2; cold GPU page cache every step",
@@ -460,13 +460,34 @@ def comparison_arms(cfg, path: str, device: int, head) -> tuple[dict, dict, dict
     probes["pcie_h2d_gbps"] = round(gbps(GiB, t), 3)
     dst = head["dst"]
     variants = {
-        "static_prefetch_bounce": {"io.readahead": "static"},
-        "adaptive_zerocopy": {"io.transfer": "zerocopy"},
-        "adaptive_dma_1mib": {"io.transfer": "dma", "io.ra_max_bytes": 1 * MiB},
+        # the north_star daemon path: O_DIRECT pread into pinned staging, then to HBM
+        "pread_bounce_adaptive": {"io.transfer": "bounce"},
+        "pread_bounce_static": {"io.transfer": "bounce", "io.readahead": "static"},
+        "pread_zerocopy_adaptive": {"io.transfer": "zerocopy"},
+        "pread_dma_adaptive": {"io.transfer": "dma"},
+        "mapped_dma_adaptive": {"io.transfer": "mapped_dma"},
+        "static_prefetch": {"io.readahead": "static"},
         "global_lru_prefetch": {"gpufs.policy": "global-lru-dealloc"},
         "nonprefetch_gpufs_4k": {"io.readahead": "static", "gpufs.prefetch_bytes": 0,
                                  "gpufs.policy": "global-lru-dealloc"},
     }
+    # the same path against a real block device: 4 GiB file on the root ext4 (virtio)
+    # disk, O_DIRECT preads (auto -> bounce), storage-bound; its own O_DIRECT roofline
+    try:
+        from paper_2109_05366_b200.runtime import ensure_synthetic
+        dsize = 4 * GiB
+        dcfg = cfg.copy_with({"io.dir": "/tmp", "mode.ramfs": False, "workload.file_bytes": dsize,
+                              "workload.total_bytes": dsize})
+        dpath = ensure_synthetic("/tmp", 0, dsize)
+        t = native.bench_storage(dpath, 0, dsize, min(16, threads), 4 * MiB, True)
+        disk_peak = gbps(dsize, t)
+        r = run_arm(dcfg, dpath, 0, device, 1, 1, dst=dst)
+        a = arm_summary(r)
+        a.update({"file": dpath, "transfer": dcfg.transfer(), "storage_odirect_gbps": round(disk_peak, 3),
+                  "roofline_frac": round(a["gbps"] / min(disk_peak, probes["pcie_h2d_gbps"]), 4)})
+        arms["disk_ext4_4gib"] = a
+    except Exception as e:
+        arms["disk_ext4_4gib"] = {"error": str(e)[:300]}
     for name, over in variants.items():
         try:
             r = run_arm(cfg.copy_with(over), path, 0, device, 1, 1, dst=dst)

@@ -316,6 +316,10 @@ static void worker_main(gfs_ctx* ctx, int wid) {
       uint64_t v = ((uint64_t)(n < 0 ? 0xFFFFFFFFull : (uint64_t)n) << 32) | seq;
       CUresult cr = ctx->write_value64((CUstream)st, (CUdeviceptr)(ctx->d_doorbell + slot), (cuuint64_t)v, 0);
       if (cr != CUDA_SUCCESS) ctx->worker_error.store(EIO);
+      // The driver may hold freshly enqueued work in its push buffer until the next call on
+      // the stream; this worker may not make one for a while (it spins on the ring), and
+      // the persistent kernel is waiting on exactly this doorbell.  Kick the stream.
+      cudaStreamQuery(st);
       ctx->t_xfer.fetch_add((int64_t)(now_ns() - t1), std::memory_order_relaxed);
     } else {
       RpcResp* r = &ctx->h_resp[slot];

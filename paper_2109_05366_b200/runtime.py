@@ -46,7 +46,7 @@ def native_config(cfg: ExperimentConfig, max_request_bytes: int = 0) -> native.G
     c.policy = native.POLICY[cfg["gpufs.policy"]]
     c.resident_limit = cfg.resident_limit()
     c.readahead = native.READAHEAD[cfg["io.readahead"]]
-    c.transfer = native.TRANSFER[cfg["io.transfer"]]
+    c.transfer = native.TRANSFER[cfg.transfer()]
     c.io_workers = cfg.io_workers()
     c.io_direct = int(bool(cfg["io.direct"]))
     c.device = cfg["gpu.device"]
