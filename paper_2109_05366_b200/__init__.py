@@ -6,7 +6,15 @@ Drop-in for the reference package ``gpuiosim``'s sequential gread path: the same
 I/O daemon) by libgfs.so.  See DESIGN.md.
 """
 
-from .config import ExperimentConfig, load_config
+import os as _os
+
+# DMA transfers run the host daemon's copies on their own streams while the persistent
+# gread kernel occupies another.  With the driver's default of 8 hardware work queues, a
+# daemon stream can alias the kernel's queue and its copy (and the doorbell behind it)
+# would wait for the kernel that waits for it.  Ask for enough queues before CUDA starts.
+_os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
+from .config import ExperimentConfig, load_config  # noqa: E402
 from .errors import GfsError, SimError
 from .rng import SeededRng
 

@@ -232,7 +232,8 @@ static void worker_main(gfs_ctx* ctx, int wid) {
   const bool bounce = ctx->cfg.transfer == GFS_XFER_BOUNCE;
   const bool mapped = ctx->cfg.transfer == GFS_XFER_MAPPED;        // copy engine from the mapping
   const bool mapped_zc = ctx->cfg.transfer == GFS_XFER_MAPPED_ZC;  // the CTA pulls it itself
-  cudaStream_t st = (dma || mapped) ? ctx->worker_streams[wid] : nullptr;
+  cudaStream_t st =
+      (dma || mapped) ? ctx->worker_streams[(size_t)wid % ctx->worker_streams.size()] : nullptr;
   if (st) cudaSetDevice(ctx->cfg.device);
   uint64_t nreq = 0;
   while (!ctx->stop.load(std::memory_order_relaxed)) {
@@ -493,7 +494,9 @@ extern "C" int gfs_create(const gfs_config* cfg_in, gfs_ctx** out) {
     if (!fn || qr != cudaDriverEntryPointSuccess)
       return bail(fail(GFS_ECUDA, "cuStreamWriteValue64 unavailable (stream memory operations)"));
     ctx->write_value64 = (CUresult(*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int))fn;
-    ctx->worker_streams.resize(cfg.io_workers, nullptr);
+    // a few copy streams shared by the workers (streams are thread-safe): every extra
+    // stream risks sharing a hardware queue with the persistent kernel's stream
+    ctx->worker_streams.resize((size_t)std::min(cfg.io_workers, 4), nullptr);
     for (auto& s : ctx->worker_streams) TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
   }
   if (cfg.transfer == GFS_XFER_DMA) {
