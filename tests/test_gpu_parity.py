@@ -160,3 +160,29 @@ def test_checksum_kernel_matches_numpy():
     with GpuFS(ExperimentConfig({"gpufs.cache_bytes": 1 * MiB})) as fs:
         assert fs.checksum(t) == grng.checksum(data)
         assert fs.checksum(t, word_base=9) == grng.checksum(data, 9)
+
+
+def test_fig10micro_preset_ordering_on_device(tmp_path, synth_dir):
+    """Criterion 5 on real hardware (tests/test_acceptance.py:145-158): with the file at 2x
+    the cache, per-tb-lra+prefetch > global+prefetch > original GPUfs, by >= 4x overall."""
+    import csv
+    from paper_2109_05366_b200.experiments import run_preset
+    base = ExperimentConfig({"repetitions": 1, "io.dir": synth_dir, "gpu.sm_count": 15})
+    path = run_preset("fig10micro", base, str(tmp_path))
+    rows = [r for r in csv.DictReader(open(path)) if r["seed"] == "mean"]
+    assert len(rows[0]) == 36
+    bw = {r["label"]: float(r["io_bandwidth_bps"]) for r in rows}
+    assert bw["lra-prefetch"] > bw["global-prefetch"] > bw["baseline-4k"]
+    assert bw["lra-prefetch"] / bw["baseline-4k"] >= 4.0
+
+
+def test_recorded_trace_matches_reference_format(tmp_path, synth_dir):
+    """workload.record_trace writes the reference's trace format (workloads.py:151-162);
+    per TB it must be the golden RPC trace."""
+    from paper_2109_05366_b200.workloads import load_trace
+    g = gu.load("micro_pf60")
+    trace = str(tmp_path / "t.txt")
+    sim, _ = run_sim(g["overrides"], g["seed"], synth_dir, **{"workload.record_trace": trace})
+    recs = load_trace(trace)
+    got = np.asarray([(r.tb_id, r.file_id, r.offset, r.size) for r in recs], dtype=np.int64)
+    assert np.array_equal(gu.by_tb(got), gu.expand_rpcs(g["rpcs_rle"]))
