@@ -295,10 +295,11 @@ def cpu_oracle_sample(path: str, cfg, sample_bytes: int, threads: int) -> dict:
             "seconds": round(el, 3)}
 
 
-def load_profile_summary() -> dict:
-    """Latest committed ncu --set full summary of gread_driver (profiles/rNN/)."""
+def load_profile_summary(transfer: str) -> dict:
+    """Latest committed ncu --set full summary of gread_driver for this transfer mode
+    (profiles/rNN/ncu_gread_<transfer>_summary.json)."""
     import glob
-    paths = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_gread_summary.json")))
+    paths = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", f"ncu_gread_{transfer}_summary.json")))
     if paths:
         with open(paths[-1]) as fh:
             d = json.load(fh)
@@ -393,7 +394,7 @@ def main() -> None:
     stor = probes.get("storage_odirect_gbps")
     io_peak = min(x for x in (h2d, stor) if x) if (h2d or stor) else None
     pk = peaks()
-    prof = load_profile_summary()
+    prof = load_profile_summary(cfg.transfer())
     ms_step = kernel_s / len(st) * 1e3
     hbm_alg = 4 * nbytes  # PCIe->frame write, frame/pb read, user-buffer write, span read
     out = {
