@@ -129,6 +129,27 @@ int gfs_file_size(gfs_ctx* ctx, int fid, int64_t* size);
  * done; cold page cache per run (as a fresh Simulation). ---- */
 int gfs_run(gfs_ctx* ctx, const gfs_program* prog, void* dst, uint64_t dst_bytes, gfs_stats* out);
 
+/* ---- streaming consumers fused into the gread loop.  After each gread
+ * the TB runs the consumer over the bytes it just delivered (they are in L2), so compute
+ * overlaps the other TBs' I/O — the real counterpart of workload.compute_ns_per_byte
+ * (gpu_exec.py:127-129).  Elements decode from the file bytes: f32 = (u32 >> 8) * 2^-24. */
+enum { GFS_CONSUME_NONE = 0, GFS_CONSUME_SUM64 = 1, GFS_CONSUME_GEMV_F32 = 2, GFS_CONSUME_NN_F32 = 3 };
+
+typedef struct gfs_consumer {
+  int32_t kind;             /* GFS_CONSUME_* */
+  int32_t reserved;
+  int64_t cols;             /* GEMV: row length (elements, multiple of 4) of the row-major file matrix */
+  const float* x;           /* GEMV: device vector [cols] */
+  float* y;                 /* GEMV: device vector [rows], accumulated into (y += A x) */
+  float qx, qy;             /* NN: query point (records are (lat, lng) pairs) */
+  unsigned long long* out;  /* SUM64: device u64 += sum_i mix64(w_i ^ (i * golden)) over file words;
+                               NN: device u64 atomicMin of (dist2 bits << 32 | record index) */
+} gfs_consumer;
+
+/* gfs_run plus a consumer (cons may be NULL); requires a user buffer. */
+int gfs_run_consume(gfs_ctx* ctx, const gfs_program* prog, void* dst, uint64_t dst_bytes,
+                    const gfs_consumer* cons, gfs_stats* out);
+
 /* ---- logs of the last run (metrics.deliveries, recorded trace, victim_log) ---- */
 int gfs_log_len(gfs_ctx* ctx, int kind, int64_t* n);
 int gfs_log_copy(gfs_ctx* ctx, int kind, int64_t* out, int64_t cap_records);

@@ -689,12 +689,37 @@ static int validate_program(gfs_ctx* ctx, const gfs_program* prog, uint64_t dst_
   return GFS_OK;
 }
 
+static int validate_consumer(const gfs_consumer* k, const gfs_program* prog, bool has_dst) {
+  if (!k || k->kind == GFS_CONSUME_NONE) return GFS_OK;
+  if (k->kind < GFS_CONSUME_NONE || k->kind > GFS_CONSUME_NN_F32)
+    return fail(GFS_EINVAL, "unknown consumer kind %d", k->kind);
+  if (!has_dst) return fail(GFS_EINVAL, "consumers read the user buffer: dst is required");
+  const int64_t align = k->kind == GFS_CONSUME_GEMV_F32 ? 16 : 8;
+  if (k->kind == GFS_CONSUME_GEMV_F32 && (k->cols <= 0 || k->cols % 4 || !k->x || !k->y))
+    return fail(GFS_EINVAL, "GEMV consumer needs cols > 0 (multiple of 4), x and y");
+  if (k->kind != GFS_CONSUME_GEMV_F32 && !k->out) return fail(GFS_EINVAL, "consumer needs out");
+  if (prog->request_bytes % align) return fail(GFS_EINVAL, "consumer needs %lld-byte aligned requests", (long long)align);
+  const int64_t n_segs = prog->prog_off[prog->n_tb];
+  for (int64_t s = 0; s < n_segs; s++)
+    if (prog->segs[3 * s + 1] % align || prog->segs[3 * s + 2] % align)
+      return fail(GFS_EINVAL, "consumer needs %lld-byte aligned segments", (long long)align);
+  for (int t = 0; t < prog->n_tb; t++)
+    if (prog->dst_off[t] % align) return fail(GFS_EINVAL, "consumer needs aligned user-buffer offsets");
+  return GFS_OK;
+}
+
 extern "C" int gfs_run(gfs_ctx* ctx, const gfs_program* prog, void* dst, uint64_t dst_bytes,
                        gfs_stats* out) {
+  return gfs_run_consume(ctx, prog, dst, dst_bytes, nullptr, out);
+}
+
+extern "C" int gfs_run_consume(gfs_ctx* ctx, const gfs_program* prog, void* dst, uint64_t dst_bytes,
+                               const gfs_consumer* cons, gfs_stats* out) {
   const uint64_t w0 = now_ns();
   if (!ctx || !prog || !out) return fail(GFS_EINVAL, "gfs_run: null argument");
   int rc = validate_program(ctx, prog, dst_bytes, dst != nullptr);
   if (rc) return rc;
+  if ((rc = validate_consumer(cons, prog, dst != nullptr))) return rc;
   CUDA_TRY(cudaSetDevice(ctx->cfg.device));
   const gfs_config& cfg = ctx->cfg;
   int64_t n_segs = 0;
@@ -781,6 +806,8 @@ extern "C" int gfs_run(gfs_ctx* ctx, const gfs_program* prog, void* dst, uint64_
   c.doorbell = ctx->d_doorbell;
   c.done_pos = ctx->d_done_pos;
   c.stats = ctx->d_stats;
+  if (cons) c.cons = *cons;
+  else c.cons.kind = GFS_CONSUME_NONE;
   for (int k = 0; k < 4; k++) {
     c.logs[k] = ctx->d_logs[k].p;
     c.log_cap[k] = ctx->log_cap[k];

@@ -1255,9 +1255,88 @@ __device__ int64_t gread(const DevCtx& c, Smem& s, int64_t fid, int64_t offset, 
   }
 }
 
+// ------------------------------------------------------------ fused consumers (K4)
+
+struct ConsAcc {
+  unsigned long long sum = 0;     // SUM64 partial
+  unsigned long long nn = ~0ull;  // NN partial minimum
+};
+
+__device__ __forceinline__ float decode_f32(uint32_t u) { return (float)(u >> 8) * (1.0f / 16777216.0f); }
+
+constexpr int GEMV_ROWS = 1024;  // rows of one request accumulated in shared memory
+
+// Consume the n bytes the TB just delivered (`data`, in the user buffer) that came from
+// file offset `file_off`.  All threads.
+template <int BS>
+__device__ void consume(const DevCtx& c, const uint8_t* data, int64_t n, int64_t file_off, ConsAcc& acc) {
+  const int tid = threadIdx.x;
+  const gfs_consumer& k = c.cons;
+  if (n <= 0) return;
+  if (k.kind == GFS_CONSUME_SUM64) {  // words of the file, position-weighted
+    const int64_t nw = n >> 3, w0 = file_off >> 3;
+    const uint64_t* w = (const uint64_t*)data;
+    for (int64_t i = tid; i < nw; i += BS)
+      acc.sum += mix64(__ldcg(w + i) ^ ((uint64_t)(w0 + i) * 0x9E3779B97F4A7C15ull));
+  } else if (k.kind == GFS_CONSUME_NN_F32) {  // records (lat, lng): nearest to (qx, qy)
+    const int64_t nr = n >> 3, r0 = file_off >> 3;
+    const uint2* rec = (const uint2*)data;
+    for (int64_t i = tid; i < nr; i += BS) {
+      const uint2 u = __ldcg(rec + i);
+      // IEEE single-precision steps without contraction: the same bits numpy float32 gets
+      const float lat = __fsub_rn(__fmul_rn(decode_f32(u.x), 180.0f), 90.0f);
+      const float lng = __fsub_rn(__fmul_rn(decode_f32(u.y), 360.0f), 180.0f);
+      const float dx = __fsub_rn(lat, k.qx), dy = __fsub_rn(lng, k.qy);
+      const float d2 = __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
+      const unsigned long long key =
+          ((unsigned long long)__float_as_uint(d2) << 32) | (unsigned long long)(uint32_t)(r0 + i);
+      acc.nn = key < acc.nn ? key : acc.nn;
+    }
+  } else if (k.kind == GFS_CONSUME_GEMV_F32) {  // y[row] += sum_col A[row, col] * x[col]
+    __shared__ float rows[GEMV_ROWS];
+    const int64_t M = k.cols;
+    const int64_t e0 = file_off >> 2, ne = n >> 2;
+    const int64_t row_lo = e0 / M, row_hi = (e0 + ne - 1) / M;
+    const bool local = row_hi - row_lo < GEMV_ROWS;
+    if (local)
+      for (int i = tid; i <= (int)(row_hi - row_lo); i += BS) rows[i] = 0.f;
+    __syncthreads();
+    const uint4* v4 = (const uint4*)data;
+    for (int64_t i = tid; i < (ne >> 2); i += BS) {
+      const uint4 u = __ldcg(v4 + i);
+      const int64_t e = e0 + 4 * i;
+      const int64_t row = e / M, col = e - row * M;  // cols % 4 == 0: one row per vector
+      const float4 xv = *(const float4*)(k.x + col);
+      const float p = decode_f32(u.x) * xv.x + decode_f32(u.y) * xv.y + decode_f32(u.z) * xv.z +
+                      decode_f32(u.w) * xv.w;
+      if (local) atomicAdd(&rows[row - row_lo], p);
+      else atomicAdd(&k.y[row], p);
+    }
+    __syncthreads();
+    if (local)
+      for (int i = tid; i <= (int)(row_hi - row_lo); i += BS) atomicAdd(&k.y[row_lo + i], rows[i]);
+    __syncthreads();
+  }
+}
+
+template <int BS>
+__device__ void consume_flush(const DevCtx& c, ConsAcc& acc) {
+  const int kind = c.cons.kind;
+  if (kind != GFS_CONSUME_SUM64 && kind != GFS_CONSUME_NN_F32) return;
+  unsigned long long v = kind == GFS_CONSUME_SUM64 ? acc.sum : acc.nn;
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = kind == GFS_CONSUME_SUM64 ? v + w : (w < v ? w : v);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (kind == GFS_CONSUME_SUM64) atomicAdd(c.cons.out, v);
+    else atomicMin(c.cons.out, v);
+  }
+}
+
 // TB program (gpu_exec.py:95-105) and TB done (drain + retire, gpu_exec.py:281-291).
 template <int BS>
-__device__ bool run_tb(const DevCtx& c, Smem& s, int tb, int& bad_words) {
+__device__ bool run_tb(const DevCtx& c, Smem& s, int tb, int& bad_words, ConsAcc& acc) {
   const int tid = threadIdx.x;
   if (tid == 0) {
     s.tb = tb;
@@ -1287,6 +1366,7 @@ __device__ bool run_tb(const DevCtx& c, Smem& s, int tb, int& bad_words) {
       uint8_t* d = c.dst ? c.dst + pos + seg_off : nullptr;
       int64_t got = gread<BS>(c, s, fid, base + seg_off, size, base + len, d, bad_words);
       if (got < 0) return false;
+      if (c.cons.kind != GFS_CONSUME_NONE && d) consume<BS>(c, d, got, base + seg_off, acc);
       seg_off += got;
       if (got < size) break;  // short read: rest of the segment is skipped
     }
@@ -1331,6 +1411,7 @@ __global__ void __launch_bounds__(BS, 4) gread_driver(DevCtx c) {
     }
   }
   int bad_words = 0;
+  ConsAcc acc;
   for (;;) {
     if (tid == 0) {
       s.k = has_error(c) ? (int64_t)c.n_tb : (int64_t)atomicAdd(&c.g->next_tb, 1ull);
@@ -1339,8 +1420,9 @@ __global__ void __launch_bounds__(BS, 4) gread_driver(DevCtx c) {
     const int64_t k = s.k;
     __syncthreads();
     if (k >= c.n_tb) break;
-    if (!run_tb<BS>(c, s, c.order[k], bad_words)) break;
+    if (!run_tb<BS>(c, s, c.order[k], bad_words, acc)) break;
   }
+  consume_flush<BS>(c, acc);
   __shared__ int mism;
   if (tid == 0) mism = 0;
   __syncthreads();

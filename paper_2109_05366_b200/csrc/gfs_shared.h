@@ -118,6 +118,8 @@ struct DevCtx {
   int64_t bounce_bytes;
   // ring reuse guard (device)
   unsigned long long* done_pos;  // [ring_mask + 1]: last completed ring position + 1 per entry
+  // fused consumer (gfs_run_consume)
+  gfs_consumer cons;
   // counters (device): [n_ctas][GFS_NSTATS]
   long long* stats;
   // logs (device): [cap][width]

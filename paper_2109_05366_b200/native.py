@@ -24,6 +24,7 @@ LOG_WIDTH = {LOG_DELIVERIES: 3, LOG_RPCS: 4, LOG_VICTIMS: 3, LOG_WINDOWS: 2}
 
 # Every entry point declared in include/gfs.h (tests check the library exports them).
 EXPORTS = ["gfs_create", "gfs_destroy", "gfs_gopen", "gfs_gclose", "gfs_file_size", "gfs_run",
+           "gfs_run_consume",
            "gfs_log_len", "gfs_log_copy", "gfs_checksum", "gfs_verify_dst", "gfs_gen_file",
            "gfs_last_error", "gfs_abi_version", "gfs_stat_count", "gfs_stat_name",
            "gfs_resident_ctas", "gfs_bench_storage", "gfs_bench_h2d", "gfs_bench_read_memcpy"]
@@ -38,6 +39,17 @@ class GfsConfig(C.Structure):
         ("device", C.c_int32), ("cta_threads", C.c_int32), ("max_ctas", C.c_int32),
         ("raw_mode", C.c_int32), ("pcie_disabled", C.c_int32), ("log", C.c_int32),
         ("verify", C.c_int32), ("reserved", C.c_int32 * 3),
+    ]
+
+
+CONSUME = {"none": 0, "sum64": 1, "gemv_f32": 2, "nn_f32": 3}
+
+
+class GfsConsumer(C.Structure):
+    _fields_ = [
+        ("kind", C.c_int32), ("reserved", C.c_int32), ("cols", C.c_int64),
+        ("x", C.c_void_p), ("y", C.c_void_p), ("qx", C.c_float), ("qy", C.c_float),
+        ("out", C.c_void_p),
     ]
 
 
@@ -70,6 +82,8 @@ def load(path: str = LIB_PATH):
     L.gfs_gclose.argtypes = [vp, i32]
     L.gfs_file_size.argtypes = [vp, i32, C.POINTER(i64)]
     L.gfs_run.argtypes = [vp, C.POINTER(GfsProgram), vp, u64, vp]
+    L.gfs_run_consume.argtypes = [vp, C.POINTER(GfsProgram), vp, u64, C.POINTER(GfsConsumer), vp]
+    L.gfs_run_consume.restype = i32
     L.gfs_log_len.argtypes = [vp, i32, C.POINTER(i64)]
     L.gfs_log_copy.argtypes = [vp, i32, C.POINTER(i64), i64]
     L.gfs_checksum.argtypes = [vp, vp, u64, u64, C.POINTER(u64)]

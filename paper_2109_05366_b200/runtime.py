@@ -82,6 +82,37 @@ def _ptr(a: np.ndarray, ctype):
     return a.ctypes.data_as(C.POINTER(ctype))
 
 
+@dataclass
+class Consumer:
+    """A streaming consumer fused into the gread loop (include/gfs.h gfs_consumer).
+
+    sum64:    out (uint64 CUDA tensor [1]) += sum_i mix64(w_i ^ (i * golden)) over file words
+    gemv_f32: y (float32 [rows]) += A x, A = the file as a row-major [rows, cols] matrix of
+              f32 = (u32 >> 8) * 2^-24 (the gesummv/mvt/bicg/atax access pattern)
+    nn_f32:   out (uint64 [1]) = min over records (lat, lng) of (dist2 bits << 32 | index),
+              the Rodinia nn scan
+    """
+    kind: str
+    out: object = None
+    x: object = None
+    y: object = None
+    cols: int = 0
+    qx: float = 0.0
+    qy: float = 0.0
+
+    def native(self) -> "native.GfsConsumer":
+        k = native.GfsConsumer()
+        if self.kind not in native.CONSUME:
+            raise GfsError(f"unknown consumer {self.kind!r}")
+        k.kind = native.CONSUME[self.kind]
+        k.cols = self.cols
+        k.x = self.x.data_ptr() if self.x is not None else None
+        k.y = self.y.data_ptr() if self.y is not None else None
+        k.out = self.out.data_ptr() if self.out is not None else None
+        k.qx, k.qy = self.qx, self.qy
+        return k
+
+
 class GpuFS:
     """One GPU's file layer: HBM page cache + RPC ring + host I/O daemon."""
 
@@ -150,8 +181,10 @@ class GpuFS:
         p.order = _ptr(keep[3], C.c_int32)
         return p, keep
 
-    def run(self, table: ProgramTable, request_bytes: int, dst=None, order=None) -> RunResult:
-        """All TBs' gread loops (gpu_exec.py:95-239); dst = uint8 CUDA tensor or None."""
+    def run(self, table: ProgramTable, request_bytes: int, dst=None, order=None,
+            consumer: "Consumer | None" = None) -> RunResult:
+        """All TBs' gread loops (gpu_exec.py:95-239); dst = uint8 CUDA tensor or None;
+        `consumer` runs a fused streaming consumer over every delivered request."""
         if order is None:
             order = np.arange(table.n_tb, dtype=np.int32)
         prog, keep = self._program(table, request_bytes, order)
@@ -162,7 +195,10 @@ class GpuFS:
             dst_ptr, dst_bytes = dst.data_ptr(), dst.numel() * dst.element_size()
         names = native.stat_names()
         out = (C.c_int64 * len(names))()
-        native.check(self._lib.gfs_run(self._h, C.byref(prog), dst_ptr, dst_bytes, out), "gfs_run")
+        cons = consumer.native() if consumer is not None else None
+        native.check(self._lib.gfs_run_consume(self._h, C.byref(prog), dst_ptr, dst_bytes,
+                                               C.byref(cons) if cons is not None else None, out),
+                     "gfs_run")
         del keep
         res = RunResult(stats=dict(zip(names, list(out))))
         if self._ncfg.log:
