@@ -514,12 +514,58 @@ def comparison_arms(cfg, path: str, device: int, head) -> tuple[dict, dict, dict
                           "sync_memcpy": sync}
         except Exception as e:
             arms[name] = {"error": str(e)[:300]}
+    try:
+        arms["consumer_gesummv_950MB"] = consumer_arm(cfg, path, device, dst)
+    except Exception as e:
+        arms["consumer_gesummv_950MB"] = {"error": str(e)[:300]}
     cpu_base = None
     try:
         cpu_base = cpu_oracle_sample(path, cfg, 2 * GiB, threads)
     except Exception as e:
         cpu_base = {"error": str(e)[:300]}
     return probes, arms, cpu_base
+
+
+def consumer_arm(cfg, path: str, device: int, dst) -> dict:
+    """C4: the gesummv input shape (950 MB, 128 TBs, workloads.py:117) read through gread
+    with the GEMV consumer fused (y += A x as each request lands) vs gread then a separate
+    torch.mv over the user buffer."""
+    import torch
+    from paper_2109_05366_b200.runtime import Consumer, GpuFS
+    from paper_2109_05366_b200.workloads import ProgramTable, gen_sequential_strided
+    n_tb, unit = 128, 128 * 4096
+    total = 950_000_000 // unit * unit
+    wl = gen_sequential_strided([cfg["workload.file_bytes"]], n_tb, total, 64 * KiB, 4096)
+    table = ProgramTable.from_programs(wl.programs)
+    cols = 4096
+    rows = total // 4 // cols
+    x = torch.rand(cols, device=f"cuda:{device}")
+    y = torch.zeros(rows, device=f"cuda:{device}")
+    out = {}
+    with GpuFS(cfg, max_request_bytes=64 * KiB) as fs:
+        fs.gopen(path, content_id=0)
+        fs.run(table, 64 * KiB, dst)  # warm-up
+        r = fs.run(table, 64 * KiB, dst)
+        out["gread_only_gbps"] = round(gbps(total, r.stats["kernel_ns"] / 1e9), 3)
+        fs.run(table, 64 * KiB, dst, consumer=Consumer("gemv_f32", x=x, y=y, cols=cols))
+        y.zero_()
+        r = fs.run(table, 64 * KiB, dst, consumer=Consumer("gemv_f32", x=x, y=y, cols=cols))
+        out["gread_fused_gemv_gbps"] = round(gbps(total, r.stats["kernel_ns"] / 1e9), 3)
+        # unfused: the same pass, then a separate GEMV over the user buffer
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        t0 = time.perf_counter()
+        r = fs.run(table, 64 * KiB, dst)
+        A = ((dst[:total].view(torch.int32) >> 8) & 0xFFFFFF).to(torch.float32).mul_(1.0 / 16777216)
+        ev[0].record()
+        y2 = A.view(rows, cols) @ x
+        ev[1].record()
+        torch.cuda.synchronize(device)
+        mv_s = ev[0].elapsed_time(ev[1]) / 1e3
+        out["gread_then_gemv_gbps"] = round(gbps(total, r.stats["kernel_ns"] / 1e9 + mv_s), 3)
+        out["max_rel_err_vs_unfused"] = float(((y - y2).abs().max() / y2.abs().max()).item())
+        out["shape"] = f"{rows}x{cols} f32 from {total} file bytes, {n_tb} TBs, 64 KiB requests"
+        del A
+    return out
 
 
 if __name__ == "__main__":
