@@ -230,10 +230,14 @@ static void worker_main(gfs_ctx* ctx, int wid) {
   const uint32_t mask = ctx->ring_size - 1;
   const bool dma = ctx->cfg.transfer == GFS_XFER_DMA;
   const bool bounce = ctx->cfg.transfer == GFS_XFER_BOUNCE;
-  const bool mapped = ctx->cfg.transfer == GFS_XFER_MAPPED;        // copy engine from the mapping
+  const bool hybrid = ctx->cfg.transfer == GFS_XFER_MAPPED_HYBRID;
+  const bool mapped_ce = ctx->cfg.transfer == GFS_XFER_MAPPED;     // copy engine from the mapping
   const bool mapped_zc = ctx->cfg.transfer == GFS_XFER_MAPPED_ZC;  // the CTA pulls it itself
-  cudaStream_t st =
-      (dma || mapped) ? ctx->worker_streams[(size_t)wid % ctx->worker_streams.size()] : nullptr;
+  const bool from_map = mapped_ce || mapped_zc || hybrid;
+  const int64_t ce_min = 1 << 20;  // hybrid: spans this large go by copy engine
+  cudaStream_t st = (dma || mapped_ce || hybrid)
+                        ? ctx->worker_streams[(size_t)wid % ctx->worker_streams.size()]
+                        : nullptr;
   if (st) cudaSetDevice(ctx->cfg.device);
   uint64_t nreq = 0;
   while (!ctx->stop.load(std::memory_order_relaxed)) {
@@ -280,7 +284,7 @@ static void worker_main(gfs_ctx* ctx, int wid) {
       }
       ctx->bounce_last[b] = seq;
       buf = ctx->h_bounce + (int64_t)b * ctx->slot_bytes;
-    } else if (mapped || mapped_zc) {
+    } else if (from_map) {
       buf = nullptr;
     } else {
       buf = ctx->h_staging + (int64_t)slot * ctx->slot_bytes;
@@ -290,7 +294,7 @@ static void worker_main(gfs_ctx* ctx, int wid) {
                      !ctx->files[fid].open || size > ctx->slot_bytes;
     if (bad) {
       n = -EINVAL;
-    } else if (mapped || mapped_zc) {  // no read at all: the span comes from the pinned mapping
+    } else if (from_map) {  // no read at all: the span comes from the pinned mapping
       const HostFile& f = ctx->files[fid];
       n = off >= f.size ? 0 : std::min(size, f.size - off);
       buf = f.map + off;
@@ -303,7 +307,7 @@ static void worker_main(gfs_ctx* ctx, int wid) {
     if (n < 0) ctx->worker_error.store((int)-n);
     // count it before completing: a launch that starts after this completion must see it
     __atomic_fetch_add(ctx->h_served, 1ull, __ATOMIC_SEQ_CST);
-    if (dma || mapped) {
+    if (dma || mapped_ce || (hybrid && n >= ce_min)) {
       cudaError_t ce = cudaSuccess;
       if (n > 0) {
         ce = cudaMemcpyAsync(ctx->d_landing + (int64_t)slot * ctx->slot_bytes, buf, (size_t)n,
@@ -325,7 +329,7 @@ static void worker_main(gfs_ctx* ctx, int wid) {
     } else {
       RpcResp* r = &ctx->h_resp[slot];
       r->nbytes = n;
-      r->buf = mapped_zc ? -1 : b;
+      r->buf = (mapped_zc || hybrid) ? -1 : b;
       if (bounce && n <= 0) ctx->bounce_last[b] = 0;  // nothing to pull: buffer stays free
       __atomic_store_n(&r->seq, seq, __ATOMIC_RELEASE);
     }
@@ -484,7 +488,8 @@ extern "C" int gfs_create(const gfs_config* cfg_in, gfs_ctx** out) {
   memset(ctx->h_resp, 0, (size_t)ctx->n_ctas * sizeof(RpcResp));
   TRY(cudaHostAlloc(&ctx->h_served, 64, cudaHostAllocMapped | cudaHostAllocPortable));
   memset(ctx->h_served, 0, 64);
-  if (cfg.transfer == GFS_XFER_DMA || cfg.transfer == GFS_XFER_MAPPED) {
+  if (cfg.transfer == GFS_XFER_DMA || cfg.transfer == GFS_XFER_MAPPED ||
+      cfg.transfer == GFS_XFER_MAPPED_HYBRID) {
     TRY(cudaMalloc(&ctx->d_landing, (size_t)(ctx->n_ctas * ctx->slot_bytes)));
     TRY(cudaMalloc(&ctx->d_doorbell, (size_t)ctx->n_ctas * 8));
     TRY(cudaMemset(ctx->d_doorbell, 0, (size_t)ctx->n_ctas * 8));
@@ -553,7 +558,8 @@ extern "C" int gfs_gopen(gfs_ctx* ctx, const char* path, int flags, int64_t cont
       return fail(GFS_ECUDA, "page table for %s: %s", path, cudaGetErrorString(e));
     }
   }
-  if ((ctx->cfg.transfer == GFS_XFER_MAPPED || ctx->cfg.transfer == GFS_XFER_MAPPED_ZC) && f.size > 0) {
+  if ((ctx->cfg.transfer == GFS_XFER_MAPPED || ctx->cfg.transfer == GFS_XFER_MAPPED_ZC ||
+       ctx->cfg.transfer == GFS_XFER_MAPPED_HYBRID) && f.size > 0) {
     // memory-resident file: pin its page-cache pages once so the daemon can DMA spans
     // straight out of them (tmpfs/shmem allows long-term pins; disk files do not)
     void* m = mmap(nullptr, (size_t)f.size, PROT_READ, MAP_SHARED | MAP_POPULATE, f.fd_buffered, 0);
@@ -862,7 +868,7 @@ extern "C" int gfs_run_consume(gfs_ctx* ctx, const gfs_program* prog, void* dst,
     const char* what = g.error < 9 ? names[g.error] : "unknown";
     int werr = ctx->worker_error.load();
     std::string diag;
-    if (g.error == ERR_TIMEOUT && (g.error_info == 21 || g.error_info == 22)) {
+    if (g.error == ERR_TIMEOUT && g.error_info >= 21 && g.error_info <= 23) {
       // a request never completed: say where it is (ring entry, mailbox/doorbell, workers)
       const int slot = (int)(g.error_arg >> 32);
       const uint32_t seq = (uint32_t)g.error_arg;

@@ -504,6 +504,33 @@ __device__ int64_t rpc_call(const DevCtx& c, Smem& s, int64_t fid, int64_t off, 
       }
       __nanosleep(256);
     }
+  } else if (c.transfer == GFS_XFER_MAPPED_HYBRID) {
+    // the daemon answers either by copy engine (doorbell in HBM, data already in the landing
+    // slot) or by mailbox (the CTA pulls the span from the pinned page-cache mapping)
+    const unsigned long long* bell = &c.doorbell[slot];
+    const RpcResp* r = &c.resp[slot];
+    for (int it = 0;; it++) {
+      const uint64_t v = ld_acquire_sys64(bell);
+      if ((uint32_t)v == seq) {
+        n = (int64_t)(v >> 32);
+        if (n == 0xFFFFFFFFll) n = -1;
+        break;
+      }
+      if ((it & 3) == 0 && ld_acquire_sys(&r->seq) == seq) {
+        n = *(volatile const int64_t*)&r->nbytes;
+        if (n > 0) {
+          s.pull_n = n;
+          s.pull_buf = -1;
+          s.pull_src = c.files[fid].map + off;
+        }
+        break;
+      }
+      if (!keep_waiting(c, t0, 23)) {
+        c.g->error_arg = ((unsigned long long)slot << 32) | seq;
+        return -1;
+      }
+      __nanosleep(1000);
+    }
   } else {
     const RpcResp* r = &c.resp[slot];
     __nanosleep(2000);

@@ -17,7 +17,8 @@ LIB_PATH = os.path.join(PKG, "_lib", "libgfs.so")
 
 POLICY = {"global-lru-dealloc": 0, "per-tb-lra": 1}
 READAHEAD = {"static": 0, "adaptive": 1}
-TRANSFER = {"zerocopy": 0, "dma": 1, "bounce": 2, "mapped_dma": 3, "mapped": 4}
+TRANSFER = {"zerocopy": 0, "dma": 1, "bounce": 2, "mapped_dma": 3, "mapped": 4,
+            "mapped_hybrid": 5}
 O_RDONLY, O_RDWR = 0, 2
 LOG_DELIVERIES, LOG_RPCS, LOG_VICTIMS, LOG_WINDOWS = 0, 1, 2, 3
 LOG_WIDTH = {LOG_DELIVERIES: 3, LOG_RPCS: 4, LOG_VICTIMS: 3, LOG_WINDOWS: 2}
