@@ -127,12 +127,22 @@ class Dist:
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
         self.pg = None
+        self.tdev = "cpu"
+        # GFS_BENCH_SHARE_GPU=1: ranks share the visible GPUs (functional check of the
+        # multi-rank path on a 1-GPU box; NCCL refuses duplicate devices, so gloo then)
+        self.share = os.environ.get("GFS_BENCH_SHARE_GPU") == "1"
         if self.world > 1:
             import torch
             import torch.distributed as dist
+            if self.share:
+                self.local = self.local % max(1, torch.cuda.device_count())
             torch.cuda.set_device(self.local)
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            if self.share:
+                dist.init_process_group("gloo")
+            else:
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+                self.tdev = f"cuda:{self.local}"
             self.pg = dist
 
     def barrier(self):
@@ -143,7 +153,7 @@ class Dist:
         if not self.pg:
             return vals
         import torch
-        t = torch.tensor(vals, dtype=torch.float64, device=f"cuda:{self.local}")
+        t = torch.tensor(vals, dtype=torch.float64, device=self.tdev)
         self.pg.all_reduce(t, op=getattr(self.pg.ReduceOp, op))
         return t.tolist()
 
@@ -153,7 +163,7 @@ class Dist:
             return v
         import torch
         t = torch.tensor([v - (1 << 64) if v >= (1 << 63) else v], dtype=torch.int64,
-                         device=f"cuda:{self.local}")
+                         device=self.tdev)
         self.pg.all_reduce(t)
         return int(t.item()) & ((1 << 64) - 1)
 

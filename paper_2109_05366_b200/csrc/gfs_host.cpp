@@ -96,17 +96,63 @@ struct HostFile {
   int read_only = 1;
   int64_t content_id = -1;
   uint32_t* d_pt = nullptr;
-  uint8_t* map = nullptr;   // mapped modes: pinned mapping of the whole file (host address)
+  uint8_t* map = nullptr;   // mapped modes: pinned mapping of [map_lo, map_lo + map_len)
   uint8_t* dmap = nullptr;  // and its device address
+  int64_t map_lo = 0, map_len = 0;
   bool open = false;
 };
 
 static void unmap_file(HostFile& f) {
   if (f.map) {
     cudaHostUnregister(f.map);
-    munmap(f.map, (size_t)f.size);
-    f.map = nullptr;
+    munmap(f.map, (size_t)f.map_len);
+    f.map = f.dmap = nullptr;
+    f.map_lo = f.map_len = 0;
   }
+}
+
+// Mapped transfers: pin the page-cache pages of [lo, hi) of a memory-resident file (tmpfs
+// allows long-term pins of shmem pages; disk files do not) so spans can be pulled / DMA'd
+// straight out of them.  Only the range a run reads is mapped (a rank maps its shard).
+static int map_range(HostFile& f, int64_t lo, int64_t hi) {
+  lo &= ~(int64_t)((2 << 20) - 1);
+  hi = std::min(f.size, (hi + (2 << 20) - 1) & ~(int64_t)((2 << 20) - 1));
+  if (f.map && f.map_lo <= lo && f.map_lo + f.map_len >= hi) return GFS_OK;
+  unmap_file(f);
+  const size_t len = (size_t)(hi - lo);
+  void* m = mmap(nullptr, len, PROT_READ, MAP_SHARED | MAP_POPULATE, f.fd_buffered, (off_t)lo);
+  cudaError_t e = m == MAP_FAILED
+                      ? cudaErrorInvalidValue
+                      : cudaHostRegister(m, len, cudaHostRegisterReadOnly | cudaHostRegisterPortable |
+                                                     cudaHostRegisterMapped);
+  if (m != MAP_FAILED && e != cudaSuccess) {
+    // platforms without read-only registration: pin a shared read-write mapping of the
+    // same pages (never written through; needs write permission on the file)
+    cudaGetLastError();
+    munmap(m, len);
+    int rw = open(f.path.c_str(), O_RDWR);
+    m = rw < 0 ? MAP_FAILED
+               : mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_SHARED | MAP_POPULATE, rw, (off_t)lo);
+    if (rw >= 0) close(rw);
+    e = m == MAP_FAILED ? cudaErrorInvalidValue
+                        : cudaHostRegister(m, len, cudaHostRegisterPortable | cudaHostRegisterMapped);
+  }
+  if (m == MAP_FAILED || e != cudaSuccess) {
+    cudaGetLastError();  // do not leave a sticky error for the next launch check
+    if (m != MAP_FAILED) munmap(m, len);
+    return fail(GFS_EIO, "mapped transfers need a memory-resident file (tmpfs); %s: %s",
+                f.path.c_str(), m == MAP_FAILED ? strerror(errno) : cudaGetErrorString(e));
+  }
+  void* dp = nullptr;
+  if (cudaHostGetDevicePointer(&dp, m, 0) != cudaSuccess) {
+    cudaGetLastError();
+    dp = m;  // UVA: the host address is the device address
+  }
+  f.map = (uint8_t*)m;
+  f.dmap = (uint8_t*)dp;
+  f.map_lo = lo;
+  f.map_len = (int64_t)len;
+  return GFS_OK;
 }
 
 template <typename T>
@@ -297,7 +343,7 @@ static void worker_main(gfs_ctx* ctx, int wid) {
     } else if (from_map) {  // no read at all: the span comes from the pinned mapping
       const HostFile& f = ctx->files[fid];
       n = off >= f.size ? 0 : std::min(size, f.size - off);
-      buf = f.map + off;
+      buf = f.map + (off - f.map_lo);
     } else {
       n = do_pread(ctx, ctx->files[fid], off, size, buf);
     }
@@ -558,43 +604,6 @@ extern "C" int gfs_gopen(gfs_ctx* ctx, const char* path, int flags, int64_t cont
       return fail(GFS_ECUDA, "page table for %s: %s", path, cudaGetErrorString(e));
     }
   }
-  if ((ctx->cfg.transfer == GFS_XFER_MAPPED || ctx->cfg.transfer == GFS_XFER_MAPPED_ZC ||
-       ctx->cfg.transfer == GFS_XFER_MAPPED_HYBRID) && f.size > 0) {
-    // memory-resident file: pin its page-cache pages once so the daemon can DMA spans
-    // straight out of them (tmpfs/shmem allows long-term pins; disk files do not)
-    void* m = mmap(nullptr, (size_t)f.size, PROT_READ, MAP_SHARED | MAP_POPULATE, f.fd_buffered, 0);
-    cudaError_t e = m == MAP_FAILED ? cudaErrorInvalidValue
-                                    : cudaHostRegister(m, (size_t)f.size,
-                                                       cudaHostRegisterReadOnly | cudaHostRegisterPortable | cudaHostRegisterMapped);
-    if (m != MAP_FAILED && e != cudaSuccess) {
-      // platforms without read-only registration: pin a shared read-write mapping of the
-      // same pages (never written through; needs write permission on the file)
-      cudaGetLastError();
-      munmap(m, (size_t)f.size);
-      int rw = open(path, O_RDWR);
-      m = rw < 0 ? MAP_FAILED
-                 : mmap(nullptr, (size_t)f.size, PROT_READ | PROT_WRITE, MAP_SHARED | MAP_POPULATE, rw, 0);
-      if (rw >= 0) close(rw);
-      e = m == MAP_FAILED ? cudaErrorInvalidValue
-                          : cudaHostRegister(m, (size_t)f.size, cudaHostRegisterPortable | cudaHostRegisterMapped);
-    }
-    if (m == MAP_FAILED || e != cudaSuccess) {
-      cudaGetLastError();  // do not leave a sticky error for the next launch check
-      if (m != MAP_FAILED) munmap(m, (size_t)f.size);
-      if (f.d_pt) cudaFree(f.d_pt);
-      close(f.fd_buffered);
-      if (f.fd_direct >= 0) close(f.fd_direct);
-      return fail(GFS_EIO, "io.transfer=mapped needs a memory-resident file (tmpfs); %s: %s", path,
-                  m == MAP_FAILED ? strerror(errno) : cudaGetErrorString(e));
-    }
-    f.map = (uint8_t*)m;
-    void* dp = nullptr;
-    if (cudaHostGetDevicePointer(&dp, m, 0) != cudaSuccess) {
-      cudaGetLastError();
-      dp = m;  // UVA: the host address is the device address
-    }
-    f.dmap = (uint8_t*)dp;
-  }
   f.open = true;
   ctx->files.push_back(f);
   *fid = (int)ctx->files.size() - 1;
@@ -635,7 +644,7 @@ static int upload_files(gfs_ctx* ctx) {
     df[i].npages = f.npages;
     df[i].read_only = f.read_only;
     df[i].content_id = (int32_t)f.content_id;
-    df[i].map = f.dmap;
+    df[i].map = f.dmap ? f.dmap - f.map_lo : nullptr;  // map + file offset = device address
   }
   CUDA_TRY(ctx->d_files.reserve(std::max<size_t>(df.size(), 1)));
   if (!df.empty())
@@ -726,6 +735,19 @@ extern "C" int gfs_run_consume(gfs_ctx* ctx, const gfs_program* prog, void* dst,
   int rc = validate_program(ctx, prog, dst_bytes, dst != nullptr);
   if (rc) return rc;
   if ((rc = validate_consumer(cons, prog, dst != nullptr))) return rc;
+  const int xfer = ctx->cfg.transfer;
+  if (xfer == GFS_XFER_MAPPED || xfer == GFS_XFER_MAPPED_ZC || xfer == GFS_XFER_MAPPED_HYBRID) {
+    // pin what this run can touch: its segments plus one span of read-ahead past each end
+    std::vector<int64_t> lo(ctx->files.size(), INT64_MAX), hi(ctx->files.size(), -1);
+    for (int64_t s = 0; s < prog->prog_off[prog->n_tb]; s++) {
+      const int64_t fid = prog->segs[3 * s], off = prog->segs[3 * s + 1], len = prog->segs[3 * s + 2];
+      lo[fid] = std::min(lo[fid], off);
+      hi[fid] = std::max(hi[fid], off + len + ctx->slot_bytes);
+    }
+    for (size_t f = 0; f < ctx->files.size(); f++)
+      if (hi[f] > lo[f] && ctx->files[f].open && ctx->files[f].size > 0 && lo[f] < ctx->files[f].size)
+        if ((rc = map_range(ctx->files[f], lo[f], hi[f]))) return rc;
+  }
   CUDA_TRY(cudaSetDevice(ctx->cfg.device));
   const gfs_config& cfg = ctx->cfg;
   int64_t n_segs = 0;
