@@ -1334,10 +1334,22 @@ __device__ void consume(const DevCtx& c, const uint8_t* data, int64_t n, int64_t
       const int64_t e = e0 + 4 * i;
       const int64_t row = e / M, col = e - row * M;  // cols % 4 == 0: one row per vector
       const float4 xv = *(const float4*)(k.x + col);
-      const float p = decode_f32(u.x) * xv.x + decode_f32(u.y) * xv.y + decode_f32(u.z) * xv.z +
-                      decode_f32(u.w) * xv.w;
-      if (local) atomicAdd(&rows[row - row_lo], p);
-      else atomicAdd(&k.y[row], p);
+      float p = decode_f32(u.x) * xv.x + decode_f32(u.y) * xv.y + decode_f32(u.z) * xv.z +
+                decode_f32(u.w) * xv.w;
+      // a warp's 32 consecutive vectors usually share one row: reduce them first
+      const unsigned active = __activemask();
+      const int64_t row0 = __shfl_sync(active, row, __ffs(active) - 1);
+      if (active == 0xffffffffu && __all_sync(active, row == row0)) {
+        for (int o = 16; o > 0; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
+        if ((threadIdx.x & 31) == 0) {
+          if (local) atomicAdd(&rows[row - row_lo], p);
+          else atomicAdd(&k.y[row], p);
+        }
+      } else if (local) {
+        atomicAdd(&rows[row - row_lo], p);
+      } else {
+        atomicAdd(&k.y[row], p);
+      }
     }
     __syncthreads();
     if (local)
