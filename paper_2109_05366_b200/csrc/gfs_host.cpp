@@ -215,7 +215,9 @@ struct gfs_ctx {
 
   // daemon
   std::vector<std::thread> workers;
-  std::vector<cudaStream_t> worker_streams;
+  std::vector<cudaStream_t> worker_streams;  // copy streams (shared by the workers)
+  std::vector<cudaStream_t> bell_streams;    // doorbell streams
+  std::vector<cudaEvent_t> bell_ev;          // per worker: "this copy is done"
   // DMA mode: per-worker pinned bounce buffers, few and small enough to stay resident in
   // the host LLC (pread writes them, the copy engine reads them right after)
   int nbounce = 0;
@@ -365,12 +367,18 @@ static void worker_main(gfs_ctx* ctx, int wid) {
         n = -EIO;
       }
       uint64_t v = ((uint64_t)(n < 0 ? 0xFFFFFFFFull : (uint64_t)n) << 32) | seq;
-      CUresult cr = ctx->write_value64((CUstream)st, (CUdeviceptr)(ctx->d_doorbell + slot), (cuuint64_t)v, 0);
+      // The doorbell goes on a separate stream that waits for this copy: copy streams then
+      // carry back-to-back copies only, so the engine never idles behind a memory op.
+      cudaStream_t bs = ctx->bell_streams[(size_t)wid % ctx->bell_streams.size()];
+      cudaEventRecord(ctx->bell_ev[wid], st);
+      cudaStreamWaitEvent(bs, ctx->bell_ev[wid], 0);
+      CUresult cr = ctx->write_value64((CUstream)bs, (CUdeviceptr)(ctx->d_doorbell + slot), (cuuint64_t)v, 0);
       if (cr != CUDA_SUCCESS) ctx->worker_error.store(EIO);
       // The driver may hold freshly enqueued work in its push buffer until the next call on
       // the stream; this worker may not make one for a while (it spins on the ring), and
-      // the persistent kernel is waiting on exactly this doorbell.  Kick the stream.
+      // the persistent kernel is waiting on exactly this doorbell.  Kick both streams.
       cudaStreamQuery(st);
+      cudaStreamQuery(bs);
       ctx->t_xfer.fetch_add((int64_t)(now_ns() - t1), std::memory_order_relaxed);
     } else {
       RpcResp* r = &ctx->h_resp[slot];
@@ -404,6 +412,10 @@ static void free_all(gfs_ctx* ctx) {
   ctx->files.clear();
   for (auto s : ctx->worker_streams)
     if (s) cudaStreamDestroy(s);
+  for (auto s : ctx->bell_streams)
+    if (s) cudaStreamDestroy(s);
+  for (auto ev : ctx->bell_ev)
+    if (ev) cudaEventDestroy(ev);
   void* dev[] = {ctx->d_frames, ctx->d_fkey, ctx->d_fstate, ctx->d_own_q, ctx->d_retired,
                  ctx->d_gfifo, ctx->d_recycled, ctx->d_g, ctx->d_landing, ctx->d_doorbell,
                  ctx->d_done_pos, ctx->d_stats, ctx->d_scratch};
@@ -547,8 +559,12 @@ extern "C" int gfs_create(const gfs_config* cfg_in, gfs_ctx** out) {
     ctx->write_value64 = (CUresult(*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int))fn;
     // a few copy streams shared by the workers (streams are thread-safe): every extra
     // stream risks sharing a hardware queue with the persistent kernel's stream
-    ctx->worker_streams.resize((size_t)std::min(cfg.io_workers, 4), nullptr);
+    ctx->worker_streams.resize((size_t)std::min(cfg.io_workers, 2), nullptr);
     for (auto& s : ctx->worker_streams) TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    ctx->bell_streams.resize((size_t)std::min(cfg.io_workers, 2), nullptr);
+    for (auto& s : ctx->bell_streams) TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    ctx->bell_ev.resize((size_t)cfg.io_workers, nullptr);
+    for (auto& ev : ctx->bell_ev) TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   }
   if (cfg.transfer == GFS_XFER_DMA) {
     // ~48 MiB of bounce buffers in total (LLC-sized), at least 2 per worker
