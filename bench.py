@@ -193,6 +193,27 @@ def shard_table(cfg, rank: int):
     return wl, ProgramTable.from_programs(wl.programs)
 
 
+def fit_size(directory: str, size: int, n: int) -> int:
+    """Bytes per GPU such that the n-shard file fits the file system holding it (an
+    existing file of the right size counts as free); whole GiB, at least 1 GiB.  Logged
+    when it has to shrink the shard."""
+    from paper_2109_05366_b200.runtime import SYNTH_VERSION  # noqa: F401
+    try:
+        st = os.statvfs(directory)
+    except OSError:
+        return size
+    free = st.f_bavail * st.f_frsize
+    existing = os.path.join(directory, f"gfs_synth_c0_{size * n}.bin")
+    if os.path.exists(existing):
+        free += os.path.getsize(existing)
+    if size * n + GiB <= free:
+        return size
+    fit = max(GiB, (free - GiB) // n // GiB * GiB)
+    print(f"bench: {directory} has {free / GiB:.1f} GiB free; shard shrunk to {fit / GiB:.0f} GiB/GPU",
+          file=sys.stderr)
+    return fit
+
+
 def ensure_file(cfg, dist: Dist) -> str:
     from paper_2109_05366_b200.runtime import ensure_synthetic
     d, size = cfg["io.dir"], cfg["workload.file_bytes"]
@@ -374,7 +395,7 @@ def main() -> None:
     native.load()
     device = dist.local
     torch.cuda.set_device(device)
-    size = int(args.size_gib * GiB)
+    size = fit_size(args.dir, int(args.size_gib * GiB), dist.world)
     cfg = make_cfg({**headline_overrides(size, dist.world, args.dir), "gpu.device": device}, args.set)
     path = ensure_file(cfg, dist)
 
