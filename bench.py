@@ -395,7 +395,8 @@ def main() -> None:
     native.load()
     device = dist.local
     torch.cuda.set_device(device)
-    size = fit_size(args.dir, int(args.size_gib * GiB), dist.world)
+    dist.barrier()  # every rank sizes the shard before rank 0 starts writing the file
+    size = int(dist.reduce([float(fit_size(args.dir, int(args.size_gib * GiB), dist.world))], "MIN")[0])
     cfg = make_cfg({**headline_overrides(size, dist.world, args.dir), "gpu.device": device}, args.set)
     path = ensure_file(cfg, dist)
 
