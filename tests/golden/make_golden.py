@@ -177,9 +177,26 @@ def run_case(name, overrides, seed, order, vorder):
     return out
 
 
+def fuzz_cases() -> dict:
+    """The randomised resident_limit-1 cases of tests/test_gpu_fuzz.py that the reference
+    can express (static readahead; the io.* keys are the B200 layer's own)."""
+    sys.path.insert(0, os.path.dirname(HERE))
+    sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+    from test_gpu_fuzz import N_CASES, random_case
+    out = {}
+    for k in range(N_CASES):
+        over = random_case(k)
+        if over["io.readahead"] != "static":
+            continue
+        seed = over.pop("seed")
+        over = {kk: v for kk, v in over.items() if not kk.startswith("io.")}
+        out[f"fuzz_{k:02d}"] = (over, seed, "global", "global")
+    return out
+
+
 def main():
     only = set(sys.argv[1:])
-    for name, (over, seed, order, vorder) in CASES.items():
+    for name, (over, seed, order, vorder) in {**CASES, **fuzz_cases()}.items():
         if only and name not in only:
             continue
         res = run_case(name, over, seed, order, vorder)
