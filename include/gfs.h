@@ -58,6 +58,7 @@ typedef struct gfs_config {
   int64_t prefetch_bytes;  /* gpufs.prefetch_bytes */
   int64_t staging_bytes;   /* rpc.staging_bytes: PCIe batch size (accounting, rpc.py:31-55) */
   int64_t ra_max_bytes;    /* io.ra_max_bytes: adaptive window cap */
+  int64_t ra_init_bytes;   /* io.ra_init_bytes: adaptive first window (0 = page + prefetch) */
   int64_t max_request_bytes; /* largest gread request (raw mode sizes staging to it) */
   int32_t policy;          /* GFS_POLICY_* */
   int32_t resident_limit;  /* reference residency (gpu_exec.py:44-50): sets the LRA quota */

@@ -424,6 +424,8 @@ static int64_t rpc_span(orc_run* r, int tb, int64_t fid, int64_t page, int64_t s
   int64_t want = (ro && pf > 0) ? pg + pf : pg;
   if (r->cfg.readahead == ORC_RA_ADAPTIVE && ro) {
     int64_t base = pg + pf;
+    int64_t init = r->cfg.ra_init_bytes < r->cfg.ra_max_bytes ? r->cfg.ra_init_bytes : r->cfg.ra_max_bytes;
+    if (init > base) base = init; /* io.ra_init_bytes: a larger first window */
     if (r->ra_win > 0 && fid == r->ra_next_fid && page == r->ra_next_page) {
       r->ra_win = 2 * r->ra_win;
       if (r->ra_win > r->cfg.ra_max_bytes) r->ra_win = r->cfg.ra_max_bytes;

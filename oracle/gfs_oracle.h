@@ -30,6 +30,7 @@ enum { ORC_LOG_DELIVERIES = 0, ORC_LOG_RPCS = 1, ORC_LOG_VICTIMS = 2, ORC_LOG_WI
 
 typedef struct {
   int64_t page_size, cache_bytes, prefetch_bytes, request_bytes, staging_bytes, ra_max_bytes;
+  int64_t ra_init_bytes; /* adaptive first window (0 = page + prefetch) */
   int32_t policy, resident_limit, raw_mode, readahead, pcie_disabled, log;
   int32_t n_files, n_tb;
   const int64_t* file_sizes;   /* n_files */

@@ -31,6 +31,7 @@ class OrcCfg(C.Structure):
     _fields_ = [
         ("page_size", C.c_int64), ("cache_bytes", C.c_int64), ("prefetch_bytes", C.c_int64),
         ("request_bytes", C.c_int64), ("staging_bytes", C.c_int64), ("ra_max_bytes", C.c_int64),
+        ("ra_init_bytes", C.c_int64),
         ("policy", C.c_int32), ("resident_limit", C.c_int32), ("raw_mode", C.c_int32),
         ("readahead", C.c_int32), ("pcie_disabled", C.c_int32), ("log", C.c_int32),
         ("n_files", C.c_int32), ("n_tb", C.c_int32),
@@ -133,6 +134,7 @@ def run_oracle(cfg, workload, *, source: int = SRC_NONE, paths=None, io_direct: 
     c.request_bytes = workload.request_bytes
     c.staging_bytes = cfg["rpc.staging_bytes"]
     c.ra_max_bytes = cfg.ra_max()
+    c.ra_init_bytes = cfg.ra_init()
     c.policy = 1 if cfg["gpufs.policy"] == "per-tb-lra" else 0
     c.resident_limit = cfg.resident_limit()
     c.raw_mode = int(bool(cfg["mode.gpu_cache_disabled"]))

@@ -355,9 +355,10 @@ static void worker_main(gfs_ctx* ctx, int wid) {
     if (n < 0) ctx->worker_error.store((int)-n);
     // count it before completing: a launch that starts after this completion must see it
     __atomic_fetch_add(ctx->h_served, 1ull, __ATOMIC_SEQ_CST);
-    if (dma || mapped_ce || (hybrid && n >= ce_min)) {
+    if (dma || mapped_ce || hybrid) {
+      const bool copy = !hybrid || n >= ce_min;  // hybrid: small spans are pulled by the CTA
       cudaError_t ce = cudaSuccess;
-      if (n > 0) {
+      if (n > 0 && copy) {
         ce = cudaMemcpyAsync(ctx->d_landing + (int64_t)slot * ctx->slot_bytes, buf, (size_t)n,
                              cudaMemcpyHostToDevice, st);
         if (ce == cudaSuccess && dma) ce = cudaEventRecord(ctx->bounce_ev[b], st);
@@ -367,11 +368,14 @@ static void worker_main(gfs_ctx* ctx, int wid) {
         n = -EIO;
       }
       uint64_t v = ((uint64_t)(n < 0 ? 0xFFFFFFFFull : (uint64_t)n) << 32) | seq;
+      if (!copy) v |= 1ull << 63;  // "not copied: pull it from the mapping"
       // The doorbell goes on a separate stream that waits for this copy: copy streams then
       // carry back-to-back copies only, so the engine never idles behind a memory op.
       cudaStream_t bs = ctx->bell_streams[(size_t)wid % ctx->bell_streams.size()];
-      cudaEventRecord(ctx->bell_ev[wid], st);
-      cudaStreamWaitEvent(bs, ctx->bell_ev[wid], 0);
+      if (copy) {
+        cudaEventRecord(ctx->bell_ev[wid], st);
+        cudaStreamWaitEvent(bs, ctx->bell_ev[wid], 0);
+      }
       CUresult cr = ctx->write_value64((CUstream)bs, (CUdeviceptr)(ctx->d_doorbell + slot), (cuuint64_t)v, 0);
       if (cr != CUDA_SUCCESS) ctx->worker_error.store(EIO);
       // The driver may hold freshly enqueued work in its push buffer until the next call on
@@ -455,6 +459,8 @@ extern "C" int gfs_create(const gfs_config* cfg_in, gfs_ctx** out) {
     return fail(GFS_EINVAL, "unknown policy %d", cfg.policy);
   if (cfg.readahead == GFS_RA_ADAPTIVE && (cfg.ra_max_bytes < cfg.page_size || cfg.ra_max_bytes % cfg.page_size))
     return fail(GFS_EINVAL, "ra_max_bytes must be a positive multiple of page_size");
+  if (cfg.ra_init_bytes < 0 || cfg.ra_init_bytes % cfg.page_size)
+    return fail(GFS_EINVAL, "ra_init_bytes must be 0 or a multiple of page_size");
   if (cfg.cta_threads != 128 && cfg.cta_threads != 256 && cfg.cta_threads != 512) cfg.cta_threads = 256;
   if (cfg.io_workers < 1) cfg.io_workers = 1;
   if (cfg.io_workers > 256) cfg.io_workers = 256;
@@ -806,6 +812,7 @@ extern "C" int gfs_run_consume(gfs_ctx* ctx, const gfs_program* prog, void* dst,
   c.page_size = cfg.page_size;
   c.prefetch_bytes = cfg.prefetch_bytes;
   c.ra_max_bytes = cfg.ra_max_bytes;
+  c.ra_init_bytes = std::min(cfg.ra_init_bytes, cfg.ra_max_bytes);
   c.pb_cap_bytes = ctx->pb_cap;
   c.slot_bytes = ctx->slot_bytes;
   c.staging_bytes = cfg.staging_bytes;

@@ -119,7 +119,9 @@ struct Smem {
     int64_t src_off[32];
     int32_t vict[32];  // 1 = frame must be evicted before reuse
   } b;
-  int32_t pb_nb[MAX_PB_ENTRIES];
+  int64_t pb_last_nb;        // bytes of the last private-buffer entry
+  int64_t page_size_cached;  // c.page_size, for the smem-only pb_take
+  uint32_t pb_absent[MAX_PB_ENTRIES / 32];  // private-buffer entries consumed / dropped
 };
 
 enum { A_HIT = 1, A_PBHIT = 2, A_RPC = 3, A_ABORT = 4 };
@@ -369,39 +371,49 @@ __device__ int64_t page_bytes(const DevFile& F, int64_t pg, int64_t page) {
 // bytes stay in the slot's span buffer at (page - base) * pg.
 __device__ void pb_fill(const DevCtx& c, Smem& s, int64_t fid, int64_t base, int64_t m,
                         int64_t rest_bytes) {
+  // Entries 1..cnt-1 are whole pages and entry cnt holds the rest (short only at EOF), so
+  // the buffer is (count, last entry's bytes, an absent-bitmap) instead of a byte count per
+  // entry.  Fill order semantics of the reference: entries are offered in page order and
+  // one that does not fit the capacity is dropped (counted as discarded).
   ST(pb_discarded_bytes) += s.pb_filled;  // every unconsumed entry is stale
   s.pb_fid = fid;
   s.pb_base = base;
-  s.pb_filled = 0;
-  const DevFile& F = c.files[fid];
-  int64_t remaining = rest_bytes;
+  const int64_t pg = c.page_size;
   int64_t cnt = m - 1;
   if (cnt >= MAX_PB_ENTRIES) {
     set_error(c, ERR_PB, (int)cnt, 0);
     cnt = MAX_PB_ENTRIES - 1;
   }
-  for (int64_t i = 1; i <= cnt; i++) {
-    int64_t nb = page_bytes(F, c.page_size, base + i);
-    if (nb > remaining) nb = remaining;
-    remaining -= nb;
-    if (s.pb_filled + nb > c.pb_cap_bytes) {
-      ST(pb_discarded_bytes) += nb;  // no room, never served
-      s.pb_nb[i] = 0;
-      continue;
-    }
-    s.pb_nb[i] = (int32_t)nb;
-    s.pb_filled += nb;
-    ST(pb_filled_bytes) += nb;
-  }
+  const int64_t last = rest_bytes - (cnt - 1) * pg;
+  const int64_t kept_full = min(cnt - 1, c.pb_cap_bytes / pg);
+  int64_t filled = kept_full * pg;
+  const bool last_fits = filled + last <= c.pb_cap_bytes;
+  ST(pb_discarded_bytes) += (cnt - 1 - kept_full) * pg + (last_fits ? 0 : last);  // no room
+  if (last_fits) filled += last;
+  ST(pb_filled_bytes) += filled;
+  s.pb_filled = filled;
   s.pb_count = cnt;
+  s.pb_last_nb = last;
+  for (int64_t w = 0; w <= (cnt >> 5); w++) {  // bit set = entry absent
+    const int64_t lo = w << 5;
+    uint32_t present = 0;
+    const int64_t a = lo > 1 ? lo : 1, b = kept_full < lo + 31 ? kept_full : lo + 31;
+    if (a <= b) present = (b - a + 1 == 32 ? 0xFFFFFFFFu : ((1u << (b - a + 1)) - 1u)) << (a - lo);
+    if (last_fits && cnt >= lo && cnt <= lo + 31) present |= 1u << (cnt - lo);
+    s.pb_absent[w] = ~present;
+  }
+}
+
+__device__ __forceinline__ bool pb_present(const Smem& s, int64_t i) {
+  return !((s.pb_absent[i >> 5] >> (i & 31)) & 1u);
 }
 
 // prefetcher.py:52-61
 __device__ int64_t pb_take(Smem& s, int64_t fid, int64_t page) {
   int64_t i = page - s.pb_base;
-  if (s.pb_count > 0 && fid == s.pb_fid && i >= 1 && i <= s.pb_count && s.pb_nb[i] > 0) {
-    int64_t nb = s.pb_nb[i];
-    s.pb_nb[i] = 0;
+  if (s.pb_count > 0 && fid == s.pb_fid && i >= 1 && i <= s.pb_count && pb_present(s, i)) {
+    const int64_t nb = i == s.pb_count ? s.pb_last_nb : s.page_size_cached;
+    s.pb_absent[i >> 5] |= 1u << (i & 31);
     s.pb_filled -= nb;
     ST(pb_hits)++;
     ST(pb_consumed_bytes) += nb;
@@ -424,7 +436,7 @@ __device__ int64_t span_peek(const DevCtx& c, const Smem& s, int64_t fid, int64_
   const bool ro = F.read_only != 0;
   int64_t want = (ro && c.prefetch_bytes > 0) ? pg + c.prefetch_bytes : pg;
   if (c.readahead == GFS_RA_ADAPTIVE && ro) {
-    const int64_t base = pg + c.prefetch_bytes;
+    const int64_t base = c.ra_init_bytes > pg + c.prefetch_bytes ? c.ra_init_bytes : pg + c.prefetch_bytes;
     int64_t win = base;
     if (s.ra_win > 0 && fid == s.ra_next_fid && page == s.ra_next_page)
       win = 2 * s.ra_win < c.ra_max_bytes ? 2 * s.ra_win : c.ra_max_bytes;
@@ -507,18 +519,15 @@ __device__ int64_t rpc_call(const DevCtx& c, Smem& s, int64_t fid, int64_t off, 
   } else if (c.transfer == GFS_XFER_MAPPED_HYBRID) {
     // the daemon answers either by copy engine (doorbell in HBM, data already in the landing
     // slot) or by mailbox (the CTA pulls the span from the pinned page-cache mapping)
+    // (both answers arrive through the HBM doorbell, so nothing polls host memory: bit 63
+    // set = "not copied, pull it yourself")
     const unsigned long long* bell = &c.doorbell[slot];
-    const RpcResp* r = &c.resp[slot];
-    for (int it = 0;; it++) {
+    for (;;) {
       const uint64_t v = ld_acquire_sys64(bell);
       if ((uint32_t)v == seq) {
-        n = (int64_t)(v >> 32);
-        if (n == 0xFFFFFFFFll) n = -1;
-        break;
-      }
-      if ((it & 3) == 0 && ld_acquire_sys(&r->seq) == seq) {
-        n = *(volatile const int64_t*)&r->nbytes;
-        if (n > 0) {
+        n = (int64_t)((v >> 32) & 0x7FFFFFFFull);
+        if (n == 0x7FFFFFFFll) n = -1;
+        if ((v >> 63) && n > 0) {
           s.pull_n = n;
           s.pull_buf = -1;
           s.pull_src = c.files[fid].map + off;
@@ -529,7 +538,7 @@ __device__ int64_t rpc_call(const DevCtx& c, Smem& s, int64_t fid, int64_t off, 
         c.g->error_arg = ((unsigned long long)slot << 32) | seq;
         return -1;
       }
-      __nanosleep(1000);
+      __nanosleep(256);
     }
   } else {
     const RpcResp* r = &c.resp[slot];
@@ -680,7 +689,7 @@ __device__ int copy_page_in(uint8_t* frame, uint8_t* dst_whole, const uint8_t* s
 
 __device__ __forceinline__ bool pb_has(const Smem& s, int64_t fid, int64_t page) {
   const int64_t i = page - s.pb_base;
-  return s.pb_count > 0 && fid == s.pb_fid && i >= 1 && i <= s.pb_count && s.pb_nb[i] > 0;
+  return s.pb_count > 0 && fid == s.pb_fid && i >= 1 && i <= s.pb_count && pb_present(s, i);
 }
 
 // Reserve n consecutive log records (one atomic); ~0 when logging is off / full.
@@ -1384,6 +1393,8 @@ __device__ bool run_tb(const DevCtx& c, Smem& s, int tb, int& bad_words, ConsAcc
     s.pb_count = 0;
     s.pb_filled = 0;
     s.pb_fid = -1;
+    s.pb_last_nb = 0;
+    s.page_size_cached = c.page_size;
     s.pb_base = 0;
     s.ra_win = 0;
     s.ra_next_fid = -1;

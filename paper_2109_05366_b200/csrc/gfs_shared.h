@@ -14,7 +14,7 @@ constexpr uint32_t PT_INFLIGHT = 0x80000000u; // frame bound, data not installed
 constexpr uint32_t FR_VALID = 1u;             // frame state bit 0; refcount in bits 1..
 constexpr uint32_t FR_REF = 2u;
 constexpr uint32_t RING_TOMB = 0xFFFFFFFFu;   // global FIFO tombstone
-constexpr int MAX_PB_ENTRIES = 2048;          // private-buffer entries per TB (smem)
+constexpr int MAX_PB_ENTRIES = 16384;         // private-buffer entries per TB (smem bitmap)
 
 // Request record in the mapped request ring (device writes, host daemon reads).
 struct alignas(32) RpcReq {
@@ -72,6 +72,7 @@ struct DevCtx {
   int64_t page_size;
   int64_t prefetch_bytes;
   int64_t ra_max_bytes;
+  int64_t ra_init_bytes;     // adaptive first window (>= page + prefetch, <= ra_max)
   int64_t pb_cap_bytes;      // private-buffer capacity (bytes)
   int64_t slot_bytes;        // span buffer bytes per CTA slot
   int64_t staging_bytes;     // PCIe batch accounting unit

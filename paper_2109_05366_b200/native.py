@@ -34,7 +34,8 @@ EXPORTS = ["gfs_create", "gfs_destroy", "gfs_gopen", "gfs_gclose", "gfs_file_siz
 class GfsConfig(C.Structure):
     _fields_ = [
         ("page_size", C.c_int64), ("cache_bytes", C.c_int64), ("prefetch_bytes", C.c_int64),
-        ("staging_bytes", C.c_int64), ("ra_max_bytes", C.c_int64), ("max_request_bytes", C.c_int64),
+        ("staging_bytes", C.c_int64), ("ra_max_bytes", C.c_int64), ("ra_init_bytes", C.c_int64),
+        ("max_request_bytes", C.c_int64),
         ("policy", C.c_int32), ("resident_limit", C.c_int32), ("readahead", C.c_int32),
         ("transfer", C.c_int32), ("io_workers", C.c_int32), ("io_direct", C.c_int32),
         ("device", C.c_int32), ("cta_threads", C.c_int32), ("max_ctas", C.c_int32),

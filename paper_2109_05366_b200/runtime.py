@@ -42,6 +42,7 @@ def native_config(cfg: ExperimentConfig, max_request_bytes: int = 0) -> native.G
     c.prefetch_bytes = cfg["gpufs.prefetch_bytes"]
     c.staging_bytes = cfg["rpc.staging_bytes"]
     c.ra_max_bytes = cfg.ra_max()
+    c.ra_init_bytes = cfg.ra_init()
     c.max_request_bytes = max_request_bytes or cfg["workload.request_bytes"]
     c.policy = native.POLICY[cfg["gpufs.policy"]]
     c.resident_limit = cfg.resident_limit()

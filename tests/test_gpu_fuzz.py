@@ -46,6 +46,7 @@ def random_case(k: int) -> dict:
         "gpu.dispatch_order": ["round-robin", "shuffled", "reverse"][r.below(3)],
         "gpu.sm_count": 1, "gpu.max_threads_per_sm": 2048, "gpu.threads_per_tb": 2048,
         "io.transfer": TRANSFERS[k % len(TRANSFERS)], "seed": 7 + k,
+        "io.ra_init_bytes": page * r.below(6),
     }
 
 

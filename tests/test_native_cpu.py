@@ -49,8 +49,8 @@ def test_stat_names_match_oracle_counters(lib):
 
 
 def test_struct_sizes_match_header(lib):
-    # gfs_config: 6 int64 + 13 int32 + 3 reserved int32 = 48 + 64 = 112 bytes
-    assert C.sizeof(native.GfsConfig) == 112
+    # gfs_config: 7 int64 + 13 int32 + 3 reserved int32 = 56 + 64 = 120 bytes
+    assert C.sizeof(native.GfsConfig) == 120
     assert C.sizeof(native.GfsProgram) == 48
 
 
