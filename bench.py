@@ -30,6 +30,9 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# before any CUDA initialisation (torch.distributed/set_device run before the package
+# import): enough hardware queues that the daemon's copy streams never alias the kernel's
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 KiB, MiB, GiB = 1 << 10, 1 << 20, 1 << 30
 METRIC = "sequential gread GB/s per GPU & box (1/2/4/8) vs PCIe H2D/storage roofline"
