@@ -102,6 +102,23 @@ CASES = {
                         "gpufs.prefetch_bytes": 60 * KiB}, 42, "per_tb", "global"),
     "c1_global_nopf": ({**C1, "gpufs.policy": "global-lru-dealloc",
                         "gpufs.prefetch_bytes": 0}, 42, "per_tb", "global"),
+    # the Mosaic-style random workload (workloads.py:84-102): requests overlap across TBs,
+    # so only residency 1 is schedule-invariant
+    "mosaic_4k_r1": ({**R1, "workload.kind": "random", "workload.n_tb": 8,
+                      "workload.file_bytes": 8 * MiB, "workload.requests_per_tb": 48,
+                      "workload.request_bytes": 4 * KiB, "gpufs.page_size": 4 * KiB,
+                      "gpufs.prefetch_bytes": 0, "gpufs.cache_bytes": 256 * 4096,
+                      "gpufs.policy": "global-lru-dealloc"}, 11, "global", "global"),
+    "mosaic_64k_pf_r1": ({**R1, "workload.kind": "random", "workload.n_tb": 6,
+                          "workload.file_bytes": 4 * MiB, "workload.requests_per_tb": 24,
+                          "workload.request_bytes": 64 * KiB, "gpufs.page_size": 4 * KiB,
+                          "gpufs.prefetch_bytes": 60 * KiB, "gpufs.cache_bytes": 512 * 4096,
+                          "gpufs.policy": "per-tb-lra"}, 12, "global", "global"),
+    "mosaic_page64k_r1": ({**R1, "workload.kind": "random", "workload.n_tb": 4,
+                           "workload.file_bytes": 6 * MiB + 4096, "workload.requests_per_tb": 40,
+                           "workload.request_bytes": 8 * KiB, "gpufs.page_size": 64 * KiB,
+                           "gpufs.prefetch_bytes": 0, "gpufs.cache_bytes": 24 * 64 * KiB,
+                           "gpufs.policy": "global-lru-dealloc"}, 13, "global", "global"),
 }
 
 COUNTERS = ["greads", "user_bytes", "cache_hit_user_bytes", "tag_mismatches", "pc_lookups",

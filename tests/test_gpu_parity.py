@@ -65,7 +65,9 @@ def test_pressure_many_waves_vs_oracle(policy, readahead, synth_dir):
             "gpufs.cache_bytes": 24 * MiB, "gpufs.policy": policy, "gpu.sm_count": 10,
             "gpu.threads_per_tb": 512, "io.readahead": readahead, "io.ra_max_bytes": 512 * KiB}
     sim, _ = run_sim(over, 42, synth_dir)
-    cfg = ExperimentConfig({**over})
+    # same io.dir as the device run: `auto` transfer (and with it the first adaptive
+    # window) is resolved from where the files live
+    cfg = ExperimentConfig({**over, "io.dir": synth_dir})
     want_sum, ref = oracle_checksum(cfg, 42)
     ref_log = orc.run_oracle(cfg, build_workload(cfg))
     st = sim.result.stats
