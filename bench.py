@@ -360,7 +360,7 @@ def reference_main(args, dist: Dist) -> None:
     cfg = make_cfg(headline_overrides(size, args.gpus, args.dir), args.set)
     path = ensure_file(cfg, dist)
     threads = os.cpu_count() or 1
-    sample = min(size, 2 * GiB)
+    sample = size  # the whole workload per step (~1-2 s on 16 host cores)
     for _ in range(args.warmup):
         cpu_oracle_sample(path, cfg, sample // 4, threads)
     runs = [cpu_oracle_sample(path, cfg, sample, threads) for _ in range(args.steps)]
@@ -370,7 +370,7 @@ def reference_main(args, dist: Dist) -> None:
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(secs / len(runs) * 1e3, 3),
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
-           "data": "synthetic", "config": {"workload": "16GiB-strided-per-tb-lra (bounded sample)",
+           "data": "synthetic", "config": {"workload": "sequential strided gread, 16 GiB/GPU, cache < file (configs[1]), whole workload per step",
                                            "sample_bytes": sample},
            "cpu_baseline": {"value": v, "unit": "GB/s", "cores": threads, "kind": "port",
                             "sample": runs[0]["sample"]},
@@ -550,21 +550,22 @@ def comparison_arms(cfg, path: str, device: int, head) -> tuple[dict, dict, dict
         except Exception as e:
             arms[name] = {"error": str(e)[:300]}
     try:
-        arms["consumer_gesummv_950MB"] = consumer_arm(cfg, path, device, dst)
+        arms["consumers_950MB"] = consumer_arm(cfg, path, device, dst)
     except Exception as e:
-        arms["consumer_gesummv_950MB"] = {"error": str(e)[:300]}
+        arms["consumers_950MB"] = {"error": str(e)[:300]}
     cpu_base = None
     try:
-        cpu_base = cpu_oracle_sample(path, cfg, 2 * GiB, threads)
+        cpu_base = cpu_oracle_sample(path, cfg, size, threads)  # the whole shard
     except Exception as e:
         cpu_base = {"error": str(e)[:300]}
     return probes, arms, cpu_base
 
 
 def consumer_arm(cfg, path: str, device: int, dst) -> dict:
-    """C4: the gesummv input shape (950 MB, 128 TBs, workloads.py:117) read through gread
-    with the GEMV consumer fused (y += A x as each request lands) vs gread then a separate
-    torch.mv over the user buffer."""
+    """C4: the gesummv/bicg input shape (950 MB, 128 TBs, workloads.py:117-120) read through
+    gread with the GEMV consumer fused (y += A x as each request lands) vs gread then a
+    separate torch.mv over the user buffer; the bicg consumer (A p and A^T r in one pass);
+    the kmeans assignment step over the same bytes as 32-feature points."""
     import torch
     from paper_2109_05366_b200.runtime import Consumer, GpuFS
     from paper_2109_05366_b200.workloads import ProgramTable, gen_sequential_strided
@@ -599,8 +600,28 @@ def consumer_arm(cfg, path: str, device: int, dst) -> dict:
         mv_s = ev[0].elapsed_time(ev[1]) / 1e3
         out["gread_then_gemv_gbps"] = round(gbps(total, r.stats["kernel_ns"] / 1e9 + mv_s), 3)
         out["max_rel_err_vs_unfused"] = float(((y - y2).abs().max() / y2.abs().max()).item())
-        out["shape"] = f"{rows}x{cols} f32 from {total} file bytes, {n_tb} TBs, 64 KiB requests"
         del A
+        # bicg / mvt: both products (A p, A^T r) fused into one pass
+        q = torch.zeros(rows, device=f"cuda:{device}")
+        r_ = torch.rand(rows, device=f"cuda:{device}")
+        s_ = torch.zeros(cols, device=f"cuda:{device}")
+        bicg = Consumer("bicg_f32", x=x, y=q, x2=r_, y2=s_, cols=cols)
+        fs.run(table, 64 * KiB, dst, consumer=bicg)
+        r = fs.run(table, 64 * KiB, dst, consumer=bicg)
+        out["gread_fused_bicg_gbps"] = round(gbps(total, r.stats["kernel_ns"] / 1e9), 3)
+        # Rodinia kmeans assignment step: 32-feature points, 8 centroids
+        D, K = 32, 8
+        cent = torch.rand(K, D, device=f"cuda:{device}")
+        sums = torch.zeros(K, D, device=f"cuda:{device}")
+        cnt = torch.zeros(K, dtype=torch.int64, device=f"cuda:{device}")
+        km = Consumer("kmeans_f32", x=cent, y=sums, out=cnt, cols=D, k=K)
+        fs.run(table, 64 * KiB, dst, consumer=km)
+        cnt.zero_()
+        r = fs.run(table, 64 * KiB, dst, consumer=km)
+        out["gread_fused_kmeans_gbps"] = round(gbps(total, r.stats["kernel_ns"] / 1e9), 3)
+        out["kmeans_points"] = int(cnt.sum().item())
+        out["shape"] = (f"{rows}x{cols} f32 from {total} file bytes, {n_tb} TBs, 64 KiB requests; "
+                        f"kmeans {total // (4 * D)} points x {D} features, {K} centroids")
     return out
 
 

@@ -136,17 +136,30 @@ int gfs_run(gfs_ctx* ctx, const gfs_program* prog, void* dst, uint64_t dst_bytes
  * the TB runs the consumer over the bytes it just delivered (they are in L2), so compute
  * overlaps the other TBs' I/O — the real counterpart of workload.compute_ns_per_byte
  * (gpu_exec.py:127-129).  Elements decode from the file bytes: f32 = (u32 >> 8) * 2^-24. */
-enum { GFS_CONSUME_NONE = 0, GFS_CONSUME_SUM64 = 1, GFS_CONSUME_GEMV_F32 = 2, GFS_CONSUME_NN_F32 = 3 };
+enum { GFS_CONSUME_NONE = 0, GFS_CONSUME_SUM64 = 1, GFS_CONSUME_GEMV_F32 = 2, GFS_CONSUME_NN_F32 = 3,
+       GFS_CONSUME_GEMVT_F32 = 4, GFS_CONSUME_BICG_F32 = 5, GFS_CONSUME_KMEANS_F32 = 6 };
+/* Shapes: the file is a row-major matrix A [rows, cols] of such f32 elements.
+ *   GEMV   (gesummv, mvt 1st, atax 1st pass):  y  += A x          x [cols], y [rows]
+ *   GEMVT  (mvt 2nd, atax 2nd pass):           y2 += A^T x2       x2 [rows], y2 [cols]
+ *   BICG   (bicg q = A p, s = A^T r; mvt):     both in one pass
+ *   KMEANS (Rodinia kmeans assignment step):   rows = points of `cols` features; each point
+ *          goes to the nearest of k centroids x [k, cols] (squared distance summed over the
+ *          features in order, IEEE fp32, lowest index on ties); y [k, cols] += the points'
+ *          features per centroid, out [k] (u64) += points per centroid. */
+#define GFS_KMEANS_MAX_K 16
 
 typedef struct gfs_consumer {
   int32_t kind;             /* GFS_CONSUME_* */
-  int32_t reserved;
-  int64_t cols;             /* GEMV: row length (elements, multiple of 4) of the row-major file matrix */
-  const float* x;           /* GEMV: device vector [cols] */
-  float* y;                 /* GEMV: device vector [rows], accumulated into (y += A x) */
+  int32_t k;                /* KMEANS: number of centroids (1..GFS_KMEANS_MAX_K) */
+  int64_t cols;             /* GEMV*, BICG, KMEANS: row length (elements, multiple of 4) */
+  const float* x;           /* GEMV/BICG: device vector [cols]; KMEANS: centroids [k, cols] */
+  float* y;                 /* GEMV/BICG: device vector [rows] (y += A x); KMEANS: sums [k, cols] */
   float qx, qy;             /* NN: query point (records are (lat, lng) pairs) */
   unsigned long long* out;  /* SUM64: device u64 += sum_i mix64(w_i ^ (i * golden)) over file words;
-                               NN: device u64 atomicMin of (dist2 bits << 32 | record index) */
+                               NN: device u64 atomicMin of (dist2 bits << 32 | record index);
+                               KMEANS: device u64 [k] += points assigned per centroid */
+  const float* x2;          /* GEMVT/BICG: device vector [rows] */
+  float* y2;                /* GEMVT/BICG: device vector [cols] (y2 += A^T x2) */
 } gfs_consumer;
 
 /* gfs_run plus a consumer (cons may be NULL); requires a user buffer. */

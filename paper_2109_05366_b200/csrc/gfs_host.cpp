@@ -728,20 +728,36 @@ static int validate_program(gfs_ctx* ctx, const gfs_program* prog, uint64_t dst_
 
 static int validate_consumer(const gfs_consumer* k, const gfs_program* prog, bool has_dst) {
   if (!k || k->kind == GFS_CONSUME_NONE) return GFS_OK;
-  if (k->kind < GFS_CONSUME_NONE || k->kind > GFS_CONSUME_NN_F32)
+  if (k->kind < GFS_CONSUME_NONE || k->kind > GFS_CONSUME_KMEANS_F32)
     return fail(GFS_EINVAL, "unknown consumer kind %d", k->kind);
   if (!has_dst) return fail(GFS_EINVAL, "consumers read the user buffer: dst is required");
-  const int64_t align = k->kind == GFS_CONSUME_GEMV_F32 ? 16 : 8;
-  if (k->kind == GFS_CONSUME_GEMV_F32 && (k->cols <= 0 || k->cols % 4 || !k->x || !k->y))
-    return fail(GFS_EINVAL, "GEMV consumer needs cols > 0 (multiple of 4), x and y");
-  if (k->kind != GFS_CONSUME_GEMV_F32 && !k->out) return fail(GFS_EINVAL, "consumer needs out");
+  const bool matrix = k->kind == GFS_CONSUME_GEMV_F32 || k->kind == GFS_CONSUME_GEMVT_F32 ||
+                      k->kind == GFS_CONSUME_BICG_F32 || k->kind == GFS_CONSUME_KMEANS_F32;
+  if (matrix && (k->cols <= 0 || k->cols % 4))
+    return fail(GFS_EINVAL, "matrix consumers need cols > 0, a multiple of 4");
+  if ((k->kind == GFS_CONSUME_GEMV_F32 || k->kind == GFS_CONSUME_BICG_F32) && (!k->x || !k->y))
+    return fail(GFS_EINVAL, "GEMV needs x [cols] and y [rows]");
+  if ((k->kind == GFS_CONSUME_GEMVT_F32 || k->kind == GFS_CONSUME_BICG_F32) && (!k->x2 || !k->y2))
+    return fail(GFS_EINVAL, "GEMVT needs x2 [rows] and y2 [cols]");
+  if (k->kind == GFS_CONSUME_KMEANS_F32) {
+    if (k->k < 1 || k->k > GFS_KMEANS_MAX_K)
+      return fail(GFS_EINVAL, "kmeans needs 1 <= k <= %d centroids", GFS_KMEANS_MAX_K);
+    if (!k->x || !k->y || !k->out) return fail(GFS_EINVAL, "kmeans needs x (centroids), y (sums), out (counts)");
+    if (2 * (int64_t)k->k * k->cols * 4 + 4 * (int64_t)k->k > 32 * 1024)
+      return fail(GFS_EINVAL, "kmeans state (2 k cols floats) must fit 32 KiB of shared memory");
+  }
+  if ((k->kind == GFS_CONSUME_SUM64 || k->kind == GFS_CONSUME_NN_F32) && !k->out)
+    return fail(GFS_EINVAL, "consumer needs out");
+  // every request starts on a record: 8 B words (sum64, nn), 16 B vectors (matrices),
+  // whole points (kmeans)
+  const int64_t align = k->kind == GFS_CONSUME_KMEANS_F32 ? k->cols * 4 : matrix ? 16 : 8;
   if (prog->request_bytes % align) return fail(GFS_EINVAL, "consumer needs %lld-byte aligned requests", (long long)align);
   const int64_t n_segs = prog->prog_off[prog->n_tb];
   for (int64_t s = 0; s < n_segs; s++)
     if (prog->segs[3 * s + 1] % align || prog->segs[3 * s + 2] % align)
       return fail(GFS_EINVAL, "consumer needs %lld-byte aligned segments", (long long)align);
   for (int t = 0; t < prog->n_tb; t++)
-    if (prog->dst_off[t] % align) return fail(GFS_EINVAL, "consumer needs aligned user-buffer offsets");
+    if (prog->dst_off[t] % 16) return fail(GFS_EINVAL, "consumer needs 16-byte aligned user-buffer offsets");
   return GFS_OK;
 }
 

@@ -1300,12 +1300,139 @@ struct ConsAcc {
 
 __device__ __forceinline__ float decode_f32(uint32_t u) { return (float)(u >> 8) * (1.0f / 16777216.0f); }
 
-constexpr int GEMV_ROWS = 1024;  // rows of one request accumulated in shared memory
+constexpr int GEMV_ROWS = 1024;          // rows of one request accumulated in shared memory
+constexpr int GEMVT_SMEM_COLS = 8192;    // A^T x2 accumulated per CTA in shared memory up to this
+
+// Dynamic shared memory a consumer needs (the launch passes it; 0 for the plain gread path).
+__host__ __device__ inline int64_t consumer_smem_bytes(const gfs_consumer& k) {
+  if ((k.kind == GFS_CONSUME_GEMVT_F32 || k.kind == GFS_CONSUME_BICG_F32) && k.cols <= GEMVT_SMEM_COLS)
+    return k.cols * 4;
+  if (k.kind == GFS_CONSUME_KMEANS_F32) return 2 * (int64_t)k.k * k.cols * 4 + (int64_t)k.k * 4;
+  return 0;
+}
+
+// y += A x over the request's rows (cols % 4 == 0: one row per 16-byte vector).
+template <int BS>
+__device__ void gemv_part(const gfs_consumer& k, const uint4* v4, int64_t ne, int64_t e0) {
+  __shared__ float rows[GEMV_ROWS];
+  const int tid = threadIdx.x;
+  const int64_t M = k.cols;
+  const int64_t row_lo = e0 / M, row_hi = (e0 + ne - 1) / M;
+  const bool local = row_hi - row_lo < GEMV_ROWS;
+  if (local)
+    for (int i = tid; i <= (int)(row_hi - row_lo); i += BS) rows[i] = 0.f;
+  __syncthreads();
+  for (int64_t i = tid; i < (ne >> 2); i += BS) {
+    const uint4 u = __ldcg(v4 + i);
+    const int64_t e = e0 + 4 * i;
+    const int64_t row = e / M, col = e - row * M;
+    const float4 xv = *(const float4*)(k.x + col);
+    float p = decode_f32(u.x) * xv.x + decode_f32(u.y) * xv.y + decode_f32(u.z) * xv.z +
+              decode_f32(u.w) * xv.w;
+    // a warp's 32 consecutive vectors usually share one row: reduce them first
+    const unsigned active = __activemask();
+    const int64_t row0 = __shfl_sync(active, row, __ffs(active) - 1);
+    if (active == 0xffffffffu && __all_sync(active, row == row0)) {
+      for (int o = 16; o > 0; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
+      if ((threadIdx.x & 31) == 0) {
+        if (local) atomicAdd(&rows[row - row_lo], p);
+        else atomicAdd(&k.y[row], p);
+      }
+    } else if (local) {
+      atomicAdd(&rows[row - row_lo], p);
+    } else {
+      atomicAdd(&k.y[row], p);
+    }
+  }
+  __syncthreads();
+  if (local)
+    for (int i = tid; i <= (int)(row_hi - row_lo); i += BS) atomicAdd(&k.y[row_lo + i], rows[i]);
+  __syncthreads();
+}
+
+// y2 += A^T x2: a warp's vectors cover consecutive columns, so the per-CTA shared
+// accumulator (held across every TB the CTA runs, flushed once) sees no same-address
+// conflicts; wider matrices accumulate straight into y2.
+__device__ void gemvt_part(const gfs_consumer& k, float* acc, const uint4* v4, int64_t ne, int64_t e0,
+                           int tid, int bs) {
+  const int64_t M = k.cols;
+  const bool sm = M <= GEMVT_SMEM_COLS;
+  for (int64_t i = tid; i < (ne >> 2); i += bs) {
+    const uint4 u = __ldcg(v4 + i);
+    const int64_t e = e0 + 4 * i;
+    const int64_t row = e / M, col = e - row * M;
+    const float xr = k.x2[row];
+    float* dst = sm ? acc + col : k.y2 + col;
+    atomicAdd(dst + 0, decode_f32(u.x) * xr);
+    atomicAdd(dst + 1, decode_f32(u.y) * xr);
+    atomicAdd(dst + 2, decode_f32(u.z) * xr);
+    atomicAdd(dst + 3, decode_f32(u.w) * xr);
+  }
+}
+
+// Kmeans assignment + accumulation, one thread per point.  Distances are summed over the
+// features in order with IEEE round-to-nearest steps and no contraction (the bits a
+// float32 reference gets); the features are read once, as 16-byte vectors.
+__device__ void kmeans_part(const gfs_consumer& k, float* smem, const uint8_t* data, int64_t np,
+                            int tid, int bs) {
+  const int K = k.k;
+  const int D = (int)k.cols;
+  const float* cent = smem;
+  float* acc = smem + K * D;
+  unsigned* cnt = (unsigned*)(smem + 2 * K * D);
+  const int lane = tid & 31;
+  for (int64_t p = tid; p < np; p += bs) {
+    const uint4* pv = (const uint4*)(data + p * (int64_t)D * 4);
+    float d[GFS_KMEANS_MAX_K];
+#pragma unroll
+    for (int c = 0; c < GFS_KMEANS_MAX_K; c++) d[c] = 0.f;
+    for (int j = 0; j < D; j += 4) {
+      const uint4 u = __ldcg(pv + (j >> 2));
+      const float v[4] = {decode_f32(u.x), decode_f32(u.y), decode_f32(u.z), decode_f32(u.w)};
+#pragma unroll
+      for (int c = 0; c < GFS_KMEANS_MAX_K; c++) {
+        if (c < K) {
+#pragma unroll
+          for (int q = 0; q < 4; q++) {
+            const float df = __fsub_rn(v[q], cent[c * D + j + q]);
+            d[c] = __fadd_rn(d[c], __fmul_rn(df, df));
+          }
+        }
+      }
+    }
+    int best = 0;
+    float bd = d[0];
+#pragma unroll
+    for (int c = 1; c < GFS_KMEANS_MAX_K; c++)
+      if (c < K && d[c] < bd) { bd = d[c]; best = c; }
+    atomicAdd(&cnt[best], 1u);
+    // lanes start at different features, so lanes of one cluster hit different words
+    const uint32_t* pw = (const uint32_t*)pv;
+    float* row = acc + best * D;
+    for (int t = 0; t < D; t++) {
+      int j = lane + t;
+      while (j >= D) j -= D;
+      atomicAdd(&row[j], decode_f32(__ldcg(pw + j)));
+    }
+  }
+}
+
+// All threads, once per launch before the first TB: zero / load the consumer's shared state.
+__device__ void consume_init(const DevCtx& c, float* smem) {
+  const gfs_consumer& k = c.cons;
+  const int64_t n = consumer_smem_bytes(k) / 4;
+  if (n == 0) return;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) smem[i] = 0.f;
+  if (k.kind == GFS_CONSUME_KMEANS_F32)
+    for (int64_t i = threadIdx.x; i < (int64_t)k.k * k.cols; i += blockDim.x) smem[i] = k.x[i];
+  __syncthreads();
+}
 
 // Consume the n bytes the TB just delivered (`data`, in the user buffer) that came from
 // file offset `file_off`.  All threads.
 template <int BS>
-__device__ void consume(const DevCtx& c, const uint8_t* data, int64_t n, int64_t file_off, ConsAcc& acc) {
+__device__ void consume(const DevCtx& c, float* smem, const uint8_t* data, int64_t n, int64_t file_off,
+                        ConsAcc& acc) {
   const int tid = threadIdx.x;
   const gfs_consumer& k = c.cons;
   if (n <= 0) return;
@@ -1328,48 +1455,37 @@ __device__ void consume(const DevCtx& c, const uint8_t* data, int64_t n, int64_t
           ((unsigned long long)__float_as_uint(d2) << 32) | (unsigned long long)(uint32_t)(r0 + i);
       acc.nn = key < acc.nn ? key : acc.nn;
     }
-  } else if (k.kind == GFS_CONSUME_GEMV_F32) {  // y[row] += sum_col A[row, col] * x[col]
-    __shared__ float rows[GEMV_ROWS];
-    const int64_t M = k.cols;
-    const int64_t e0 = file_off >> 2, ne = n >> 2;
-    const int64_t row_lo = e0 / M, row_hi = (e0 + ne - 1) / M;
-    const bool local = row_hi - row_lo < GEMV_ROWS;
-    if (local)
-      for (int i = tid; i <= (int)(row_hi - row_lo); i += BS) rows[i] = 0.f;
-    __syncthreads();
-    const uint4* v4 = (const uint4*)data;
-    for (int64_t i = tid; i < (ne >> 2); i += BS) {
-      const uint4 u = __ldcg(v4 + i);
-      const int64_t e = e0 + 4 * i;
-      const int64_t row = e / M, col = e - row * M;  // cols % 4 == 0: one row per vector
-      const float4 xv = *(const float4*)(k.x + col);
-      float p = decode_f32(u.x) * xv.x + decode_f32(u.y) * xv.y + decode_f32(u.z) * xv.z +
-                decode_f32(u.w) * xv.w;
-      // a warp's 32 consecutive vectors usually share one row: reduce them first
-      const unsigned active = __activemask();
-      const int64_t row0 = __shfl_sync(active, row, __ffs(active) - 1);
-      if (active == 0xffffffffu && __all_sync(active, row == row0)) {
-        for (int o = 16; o > 0; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
-        if ((threadIdx.x & 31) == 0) {
-          if (local) atomicAdd(&rows[row - row_lo], p);
-          else atomicAdd(&k.y[row], p);
-        }
-      } else if (local) {
-        atomicAdd(&rows[row - row_lo], p);
-      } else {
-        atomicAdd(&k.y[row], p);
-      }
-    }
-    __syncthreads();
-    if (local)
-      for (int i = tid; i <= (int)(row_hi - row_lo); i += BS) atomicAdd(&k.y[row_lo + i], rows[i]);
-    __syncthreads();
+  } else if (k.kind == GFS_CONSUME_GEMV_F32) {
+    gemv_part<BS>(k, (const uint4*)data, n >> 2, file_off >> 2);
+  } else if (k.kind == GFS_CONSUME_GEMVT_F32) {
+    gemvt_part(k, smem, (const uint4*)data, n >> 2, file_off >> 2, tid, BS);
+  } else if (k.kind == GFS_CONSUME_BICG_F32) {
+    gemvt_part(k, smem, (const uint4*)data, n >> 2, file_off >> 2, tid, BS);
+    gemv_part<BS>(k, (const uint4*)data, n >> 2, file_off >> 2);
+  } else if (k.kind == GFS_CONSUME_KMEANS_F32) {
+    kmeans_part(k, smem, data, n / (k.cols * 4), tid, BS);
   }
 }
 
 template <int BS>
-__device__ void consume_flush(const DevCtx& c, ConsAcc& acc) {
+__device__ void consume_flush(const DevCtx& c, float* smem, ConsAcc& acc) {
   const int kind = c.cons.kind;
+  const gfs_consumer& k = c.cons;
+  if (kind == GFS_CONSUME_GEMVT_F32 || kind == GFS_CONSUME_BICG_F32 || kind == GFS_CONSUME_KMEANS_F32) {
+    __syncthreads();
+    if (kind == GFS_CONSUME_KMEANS_F32) {
+      const int64_t kd = (int64_t)k.k * k.cols;
+      for (int64_t i = threadIdx.x; i < kd; i += BS)
+        if (smem[kd + i] != 0.f) atomicAdd(&k.y[i], smem[kd + i]);
+      const unsigned* cnt = (const unsigned*)(smem + 2 * kd);
+      for (int i = threadIdx.x; i < k.k; i += BS)
+        if (cnt[i]) atomicAdd(&k.out[i], (unsigned long long)cnt[i]);
+    } else if (k.cols <= GEMVT_SMEM_COLS) {
+      for (int64_t i = threadIdx.x; i < k.cols; i += BS)
+        if (smem[i] != 0.f) atomicAdd(&k.y2[i], smem[i]);
+    }
+    return;
+  }
   if (kind != GFS_CONSUME_SUM64 && kind != GFS_CONSUME_NN_F32) return;
   unsigned long long v = kind == GFS_CONSUME_SUM64 ? acc.sum : acc.nn;
   for (int o = 16; o > 0; o >>= 1) {
@@ -1384,7 +1500,7 @@ __device__ void consume_flush(const DevCtx& c, ConsAcc& acc) {
 
 // TB program (gpu_exec.py:95-105) and TB done (drain + retire, gpu_exec.py:281-291).
 template <int BS>
-__device__ bool run_tb(const DevCtx& c, Smem& s, int tb, int& bad_words, ConsAcc& acc) {
+__device__ bool run_tb(const DevCtx& c, Smem& s, float* cons_smem, int tb, int& bad_words, ConsAcc& acc) {
   const int tid = threadIdx.x;
   if (tid == 0) {
     s.tb = tb;
@@ -1416,7 +1532,7 @@ __device__ bool run_tb(const DevCtx& c, Smem& s, int tb, int& bad_words, ConsAcc
       uint8_t* d = c.dst ? c.dst + pos + seg_off : nullptr;
       int64_t got = gread<BS>(c, s, fid, base + seg_off, size, base + len, d, bad_words);
       if (got < 0) return false;
-      if (c.cons.kind != GFS_CONSUME_NONE && d) consume<BS>(c, d, got, base + seg_off, acc);
+      if (c.cons.kind != GFS_CONSUME_NONE && d) consume<BS>(c, cons_smem, d, got, base + seg_off, acc);
       seg_off += got;
       if (got < size) break;  // short read: rest of the segment is skipped
     }
@@ -1460,6 +1576,8 @@ __global__ void __launch_bounds__(BS, 4) gread_driver(DevCtx c) {
       __threadfence();
     }
   }
+  extern __shared__ float cons_smem[];  // consumer state (consumer_smem_bytes)
+  consume_init(c, cons_smem);
   int bad_words = 0;
   ConsAcc acc;
   for (;;) {
@@ -1470,9 +1588,9 @@ __global__ void __launch_bounds__(BS, 4) gread_driver(DevCtx c) {
     const int64_t k = s.k;
     __syncthreads();
     if (k >= c.n_tb) break;
-    if (!run_tb<BS>(c, s, c.order[k], bad_words, acc)) break;
+    if (!run_tb<BS>(c, s, cons_smem, c.order[k], bad_words, acc)) break;
   }
-  consume_flush<BS>(c, acc);
+  consume_flush<BS>(c, cons_smem, acc);
   __shared__ int mism;
   if (tid == 0) mism = 0;
   __syncthreads();
@@ -1561,10 +1679,11 @@ __global__ void verify_dst_kernel(const uint8_t* buf, const int64_t* segs, const
 // ------------------------------------------------------------------ host-side launchers
 
 cudaError_t launch_gread(const DevCtx& c, int cta_threads, cudaStream_t st) {
+  const size_t smem = (size_t)consumer_smem_bytes(c.cons);
   switch (cta_threads) {
-    case 128: gread_driver<128><<<c.n_ctas, 128, 0, st>>>(c); break;
-    case 512: gread_driver<512><<<c.n_ctas, 512, 0, st>>>(c); break;
-    default: gread_driver<256><<<c.n_ctas, 256, 0, st>>>(c); break;
+    case 128: gread_driver<128><<<c.n_ctas, 128, smem, st>>>(c); break;
+    case 512: gread_driver<512><<<c.n_ctas, 512, smem, st>>>(c); break;
+    default: gread_driver<256><<<c.n_ctas, 256, smem, st>>>(c); break;
   }
   return cudaGetLastError();
 }

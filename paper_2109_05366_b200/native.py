@@ -44,14 +44,16 @@ class GfsConfig(C.Structure):
     ]
 
 
-CONSUME = {"none": 0, "sum64": 1, "gemv_f32": 2, "nn_f32": 3}
+CONSUME = {"none": 0, "sum64": 1, "gemv_f32": 2, "nn_f32": 3, "gemvt_f32": 4, "bicg_f32": 5,
+           "kmeans_f32": 6}
+KMEANS_MAX_K = 16
 
 
 class GfsConsumer(C.Structure):
     _fields_ = [
-        ("kind", C.c_int32), ("reserved", C.c_int32), ("cols", C.c_int64),
+        ("kind", C.c_int32), ("k", C.c_int32), ("cols", C.c_int64),
         ("x", C.c_void_p), ("y", C.c_void_p), ("qx", C.c_float), ("qy", C.c_float),
-        ("out", C.c_void_p),
+        ("out", C.c_void_p), ("x2", C.c_void_p), ("y2", C.c_void_p),
     ]
 
 

@@ -92,6 +92,12 @@ class Consumer:
               f32 = (u32 >> 8) * 2^-24 (the gesummv/mvt/bicg/atax access pattern)
     nn_f32:   out (uint64 [1]) = min over records (lat, lng) of (dist2 bits << 32 | index),
               the Rodinia nn scan
+    gemvt_f32: y2 (float32 [cols]) += A^T x2 (x2 float32 [rows]); mvt's second product and
+              atax's second pass
+    bicg_f32: both products in one pass (bicg: q = A p, s = A^T r; mvt)
+    kmeans_f32: Rodinia kmeans assignment step over points of `cols` features: x = centroids
+              float32 [k, cols]; y float32 [k, cols] += features of the points nearest to each
+              centroid; out uint64 [k] += their count
     """
     kind: str
     out: object = None
@@ -100,6 +106,9 @@ class Consumer:
     cols: int = 0
     qx: float = 0.0
     qy: float = 0.0
+    x2: object = None
+    y2: object = None
+    k: int = 0
 
     def native(self) -> "native.GfsConsumer":
         k = native.GfsConsumer()
@@ -110,6 +119,9 @@ class Consumer:
         k.x = self.x.data_ptr() if self.x is not None else None
         k.y = self.y.data_ptr() if self.y is not None else None
         k.out = self.out.data_ptr() if self.out is not None else None
+        k.x2 = self.x2.data_ptr() if self.x2 is not None else None
+        k.y2 = self.y2.data_ptr() if self.y2 is not None else None
+        k.k = self.k
         k.qx, k.qy = self.qx, self.qy
         return k
 

@@ -83,3 +83,98 @@ def test_gemv_consumer_matches_float64_reference(setup):
     ref = A @ x.cpu().numpy().astype(np.float64)
     got = y.cpu().numpy().astype(np.float64)
     assert np.allclose(got, ref, rtol=GEMV_RTOL, atol=GEMV_RTOL * np.abs(ref).max())
+
+
+def _matrix(host, cols):
+    return decode(host.view("<u4")).astype(np.float64).reshape(-1, cols)
+
+
+@pytest.mark.parametrize("cols", [1024, 16384])  # shared-memory and global accumulators
+def test_gemvt_consumer_matches_float64_reference(setup, cols):
+    import torch
+    from paper_2109_05366_b200.runtime import Consumer
+    fs, table, dst, host, size = setup
+    rows = size // 4 // cols
+    x2 = torch.cos(torch.arange(rows, dtype=torch.float32, device="cuda") * 0.01)
+    y2 = torch.zeros(cols, dtype=torch.float32, device="cuda")
+    fs.run(table, 64 * KiB, dst, consumer=Consumer("gemvt_f32", x2=x2, y2=y2, cols=cols))
+    ref = _matrix(host, cols).T @ x2.cpu().numpy().astype(np.float64)
+    got = y2.cpu().numpy().astype(np.float64)
+    assert np.allclose(got, ref, rtol=GEMV_RTOL, atol=GEMV_RTOL * np.abs(ref).max())
+
+
+def test_bicg_consumer_both_products_in_one_pass(setup):
+    """POLYBENCH bicg (q = A p, s = A^T r) — also mvt's two products — from one gread pass."""
+    import torch
+    from paper_2109_05366_b200.runtime import Consumer
+    fs, table, dst, host, size = setup
+    cols = 2048
+    rows = size // 4 // cols
+    p = torch.linspace(-1, 1, cols, dtype=torch.float32, device="cuda")
+    r = torch.sin(torch.arange(rows, dtype=torch.float32, device="cuda") * 0.1)
+    q = torch.zeros(rows, dtype=torch.float32, device="cuda")
+    s = torch.zeros(cols, dtype=torch.float32, device="cuda")
+    fs.run(table, 64 * KiB, dst, consumer=Consumer("bicg_f32", x=p, y=q, x2=r, y2=s, cols=cols))
+    A = _matrix(host, cols)
+    for got, ref in ((q, A @ p.cpu().numpy().astype(np.float64)),
+                     (s, A.T @ r.cpu().numpy().astype(np.float64))):
+        got = got.cpu().numpy().astype(np.float64)
+        assert np.allclose(got, ref, rtol=GEMV_RTOL, atol=GEMV_RTOL * np.abs(ref).max())
+
+
+def test_atax_two_gread_passes(setup):
+    """POLYBENCH atax y = A^T (A x): pass 1 GEMV, pass 2 GEMVT over a second gread pass."""
+    import torch
+    from paper_2109_05366_b200.runtime import Consumer
+    fs, table, dst, host, size = setup
+    cols = 4096
+    rows = size // 4 // cols
+    x = torch.linspace(0, 1, cols, dtype=torch.float32, device="cuda")
+    tmp = torch.zeros(rows, dtype=torch.float32, device="cuda")
+    y = torch.zeros(cols, dtype=torch.float32, device="cuda")
+    fs.run(table, 64 * KiB, dst, consumer=Consumer("gemv_f32", x=x, y=tmp, cols=cols))
+    fs.run(table, 64 * KiB, dst, consumer=Consumer("gemvt_f32", x2=tmp, y2=y, cols=cols))
+    A = _matrix(host, cols)
+    ref = A.T @ (A @ x.cpu().numpy().astype(np.float64))
+    got = y.cpu().numpy().astype(np.float64)
+    assert np.allclose(got, ref, rtol=2 * GEMV_RTOL, atol=2 * GEMV_RTOL * np.abs(ref).max())
+
+
+def test_kmeans_consumer_assignment_exact(setup):
+    """Rodinia kmeans assignment step: per-centroid counts are exact (fp32 distances summed
+    over the features in order, as the float32 reference below does); per-centroid feature
+    sums within rtol 1e-4 (fp32 accumulation order differs)."""
+    import torch
+    from paper_2109_05366_b200.runtime import Consumer
+    fs, table, dst, host, size = setup
+    D, K = 16, 5
+    P = decode(host.view("<u4")).reshape(-1, D)
+    cent = P[[0, 1000, 20000, 300000, 390000]].copy()
+    C = torch.from_numpy(cent).cuda()
+    sums = torch.zeros(K, D, dtype=torch.float32, device="cuda")
+    counts = torch.zeros(K, dtype=torch.int64, device="cuda")
+    fs.run(table, 64 * KiB, dst, consumer=Consumer("kmeans_f32", x=C, y=sums, out=counts, cols=D, k=K))
+    d = np.zeros((K, P.shape[0]), dtype=np.float32)
+    for c in range(K):
+        for j in range(D):
+            df = P[:, j] - cent[c, j]
+            d[c] = d[c] + df * df
+    assign = np.argmin(d, axis=0)
+    want_counts = np.bincount(assign, minlength=K)
+    assert counts.cpu().numpy().tolist() == want_counts.tolist()
+    want_sums = np.stack([P[assign == c].astype(np.float64).sum(0) for c in range(K)])
+    assert np.allclose(sums.cpu().numpy(), want_sums, rtol=1e-4)
+
+
+def test_consumer_validation_is_loud(setup):
+    import torch
+    from paper_2109_05366_b200.errors import GfsError
+    from paper_2109_05366_b200.runtime import Consumer
+    fs, table, dst, host, size = setup
+    C = torch.zeros(17, 16, device="cuda")
+    with pytest.raises(GfsError):  # too many centroids
+        fs.run(table, 64 * KiB, dst, consumer=Consumer("kmeans_f32", x=C, y=C, out=C, cols=16, k=17))
+    with pytest.raises(GfsError):  # points of 12 features do not tile 64 KiB requests
+        fs.run(table, 64 * KiB, dst, consumer=Consumer("kmeans_f32", x=C, y=C, out=C, cols=12, k=2))
+    with pytest.raises(GfsError):  # GEMVT without its vectors
+        fs.run(table, 64 * KiB, dst, consumer=Consumer("gemvt_f32", cols=1024))

@@ -86,7 +86,8 @@ def test_pressure_many_waves_vs_oracle(policy, readahead, synth_dir):
 
 def test_adaptive_window_law_single_stream(synth_dir):
     over = {"workload.n_tb": 1, "workload.file_bytes": 8 * MiB, "gpufs.prefetch_bytes": 60 * KiB,
-            "io.readahead": "adaptive", "io.ra_max_bytes": 1 * MiB, "gpufs.cache_bytes": 16 * MiB}
+            "io.readahead": "adaptive", "io.ra_max_bytes": 1 * MiB, "gpufs.cache_bytes": 16 * MiB,
+            "io.ra_init_bytes": 64 * KiB}  # explicit: auto depends on the transfer mode
     sim, rep = run_sim(over, 1, synth_dir)
     w = [int(x) for x in sim.result.windows[:, 1]]
     assert w[:5] == [64 * KiB, 128 * KiB, 256 * KiB, 512 * KiB, 1 * MiB]
