@@ -191,6 +191,15 @@ int gfs_bench_h2d(int device, int64_t bytes, int reps, double* best_seconds);
 int gfs_bench_read_memcpy(const char* path, int64_t offset, int64_t size, void* dst_dev, int device,
                           int threads, int64_t chunk, int direct, int sync, double* seconds);
 
+/* host-only replay of a recorded RPC trace (the reference's `gpuiosim replay`,
+ * simulation.py:147-164): recs = [n_recs][4] (tb, file, offset, size);
+ * record r is served by worker (tb % n_slots) / (n_slots / n_workers), each worker preads
+ * its records back to back.  No GPU involved.  Errors: unknown file / read past EOF
+ * (trace_workload, simulation.py:50-64) -> GFS_EINVAL. */
+int gfs_replay(const char* const* paths, int n_files, const int64_t* recs, int64_t n_recs,
+               int n_slots, int n_workers, int direct, int64_t* user_bytes, int64_t* preads,
+               double* seconds);
+
 /* ---- introspection ---- */
 const char* gfs_last_error(void);
 int gfs_abi_version(void);

@@ -201,3 +201,94 @@ extern "C" int gfs_bench_read_memcpy(const char* path, int64_t offset, int64_t s
   *seconds = el;
   return GFS_OK;
 }
+
+// ---------------------------------------------------------------- host-only trace replay
+//
+// The paper's §3.3 methodology and the reference's `gpuiosim replay`
+// (simulation.py:147-164, HostStream :67-95): the RPC trace a GPU run recorded is replayed
+// by host threads alone — no GPU, no PCIe — to separate the host I/O cost of the GPU's
+// access pattern from the GPU side.  Record r goes to worker
+// slot_for_threadblock(tb, n_slots) / (n_slots / n_workers) (rpc.py:27-28); each worker
+// issues its records back to back (HostStream._next), each a pread of
+// min(size, file_size - offset) bytes (host_os.py:221-230) into a private buffer.
+extern "C" int gfs_replay(const char* const* paths, int n_files, const int64_t* recs, int64_t n_recs,
+                          int n_slots, int n_workers, int direct, int64_t* user_bytes,
+                          int64_t* preads, double* seconds) {
+  if (!paths || n_files < 1 || !recs || n_recs < 1 || n_slots < 1 || n_workers < 1 ||
+      n_slots % n_workers || !user_bytes || !preads || !seconds)
+    return failf(GFS_EINVAL, "gfs_replay: bad argument (n_slots must be a multiple of n_workers)");
+  const int per_worker = n_slots / n_workers;
+  std::vector<int> fd_d(n_files, -1), fd_b(n_files, -1);
+  std::vector<int64_t> fsize(n_files, 0);
+  auto close_all = [&]() {
+    for (int f = 0; f < n_files; f++) {
+      if (fd_d[f] >= 0) close(fd_d[f]);
+      if (fd_b[f] >= 0) close(fd_b[f]);
+    }
+  };
+  for (int f = 0; f < n_files; f++) {
+    fd_b[f] = open(paths[f], O_RDONLY);
+    if (fd_b[f] < 0) {
+      int e = errno;
+      close_all();
+      return failf(GFS_EIO, "gfs_replay: open %s: %s", paths[f], strerror(e));
+    }
+    fsize[f] = lseek(fd_b[f], 0, SEEK_END);
+    if (direct) fd_d[f] = open(paths[f], O_RDONLY | O_DIRECT);  // -1: buffered only
+  }
+  // group per worker, keeping trace order within a worker; validate like trace_workload
+  std::vector<std::vector<int64_t>> groups(n_workers);
+  int64_t max_size = 0;
+  for (int64_t i = 0; i < n_recs; i++) {
+    const int64_t tb = recs[4 * i], fid = recs[4 * i + 1], off = recs[4 * i + 2], size = recs[4 * i + 3];
+    if (tb < 0 || fid < 0 || fid >= n_files || off < 0 || size <= 0) {
+      close_all();
+      return failf(GFS_EINVAL, "trace record %lld: unknown file or bad field", (long long)i);
+    }
+    if (off + size > fsize[fid]) {
+      close_all();
+      return failf(GFS_EINVAL, "trace record %lld: read past EOF", (long long)i);
+    }
+    groups[(tb % n_slots) / per_worker].push_back(i);
+    max_size = std::max(max_size, size);
+  }
+  const int64_t buf_bytes = (max_size + 8191) / 4096 * 4096;
+  std::atomic<int64_t> bytes{0}, count{0};
+  std::atomic<int> err{0};
+  auto body = [&](int w) {
+    void* buf = nullptr;
+    if (posix_memalign(&buf, 4096, (size_t)buf_bytes)) {
+      err.store(ENOMEM);
+      return;
+    }
+    int64_t b = 0, c = 0;
+    for (int64_t i : groups[w]) {
+      if (err.load(std::memory_order_relaxed)) break;
+      const int64_t fid = recs[4 * i + 1], off = recs[4 * i + 2];
+      const int64_t n = std::min(recs[4 * i + 3], fsize[fid] - off);
+      const bool dio = fd_d[fid] >= 0 && (off & 4095) == 0;
+      int64_t r = read_fully(dio ? fd_d[fid] : fd_b[fid], (uint8_t*)buf, dio ? (n + 4095) / 4096 * 4096 : n, off);
+      if (r < 0 && dio && r == -EINVAL) r = read_fully(fd_b[fid], (uint8_t*)buf, n, off);
+      if (r < 0) {
+        err.store((int)-r);
+        break;
+      }
+      b += std::min(r, n);
+      c++;
+    }
+    bytes.fetch_add(b);
+    count.fetch_add(c);
+    free(buf);
+  };
+  const double t0 = now_s();
+  std::vector<std::thread> th;
+  for (int w = 0; w < n_workers; w++)
+    if (!groups[w].empty()) th.emplace_back(body, w);
+  for (auto& t : th) t.join();
+  *seconds = now_s() - t0;
+  close_all();
+  if (err.load()) return failf(GFS_EIO, "gfs_replay: pread failed: %s", strerror(err.load()));
+  *user_bytes = bytes.load();
+  *preads = count.load();
+  return GFS_OK;
+}

@@ -79,19 +79,41 @@ def _arms_bench(base):
                 "gpufs.cache_bytes": cache, **over})
 
 
-PRESETS = {"fig2": _arms_fig2, "fig8": _arms_fig8, "fig10micro": _arms_fig10micro,
-           "bench": _arms_bench}
+def _run_fig3(base, out_dir):
+    """The GPU's access pattern vs its host-only replay (experiments.py:135-156): a raw-mode
+    gread run (no GPU page cache) records its RPC trace, then host threads replay it with
+    no GPU and no PCIe in the loop."""
+    rows = []
+    for size in (4 * KiB, 16 * KiB, 64 * KiB, 128 * KiB, 256 * KiB, 800 * KiB):
+        trace = os.path.join(out_dir, f"fig3-trace-{size}.txt")
+        rows.extend(run_config(base.copy_with({**_MICRO, "repetitions": 1,
+                                               "workload.request_bytes": size,
+                                               "mode.gpu_cache_disabled": True,
+                                               "workload.record_trace": trace}),
+                               label=f"gpu-pattern-{size}"))
+        rows.extend(run_config(base.copy_with({**_MICRO, "repetitions": 1,
+                                               "workload.request_bytes": size,
+                                               "mode.replay_trace": trace}),
+                               label=f"cpu-replay-{size}"))
+    return rows
+
+
+PRESETS = {"fig2": _arms_fig2, "fig3": _run_fig3, "fig8": _arms_fig8,
+           "fig10micro": _arms_fig10micro, "bench": _arms_bench}
 
 
 def run_preset(name: str, base: ExperimentConfig, out_dir: str) -> str:
     """Run a figure preset; returns the CSV path (same name as the reference's)."""
     if name not in PRESETS:
         raise GfsError(f"unknown preset {name!r}; have {', '.join(PRESETS)} "
-                       "(fig3/fig5/fig6 reproduce host-model pathologies, out of scope)")
+                       "(fig5/fig6 reproduce host-model pathologies, out of scope)")
     os.makedirs(out_dir, exist_ok=True)
     rows = []
-    for label, cfg in PRESETS[name](base):
-        rows.extend(run_config(cfg, label))
+    if name == "fig3":
+        rows = _run_fig3(base, out_dir)
+    else:
+        for label, cfg in PRESETS[name](base):
+            rows.extend(run_config(cfg, label))
     path = os.path.join(out_dir, f"{name}.csv")
     write_csv(path, rows)
     return path

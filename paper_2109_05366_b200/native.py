@@ -28,7 +28,8 @@ EXPORTS = ["gfs_create", "gfs_destroy", "gfs_gopen", "gfs_gclose", "gfs_file_siz
            "gfs_run_consume",
            "gfs_log_len", "gfs_log_copy", "gfs_checksum", "gfs_verify_dst", "gfs_gen_file",
            "gfs_last_error", "gfs_abi_version", "gfs_stat_count", "gfs_stat_name",
-           "gfs_resident_ctas", "gfs_bench_storage", "gfs_bench_h2d", "gfs_bench_read_memcpy"]
+           "gfs_resident_ctas", "gfs_bench_storage", "gfs_bench_h2d", "gfs_bench_read_memcpy",
+           "gfs_replay"]
 
 
 class GfsConfig(C.Structure):
@@ -101,9 +102,11 @@ def load(path: str = LIB_PATH):
     L.gfs_bench_storage.argtypes = [C.c_char_p, i64, i64, i32, i64, i32, dp]
     L.gfs_bench_h2d.argtypes = [i32, i64, i32, dp]
     L.gfs_bench_read_memcpy.argtypes = [C.c_char_p, i64, i64, vp, i32, i32, i64, i32, i32, dp]
+    L.gfs_replay.argtypes = [C.POINTER(C.c_char_p), i32, C.POINTER(i64), i64, i32, i32, i32,
+                             C.POINTER(i64), C.POINTER(i64), dp]
     for name in ("gfs_create", "gfs_gopen", "gfs_gclose", "gfs_file_size", "gfs_run",
                  "gfs_log_len", "gfs_log_copy", "gfs_checksum", "gfs_verify_dst", "gfs_gen_file",
-                 "gfs_bench_storage", "gfs_bench_h2d", "gfs_bench_read_memcpy"):
+                 "gfs_bench_storage", "gfs_bench_h2d", "gfs_bench_read_memcpy", "gfs_replay"):
         getattr(L, name).restype = i32
     _lib = L
     return L
@@ -154,3 +157,17 @@ def bench_read_memcpy(path: str, offset: int, size: int, dst_ptr: int, device: i
     check(L.gfs_bench_read_memcpy(os.fsencode(path), offset, size, dst_ptr, device, threads, chunk,
                                   int(direct), int(sync), C.byref(sec)), "gfs_bench_read_memcpy")
     return sec.value
+
+
+def replay(paths: list[str], records, n_slots: int, n_workers: int, direct: bool = True):
+    """Host-only replay of a recorded RPC trace (include/gfs.h gfs_replay); records is an
+    int64 [n, 4] array of (tb, file, offset, size).  Returns (user_bytes, preads, seconds)."""
+    import numpy as np
+    L = load()
+    recs = np.ascontiguousarray(records, dtype=np.int64).reshape(-1, 4)
+    arr = (C.c_char_p * len(paths))(*[os.fsencode(p) for p in paths])
+    ub, npr, sec = C.c_int64(), C.c_int64(), C.c_double()
+    check(L.gfs_replay(arr, len(paths), recs.ctypes.data_as(C.POINTER(C.c_int64)), len(recs),
+                       n_slots, n_workers, int(direct), C.byref(ub), C.byref(npr), C.byref(sec)),
+          "gfs_replay")
+    return ub.value, npr.value, sec.value

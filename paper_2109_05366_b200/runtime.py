@@ -28,7 +28,7 @@ from .errors import GfsError
 from .metrics import Metrics, MetricsReport, build_report
 from .rng import SeededRng
 from .workloads import (ProgramTable, TraceRecord, WorkloadSpec, build_workload,
-                        dispatch_order, save_trace)
+                        dispatch_order, load_trace, save_trace, trace_workload)
 
 O_RDONLY, O_RDWR = native.O_RDONLY, native.O_RDWR
 
@@ -313,14 +313,13 @@ class Simulation:
     """
 
     def __init__(self, cfg: ExperimentConfig, seed: int, label: str = "run", rep: int = 0):
-        if cfg["mode.replay_trace"]:
-            raise GfsError("mode.replay_trace drives the host path only; "
-                           "not part of the B200 gread path (DESIGN.md scope)")
         self.cfg = cfg
         self.seed = seed
         self.label = label
         self.rep = rep
-        self.workload = build_workload(cfg, SeededRng(seed))
+        self.trace = load_trace(cfg["mode.replay_trace"]) if cfg["mode.replay_trace"] else None
+        self.workload = (trace_workload(self.trace, cfg) if self.trace is not None
+                         else build_workload(cfg, SeededRng(seed)))
         self.metrics = Metrics()
         self.cache = _CacheView()
         self.recorded: list | None = None
@@ -329,6 +328,8 @@ class Simulation:
         self.mismatched_words: int | None = None
 
     def run(self, keep_output: bool = False) -> MetricsReport:
+        if self.trace is not None:
+            return self._run_replay()
         import torch
         cfg = self.cfg
         wl = self.workload
@@ -361,6 +362,26 @@ class Simulation:
         self._verify(res.stats)
         return build_report(self.label, wl.name, self.seed, self.rep, res.stats,
                             self.metrics.window_history)
+
+    def _run_replay(self) -> MetricsReport:
+        """Host-only replay (simulation.py:147-164, HostStream :67-95): the trace's preads
+        issued back to back by rpc.n_workers host threads, grouped by the reference's
+        slot partitioning; no GPU, no PCIe (the paper's §3.3 methodology)."""
+        cfg, wl = self.cfg, self.workload
+        paths = [p for p in cfg["io.paths"].split(",") if p] if cfg["io.paths"] else []
+        if not paths:
+            paths = [ensure_synthetic(synth_dir(cfg), f, wl.files[f]) for f in range(len(wl.files))]
+        recs = np.array([(r.tb_id, r.file_id, r.offset, r.size) for r in self.trace], dtype=np.int64)
+        user, preads, sec = native.replay(paths, recs, cfg["rpc.n_slots"], cfg["rpc.n_workers"],
+                                          cfg["io.direct"])
+        st = {k: 0 for k in native.stat_names()}
+        st.update(user_bytes=user, preads=preads, pread_bytes=user, storage_bytes=user,
+                  kernel_ns=int(sec * 1e9), wall_ns=int(sec * 1e9))
+        self.result = RunResult(stats=st)
+        self.metrics = Metrics(st)
+        if user != wl.total_bytes:
+            raise GfsError(f"replay delivered {user} of {wl.total_bytes} bytes")
+        return build_report(self.label, wl.name, self.seed, self.rep, st)
 
     def _verify(self, st: dict) -> None:
         """Post-run invariants of gpuiosim/simulation.py:246-264 on real counters."""

@@ -189,3 +189,23 @@ def test_recorded_trace_matches_reference_format(tmp_path, synth_dir):
     recs = load_trace(trace)
     got = np.asarray([(r.tb_id, r.file_id, r.offset, r.size) for r in recs], dtype=np.int64)
     assert np.array_equal(gu.by_tb(got), gu.expand_rpcs(g["rpcs_rle"]))
+
+
+def test_record_then_host_replay_round_trip(synth_dir, tmp_path):
+    """fig3 methodology (experiments.py:135-156): a raw-mode gread run records its RPC trace
+    in the reference's format; the host-only replay of that trace reads the same bytes."""
+    from paper_2109_05366_b200.runtime import Simulation
+    from paper_2109_05366_b200.workloads import load_trace
+    trace = str(tmp_path / "trace.txt")
+    over = {"workload.n_tb": 16, "workload.file_bytes": 16 * MiB, "workload.request_bytes": 128 * KiB,
+            "mode.gpu_cache_disabled": True, "io.dir": synth_dir, "workload.record_trace": trace}
+    gpu = Simulation(ExperimentConfig(over), 42)
+    rep = gpu.run()
+    recs = load_trace(trace)
+    assert len(recs) == rep["rpc_count"] == 16 * 8
+    assert sorted((r.tb_id, r.offset) for r in recs) == sorted((t, t * MiB + k * 128 * KiB)
+                                                               for t in range(16) for k in range(8))
+    host = Simulation(ExperimentConfig({**over, "workload.record_trace": "", "mode.replay_trace": trace}), 42)
+    hrep = host.run()
+    assert hrep["user_bytes"] == rep["user_bytes"] == 16 * MiB
+    assert hrep["ssd_requests"] == len(recs)
