@@ -50,7 +50,13 @@ enum { GFS_XFER_ZEROCOPY = 0, GFS_XFER_DMA = 1, GFS_XFER_BOUNCE = 2, GFS_XFER_MA
 /* gopen flags: read-only files are the only ones prefetched (prefetcher.py:22-24) */
 enum { GFS_O_RDONLY = 0, GFS_O_RDWR = 2 };
 /* log kinds (deterministic mode) */
-enum { GFS_LOG_DELIVERIES = 0, GFS_LOG_RPCS = 1, GFS_LOG_VICTIMS = 2, GFS_LOG_WINDOWS = 3 };
+enum { GFS_LOG_DELIVERIES = 0, GFS_LOG_RPCS = 1, GFS_LOG_VICTIMS = 2, GFS_LOG_WINDOWS = 3,
+       GFS_LOG_TIMELINE = 4 };
+/* timeline records (gfs_config.timeline): 4 int64 each —
+ *   (kind << 56 | cta << 32 | tb, bytes, t_begin_ns, t_end_ns) on the GPU's global timer;
+ *   kind: GFS_TL_RPC = request published .. its data ready (the PCIe transfer outstanding),
+ *         GFS_TL_GREAD = one gread call, GFS_TL_CONSUME = the fused consumer over a request */
+enum { GFS_TL_RPC = 0, GFS_TL_GREAD = 1, GFS_TL_CONSUME = 2 };
 
 typedef struct gfs_config {
   int64_t page_size;       /* gpufs.page_size (multiple of 4096) */
@@ -73,7 +79,8 @@ typedef struct gfs_config {
   int32_t pcie_disabled;   /* mode.pcie_disabled: accounting only */
   int32_t log;             /* record delivery / RPC / victim logs on the device */
   int32_t verify;          /* check every fetched word against the synthetic law */
-  int32_t reserved[3];
+  int32_t timeline;        /* record the GFS_LOG_TIMELINE log (mode.timeline) */
+  int32_t reserved[2];
 } gfs_config;
 
 /* One gread program set (workloads.py:24-31 programs, flattened).

@@ -202,9 +202,9 @@ struct gfs_ctx {
   DevBuf<int64_t> d_segs, d_prog_off, d_dst_off, d_seg_dst;
   DevBuf<int32_t> d_order;
   DevBuf<DevFile> d_files;
-  DevBuf<long long> d_logs[4];
-  unsigned long long log_cap[4] = {0, 0, 0, 0};
-  unsigned long long log_n[4] = {0, 0, 0, 0};
+  DevBuf<long long> d_logs[5];
+  unsigned long long log_cap[5] = {0, 0, 0, 0, 0};
+  unsigned long long log_n[5] = {0, 0, 0, 0, 0};
 
   // mapped pinned host memory
   RpcReq* h_ring = nullptr;
@@ -798,9 +798,14 @@ extern "C" int gfs_run_consume(gfs_ctx* ctx, const gfs_program* prog, void* dst,
     pages += len / cfg.page_size + 2;
     requests += len / prog->request_bytes + 1;
   }
-  for (int k = 0; k < 4; k++) {
+  for (int k = 0; k < 5; k++) {
     ctx->log_cap[k] = 0;
     ctx->log_n[k] = 0;
+  }
+  if (cfg.timeline) {  // per request: one gread, at most one RPC, one consume
+    const int64_t cap = 3 * requests + 2 * (int64_t)prog->n_tb + 16;
+    CUDA_TRY(ctx->d_logs[GFS_LOG_TIMELINE].reserve((size_t)(cap * 4)));
+    ctx->log_cap[GFS_LOG_TIMELINE] = (unsigned long long)cap;
   }
   if (cfg.log) {
     const int width[4] = {3, 4, 3, 2};
@@ -841,6 +846,7 @@ extern "C" int gfs_run_consume(gfs_ctx* ctx, const gfs_program* prog, void* dst,
   c.transfer = cfg.transfer;
   c.raw_mode = cfg.raw_mode;
   c.log = cfg.log;
+  c.timeline = cfg.timeline;
   c.verify = cfg.verify;
   c.pcie_disabled = cfg.pcie_disabled;
   c.n_files = (int32_t)ctx->files.size();
@@ -875,7 +881,7 @@ extern "C" int gfs_run_consume(gfs_ctx* ctx, const gfs_program* prog, void* dst,
   c.stats = ctx->d_stats;
   if (cons) c.cons = *cons;
   else c.cons.kind = GFS_CONSUME_NONE;
-  for (int k = 0; k < 4; k++) {
+  for (int k = 0; k < 5; k++) {
     c.logs[k] = ctx->d_logs[k].p;
     c.log_cap[k] = ctx->log_cap[k];
   }
@@ -917,7 +923,7 @@ extern "C" int gfs_run_consume(gfs_ctx* ctx, const gfs_program* prog, void* dst,
   out->v[GFS_STAT_host_xfer_ns] = ctx->t_xfer.load();
   out->v[GFS_STAT_host_requests] = ctx->n_served.load();
   out->v[GFS_STAT_io_workers] = ctx->cfg.io_workers;
-  for (int k = 0; k < 4; k++) ctx->log_n[k] = std::min(g.log_n[k], ctx->log_cap[k]);
+  for (int k = 0; k < 5; k++) ctx->log_n[k] = std::min(g.log_n[k], ctx->log_cap[k]);
   ctx->has_run = true;
   out->v[GFS_STAT_wall_ns] = (int64_t)(now_ns() - w0);
   if (g.error) {
@@ -963,14 +969,14 @@ extern "C" int gfs_run_consume(gfs_ctx* ctx, const gfs_program* prog, void* dst,
 // ------------------------------------------------------------------- logs
 
 extern "C" int gfs_log_len(gfs_ctx* ctx, int kind, int64_t* n) {
-  if (!ctx || !n || kind < 0 || kind > 3) return fail(GFS_EINVAL, "gfs_log_len: bad argument");
+  if (!ctx || !n || kind < 0 || kind > GFS_LOG_TIMELINE) return fail(GFS_EINVAL, "gfs_log_len: bad argument");
   *n = (int64_t)ctx->log_n[kind];
   return GFS_OK;
 }
 
 extern "C" int gfs_log_copy(gfs_ctx* ctx, int kind, int64_t* out, int64_t cap_records) {
-  if (!ctx || !out || kind < 0 || kind > 3) return fail(GFS_EINVAL, "gfs_log_copy: bad argument");
-  const int width[4] = {3, 4, 3, 2};
+  if (!ctx || !out || kind < 0 || kind > GFS_LOG_TIMELINE) return fail(GFS_EINVAL, "gfs_log_copy: bad argument");
+  const int width[5] = {3, 4, 3, 2, 4};
   int64_t n = std::min<int64_t>((int64_t)ctx->log_n[kind], cap_records);
   if (n > 0)
     CUDA_TRY(cudaMemcpy(out, ctx->d_logs[kind].p, (size_t)(n * width[kind]) * 8, cudaMemcpyDeviceToHost));

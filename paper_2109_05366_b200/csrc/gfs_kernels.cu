@@ -164,6 +164,18 @@ __device__ void log_rec(const DevCtx& c, int kind, long long a, long long b, lon
   if (width > 3) r[3] = e;
 }
 
+// Timeline record (thread 0; gfs_config.timeline): what a CTA was doing, and when.
+__device__ void tl_rec(const DevCtx& c, int kind, int tb, long long bytes, uint64_t t0, uint64_t t1) {
+  if (!c.timeline) return;
+  unsigned long long i = atomicAdd(&c.g->log_n[GFS_LOG_TIMELINE], 1ull);
+  if (i >= c.log_cap[GFS_LOG_TIMELINE]) return;  // full: later records are dropped
+  long long* r = c.logs[GFS_LOG_TIMELINE] + i * 4;
+  r[0] = ((long long)kind << 56) | ((long long)blockIdx.x << 32) | (long long)(uint32_t)tb;
+  r[1] = bytes;
+  r[2] = (long long)t0;
+  r[3] = (long long)t1;
+}
+
 // ------------------------------------------------------------ frame ownership
 
 __device__ __forceinline__ unsigned long long page_key(int64_t fid, int64_t page) {
@@ -566,7 +578,9 @@ __device__ int64_t rpc_call(const DevCtx& c, Smem& s, int64_t fid, int64_t off, 
     }
   }
   atomicMax(&c.done_pos[pos & c.ring_mask], pos + 1);
-  ST(wait_ns) += (long long)(globaltimer() - tw);
+  const uint64_t tr = globaltimer();
+  ST(wait_ns) += (long long)(tr - tw);
+  tl_rec(c, GFS_TL_RPC, s.tb, n, tw, tr);
   if (n < 0) {
     set_error(c, ERR_IO, (int)fid, (unsigned long long)off);
     return -1;
@@ -1530,9 +1544,18 @@ __device__ bool run_tb(const DevCtx& c, Smem& s, float* cons_smem, int tb, int& 
     while (seg_off < len) {
       int64_t size = c.request_bytes < len - seg_off ? c.request_bytes : len - seg_off;
       uint8_t* d = c.dst ? c.dst + pos + seg_off : nullptr;
+      const uint64_t tg = c.timeline ? globaltimer() : 0;
       int64_t got = gread<BS>(c, s, fid, base + seg_off, size, base + len, d, bad_words);
       if (got < 0) return false;
-      if (c.cons.kind != GFS_CONSUME_NONE && d) consume<BS>(c, cons_smem, d, got, base + seg_off, acc);
+      if (c.timeline && tid == 0) tl_rec(c, GFS_TL_GREAD, tb, got, tg, globaltimer());
+      if (c.cons.kind != GFS_CONSUME_NONE && d) {
+        const uint64_t tc = c.timeline ? globaltimer() : 0;
+        consume<BS>(c, cons_smem, d, got, base + seg_off, acc);
+        if (c.timeline) {
+          __syncthreads();
+          if (tid == 0) tl_rec(c, GFS_TL_CONSUME, tb, got, tc, globaltimer());
+        }
+      }
       seg_off += got;
       if (got < size) break;  // short read: rest of the segment is skipped
     }

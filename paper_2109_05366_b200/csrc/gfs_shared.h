@@ -54,7 +54,7 @@ struct DevGlobals {
   unsigned long long req_base;     // ring position of this launch's first request
   int base_state;                  // 0 = unset, 1 = being set, 2 = ready
   int pad0;
-  unsigned long long log_n[4];     // log record counts
+  unsigned long long log_n[5];     // log record counts
   unsigned long long recycled_n;   // released (EOF) frames stack depth
   int lock;                        // global policy structural lock
   int recycled_lock;
@@ -80,7 +80,7 @@ struct DevCtx {
   int64_t nframes;
   int64_t quota;             // per-TB LRA queue cap
   int64_t gfifo_cap;
-  int32_t policy, readahead, transfer, raw_mode, log, verify, pcie_disabled;
+  int32_t policy, readahead, transfer, raw_mode, log, verify, pcie_disabled, timeline;
   int32_t n_files, n_tb, n_ctas;
   uint32_t ring_mask;
   uint64_t timeout_ns;
@@ -124,8 +124,8 @@ struct DevCtx {
   // counters (device): [n_ctas][GFS_NSTATS]
   long long* stats;
   // logs (device): [cap][width]
-  long long* logs[4];
-  unsigned long long log_cap[4];
+  long long* logs[5];
+  unsigned long long log_cap[5];
 };
 
 }  // namespace gfs

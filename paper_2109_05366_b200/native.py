@@ -20,8 +20,9 @@ READAHEAD = {"static": 0, "adaptive": 1}
 TRANSFER = {"zerocopy": 0, "dma": 1, "bounce": 2, "mapped_dma": 3, "mapped": 4,
             "mapped_hybrid": 5}
 O_RDONLY, O_RDWR = 0, 2
-LOG_DELIVERIES, LOG_RPCS, LOG_VICTIMS, LOG_WINDOWS = 0, 1, 2, 3
-LOG_WIDTH = {LOG_DELIVERIES: 3, LOG_RPCS: 4, LOG_VICTIMS: 3, LOG_WINDOWS: 2}
+LOG_DELIVERIES, LOG_RPCS, LOG_VICTIMS, LOG_WINDOWS, LOG_TIMELINE = 0, 1, 2, 3, 4
+LOG_WIDTH = {LOG_DELIVERIES: 3, LOG_RPCS: 4, LOG_VICTIMS: 3, LOG_WINDOWS: 2, LOG_TIMELINE: 4}
+TL_RPC, TL_GREAD, TL_CONSUME = 0, 1, 2
 
 # Every entry point declared in include/gfs.h (tests check the library exports them).
 EXPORTS = ["gfs_create", "gfs_destroy", "gfs_gopen", "gfs_gclose", "gfs_file_size", "gfs_run",
@@ -41,7 +42,7 @@ class GfsConfig(C.Structure):
         ("transfer", C.c_int32), ("io_workers", C.c_int32), ("io_direct", C.c_int32),
         ("device", C.c_int32), ("cta_threads", C.c_int32), ("max_ctas", C.c_int32),
         ("raw_mode", C.c_int32), ("pcie_disabled", C.c_int32), ("log", C.c_int32),
-        ("verify", C.c_int32), ("reserved", C.c_int32 * 3),
+        ("verify", C.c_int32), ("timeline", C.c_int32), ("reserved", C.c_int32 * 2),
     ]
 
 

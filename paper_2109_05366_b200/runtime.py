@@ -57,6 +57,7 @@ def native_config(cfg: ExperimentConfig, max_request_bytes: int = 0) -> native.G
     c.pcie_disabled = int(bool(cfg["mode.pcie_disabled"]))
     c.log = int(bool(cfg["mode.deterministic"]))
     c.verify = int(bool(cfg["mode.verify"]))
+    c.timeline = int(bool(cfg["mode.timeline"]))
     return c
 
 
@@ -67,6 +68,7 @@ class RunResult:
     rpcs: np.ndarray | None = None
     victims: np.ndarray | None = None
     windows: np.ndarray | None = None
+    timeline: np.ndarray | None = None  # [n, 4] GFS_LOG_TIMELINE records (mode.timeline)
     extra: dict = field(default_factory=dict)
 
     @property
@@ -214,6 +216,8 @@ class GpuFS:
                      "gfs_run")
         del keep
         res = RunResult(stats=dict(zip(names, list(out))))
+        if self._ncfg.timeline:
+            res.timeline = self.log(native.LOG_TIMELINE)
         if self._ncfg.log:
             res.deliveries = self.log(native.LOG_DELIVERIES)
             res.rpcs = self.log(native.LOG_RPCS)

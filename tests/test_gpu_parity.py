@@ -209,3 +209,22 @@ def test_record_then_host_replay_round_trip(synth_dir, tmp_path):
     hrep = host.run()
     assert hrep["user_bytes"] == rep["user_bytes"] == 16 * MiB
     assert hrep["ssd_requests"] == len(recs)
+
+
+def test_timeline_log(synth_dir):
+    """mode.timeline: one rpc record per RPC, one gread record per gread, intervals ordered
+    on the device clock, every resident CTA present."""
+    from paper_2109_05366_b200 import timeline
+    from paper_2109_05366_b200.runtime import Simulation
+    over = {"workload.n_tb": 32, "workload.file_bytes": 32 * MiB, "workload.request_bytes": 64 * KiB,
+            "gpufs.prefetch_bytes": 60 * KiB, "gpu.sm_count": 4, "io.dir": synth_dir,
+            "mode.timeline": True}
+    sim = Simulation(ExperimentConfig(over), 42)
+    rep = sim.run()
+    d = timeline.decode(sim.result.timeline)
+    assert int((d["kind"] == 0).sum()) == rep["rpc_count"]
+    assert int((d["kind"] == 1).sum()) == rep["greads"]
+    assert int(d["bytes"][d["kind"] == 1].sum()) == 32 * MiB
+    assert (d["t1"] >= d["t0"]).all()
+    s = timeline.summary(sim.result.timeline)
+    assert 0 < s["io_busy_frac"] <= 1 and s["ctas"] == min(32, sim.result.stats["ctas"])
