@@ -79,6 +79,18 @@ def _arms_bench(base):
                 "gpufs.cache_bytes": cache, **over})
 
 
+def _arms_mosaic(base):
+    """The Mosaic-style random workload (workloads.py:84-102): page-aligned
+    random 4 KiB reads, 4 KiB vs 64 KiB GPU pages, no prefetch (prefetching a random stream
+    only wastes transfer)."""
+    for page in (4 * KiB, 64 * KiB):
+        yield f"random-page-{page}", base.copy_with({
+            "workload.kind": "random", "workload.n_tb": 256, "workload.requests_per_tb": 256,
+            "workload.file_bytes": 1 << 30, "workload.request_bytes": 4 * KiB,
+            "gpufs.page_size": page, "gpufs.prefetch_bytes": 0,
+            "gpufs.cache_bytes": 256 * MiB, "gpufs.policy": "per-tb-lra"})
+
+
 def _run_fig3(base, out_dir):
     """The GPU's access pattern vs its host-only replay (experiments.py:135-156): a raw-mode
     gread run (no GPU page cache) records its RPC trace, then host threads replay it with
@@ -99,7 +111,7 @@ def _run_fig3(base, out_dir):
 
 
 PRESETS = {"fig2": _arms_fig2, "fig3": _run_fig3, "fig8": _arms_fig8,
-           "fig10micro": _arms_fig10micro, "bench": _arms_bench}
+           "fig10micro": _arms_fig10micro, "bench": _arms_bench, "mosaic": _arms_mosaic}
 
 
 def run_preset(name: str, base: ExperimentConfig, out_dir: str) -> str:

@@ -71,3 +71,11 @@ def test_replay_cli_and_trace_errors(tmp_path, capsys):
     _write_trace(bad, [(0, 0, fb - 4096, 8192)])  # past EOF
     assert cli.main(["replay", bad, "--set", f"workload.file_bytes={fb}", "--set",
                      f"io.dir={tmp_path}"]) == 2
+
+
+def test_mosaic_and_fig3_presets_exist():
+    base = ExperimentConfig()
+    arms = dict(PRESETS["mosaic"](base))
+    assert set(arms) == {"random-page-4096", "random-page-65536"}
+    assert all(c["workload.kind"] == "random" and c["gpufs.prefetch_bytes"] == 0 for c in arms.values())
+    assert "fig3" in PRESETS
