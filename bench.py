@@ -365,10 +365,12 @@ def peaks() -> dict:
 def reference_main(args, dist: Dist) -> None:
     if dist.rank != 0:
         return
-    from paper_2109_05366_b200.runtime import ensure_synthetic  # noqa: F401
-    size = int(args.size_gib * GiB)
-    cfg = make_cfg(headline_overrides(size, args.gpus, args.dir), args.set)
-    path = ensure_file(cfg, dist)
+    from paper_2109_05366_b200.runtime import ensure_synthetic
+    # rank 0 alone (the other ranks have already left): no barriers from here on; the CPU
+    # implementation reads one GPU's shard of the workload
+    size = fit_size(args.dir, int(args.size_gib * GiB), 1)
+    cfg = make_cfg(headline_overrides(size, 1, args.dir), args.set)
+    path = ensure_synthetic(cfg["io.dir"], 0, cfg["workload.file_bytes"])
     threads = os.cpu_count() or 1
     sample = size  # the whole workload per step (~1-2 s on 16 host cores)
     for _ in range(args.warmup):

@@ -52,6 +52,12 @@ def main():
                     "cta_meta": round(st["meta_ns"] / cta_ns, 3),
                     "cta_copy": round(st["copy_ns"] / cta_ns, 3),
                     "us_rpc_wait": round(st["wait_ns"] / max(1, st["rpc_count"]) / 1e3, 1),
+                    "greads": st["greads"],
+                    "us_gread_meta": round(st["meta_ns"] / max(1, st["greads"]) / 1e3, 2),
+                    "us_gread_copy": round(st["copy_ns"] / max(1, st["greads"]) / 1e3, 2),
+                    "us_gread_install": round(st["install_ns"] / max(1, st["greads"]) / 1e3, 2),
+                    "us_gread_other": round((cta_ns - st["wait_ns"] - st["meta_ns"] - st["copy_ns"]
+                                             - st["install_ns"]) / max(1, st["greads"]) / 1e3, 2),
                     "host_pread": round(st["host_pread_ns"] / (W * ns), 3),
                     "host_xfer": round(st["host_xfer_ns"] / (W * ns), 3),
                     "host_idle": round(st["host_idle_ns"] / (W * ns), 3),
