@@ -32,9 +32,11 @@ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
 }
 
 // W(f, i) = mix64(page_tag(f, i >> 9) ^ i): the synthetic content law.
+__device__ __forceinline__ uint64_t block_tag(int64_t cid, int64_t i) {
+  return mix64(((uint64_t)cid << 40) ^ (uint64_t)(i >> 9) ^ 0xA5A5A5A5A5A5A5A5ull);
+}
 __device__ __forceinline__ uint64_t word_law(int64_t cid, int64_t i) {
-  uint64_t tag = mix64(((uint64_t)cid << 40) ^ (uint64_t)(i >> 9) ^ 0xA5A5A5A5A5A5A5A5ull);
-  return mix64(tag ^ (uint64_t)i);
+  return mix64(block_tag(cid, i) ^ (uint64_t)i);
 }
 
 __device__ __forceinline__ uint64_t globaltimer() {
@@ -1012,13 +1014,15 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
   int bad = 0;
   const uint4* src4 = (const uint4*)(span_buf + s.b.src_off[0]);  // pages are consecutive
   const bool contiguous = s.b.src_off[kk - 1] == s.b.src_off[0] + (int64_t)(kk - 1) * pg;
+  // vector v of the batch is vector w of page j: shifts when the page size is a power of 2
+  const int vsh = (pg & (pg - 1)) == 0 ? __ffsll(pg) - 1 - 4 : -1;
   for (int64_t v0 = tid; v0 < nvec; v0 += 4 * BS) {
     uint4 q[4];
 #pragma unroll
     for (int u = 0; u < 4; u++) {
       const int64_t v = v0 + u * BS;
       if (v < nvec) {
-        const int j = (int)(v / vpp);
+        const int j = (int)(vsh >= 0 ? v >> vsh : v / vpp);
         const int64_t w = v - (int64_t)j * vpp;
         const uint4* sp = contiguous ? src4 + v : (const uint4*)(span_buf + s.b.src_off[j]) + w;
         q[u] = (w << 4) < s.b.nb[j] ? (c.transfer != GFS_XFER_ZEROCOPY ? ld16<SRC_HBM>(sp) : ld16<SRC_SYS>(sp))
@@ -1029,7 +1033,7 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
     for (int u = 0; u < 4; u++) {
       const int64_t v = v0 + u * BS;
       if (v >= nvec) break;
-      const int j = (int)(v / vpp);
+      const int j = (int)(vsh >= 0 ? v >> vsh : v / vpp);
       const int64_t w = v - (int64_t)j * vpp;
       const int64_t nbj = s.b.nb[j];
       if ((w << 4) + 16 > nbj) continue;  // sub-16 B EOF tail: byte loop below
@@ -1038,10 +1042,11 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
       const int64_t ps = (p0 + j) * pg;
       if (dst_ok && ps >= g_pos && ps + nbj <= g_end)
         ((uint4*)(d0 + (ps - g_pos)))[w] = q[u];
-      if (chk) {
+      if (chk) {  // both words of a vector share one 4 KiB block tag
         const int64_t wi = (ps >> 3) + 2 * w;
+        const uint64_t tag = block_tag(cid, wi);
         const uint64_t lo = ((uint64_t)q[u].y << 32) | q[u].x, hi = ((uint64_t)q[u].w << 32) | q[u].z;
-        bad += (lo != word_law(cid, wi)) + (hi != word_law(cid, wi + 1));
+        bad += (lo != mix64(tag ^ (uint64_t)wi)) + (hi != mix64(tag ^ (uint64_t)(wi + 1)));
       }
     }
   }
@@ -1317,11 +1322,23 @@ __device__ __forceinline__ float decode_f32(uint32_t u) { return (float)(u >> 8)
 constexpr int GEMV_ROWS = 1024;          // rows of one request accumulated in shared memory
 constexpr int GEMVT_SMEM_COLS = 8192;    // A^T x2 accumulated per CTA in shared memory up to this
 
+constexpr int64_t CONS_SMEM_MAX = 48 * 1024;  // dynamic shared memory without the opt-in
+
+// Kmeans keeps one private [k, cols] accumulator (and counts) per warp when it fits: lanes
+// then update distinct words with plain shared stores, no atomics.  Needs cols >= 32.
+__host__ __device__ inline bool kmeans_warp_acc(const gfs_consumer& k, int bs) {
+  const int64_t w = bs / 32, kd = (int64_t)k.k * k.cols;
+  return k.cols >= 32 && (1 + w) * kd * 4 + w * k.k * 4 <= CONS_SMEM_MAX;
+}
+
 // Dynamic shared memory a consumer needs (the launch passes it; 0 for the plain gread path).
-__host__ __device__ inline int64_t consumer_smem_bytes(const gfs_consumer& k) {
+__host__ __device__ inline int64_t consumer_smem_bytes(const gfs_consumer& k, int bs) {
   if ((k.kind == GFS_CONSUME_GEMVT_F32 || k.kind == GFS_CONSUME_BICG_F32) && k.cols <= GEMVT_SMEM_COLS)
     return k.cols * 4;
-  if (k.kind == GFS_CONSUME_KMEANS_F32) return 2 * (int64_t)k.k * k.cols * 4 + (int64_t)k.k * 4;
+  if (k.kind == GFS_CONSUME_KMEANS_F32) {
+    const int64_t w = bs / 32, kd = (int64_t)k.k * k.cols;
+    return kmeans_warp_acc(k, bs) ? (1 + w) * kd * 4 + w * k.k * 4 : 2 * kd * 4 + k.k * 4;
+  }
   return 0;
 }
 
@@ -1333,13 +1350,16 @@ __device__ void gemv_part(const gfs_consumer& k, const uint4* v4, int64_t ne, in
   const int64_t M = k.cols;
   const int64_t row_lo = e0 / M, row_hi = (e0 + ne - 1) / M;
   const bool local = row_hi - row_lo < GEMV_ROWS;
+  // element e0 + l sits at (row_lo + (r0 + l) / M, (r0 + l) % M): 32-bit division
+  const uint32_t r0 = (uint32_t)(e0 - row_lo * M), M32 = (uint32_t)M;
   if (local)
     for (int i = tid; i <= (int)(row_hi - row_lo); i += BS) rows[i] = 0.f;
   __syncthreads();
   for (int64_t i = tid; i < (ne >> 2); i += BS) {
     const uint4 u = __ldcg(v4 + i);
-    const int64_t e = e0 + 4 * i;
-    const int64_t row = e / M, col = e - row * M;
+    const uint32_t l = r0 + 4 * (uint32_t)i;
+    const uint32_t q = l / M32;
+    const int64_t row = row_lo + q, col = l - q * M32;
     const float4 xv = *(const float4*)(k.x + col);
     float p = decode_f32(u.x) * xv.x + decode_f32(u.y) * xv.y + decode_f32(u.z) * xv.z +
               decode_f32(u.w) * xv.w;
@@ -1371,10 +1391,13 @@ __device__ void gemvt_part(const gfs_consumer& k, float* acc, const uint4* v4, i
                            int tid, int bs) {
   const int64_t M = k.cols;
   const bool sm = M <= GEMVT_SMEM_COLS;
+  const int64_t row_lo = e0 / M;
+  const uint32_t r0 = (uint32_t)(e0 - row_lo * M), M32 = (uint32_t)M;
   for (int64_t i = tid; i < (ne >> 2); i += bs) {
     const uint4 u = __ldcg(v4 + i);
-    const int64_t e = e0 + 4 * i;
-    const int64_t row = e / M, col = e - row * M;
+    const uint32_t l = r0 + 4 * (uint32_t)i;
+    const uint32_t q = l / M32;
+    const int64_t row = row_lo + q, col = l - q * M32;
     const float xr = k.x2[row];
     float* dst = sm ? acc + col : k.y2 + col;
     atomicAdd(dst + 0, decode_f32(u.x) * xr);
@@ -1386,47 +1409,68 @@ __device__ void gemvt_part(const gfs_consumer& k, float* acc, const uint4* v4, i
 
 // Kmeans assignment + accumulation, one thread per point.  Distances are summed over the
 // features in order with IEEE round-to-nearest steps and no contraction (the bits a
-// float32 reference gets); the features are read once, as 16-byte vectors.
-__device__ void kmeans_part(const gfs_consumer& k, float* smem, const uint8_t* data, int64_t np,
-                            int tid, int bs) {
+// float32 reference gets); the features are read once, as 16-byte vectors.  Warp-uniform
+// loop: a warp takes 32 consecutive points per step.
+template <int BS>
+__device__ void kmeans_part(const gfs_consumer& k, float* smem, const uint8_t* data, int64_t np) {
   const int K = k.k;
   const int D = (int)k.cols;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int W = BS / 32;
+  const bool wacc = kmeans_warp_acc(k, BS);
   const float* cent = smem;
-  float* acc = smem + K * D;
-  unsigned* cnt = (unsigned*)(smem + 2 * K * D);
-  const int lane = tid & 31;
-  for (int64_t p = tid; p < np; p += bs) {
-    const uint4* pv = (const uint4*)(data + p * (int64_t)D * 4);
-    float d[GFS_KMEANS_MAX_K];
+  float* acc = smem + K * D + (wacc ? warp * K * D : 0);
+  unsigned* cnt = (unsigned*)(smem + K * D + (wacc ? W : 1) * K * D) + (wacc ? warp * K : 0);
+  for (int64_t pb = (int64_t)warp * 32; pb < np; pb += BS) {
+    const int64_t p = pb + lane;
+    const bool valid = p < np;
+    const uint4* pv = (const uint4*)(data + (valid ? p : 0) * (int64_t)D * 4);
+    int best = 0;
+    if (valid) {
+      float d[GFS_KMEANS_MAX_K];
 #pragma unroll
-    for (int c = 0; c < GFS_KMEANS_MAX_K; c++) d[c] = 0.f;
-    for (int j = 0; j < D; j += 4) {
-      const uint4 u = __ldcg(pv + (j >> 2));
-      const float v[4] = {decode_f32(u.x), decode_f32(u.y), decode_f32(u.z), decode_f32(u.w)};
+      for (int c = 0; c < GFS_KMEANS_MAX_K; c++) d[c] = 0.f;
+      for (int j = 0; j < D; j += 4) {
+        const uint4 u = __ldcg(pv + (j >> 2));
+        const float v[4] = {decode_f32(u.x), decode_f32(u.y), decode_f32(u.z), decode_f32(u.w)};
 #pragma unroll
-      for (int c = 0; c < GFS_KMEANS_MAX_K; c++) {
-        if (c < K) {
+        for (int c = 0; c < GFS_KMEANS_MAX_K; c++) {
+          if (c < K) {
 #pragma unroll
-          for (int q = 0; q < 4; q++) {
-            const float df = __fsub_rn(v[q], cent[c * D + j + q]);
-            d[c] = __fadd_rn(d[c], __fmul_rn(df, df));
+            for (int q = 0; q < 4; q++) {
+              const float df = __fsub_rn(v[q], cent[c * D + j + q]);
+              d[c] = __fadd_rn(d[c], __fmul_rn(df, df));
+            }
           }
         }
       }
-    }
-    int best = 0;
-    float bd = d[0];
+      float bd = d[0];
 #pragma unroll
-    for (int c = 1; c < GFS_KMEANS_MAX_K; c++)
-      if (c < K && d[c] < bd) { bd = d[c]; best = c; }
-    atomicAdd(&cnt[best], 1u);
-    // lanes start at different features, so lanes of one cluster hit different words
+      for (int c = 1; c < GFS_KMEANS_MAX_K; c++)
+        if (c < K && d[c] < bd) { bd = d[c]; best = c; }
+    }
     const uint32_t* pw = (const uint32_t*)pv;
     float* row = acc + best * D;
-    for (int t = 0; t < D; t++) {
-      int j = lane + t;
-      while (j >= D) j -= D;
-      atomicAdd(&row[j], decode_f32(__ldcg(pw + j)));
+    if (wacc) {
+      for (int c = 0; c < K; c++) {  // per-warp counts: one ballot per centroid
+        const unsigned m = __ballot_sync(0xffffffffu, valid && best == c);
+        if (lane == 0) cnt[c] += __popc(m);
+      }
+      // lanes start at different features (cols >= 32), so in every step the 32 lanes
+      // touch 32 distinct words of this warp's accumulator: plain read-modify-write
+      for (int t = 0; t < D; t++) {
+        int j = lane + t;
+        if (j >= D) j -= D;
+        if (valid) row[j] += decode_f32(__ldcg(pw + j));
+        __syncwarp();
+      }
+    } else if (valid) {
+      atomicAdd(&cnt[best], 1u);
+      for (int t = 0; t < D; t++) {
+        int j = lane + t;
+        while (j >= D) j -= D;
+        atomicAdd(&row[j], decode_f32(__ldcg(pw + j)));
+      }
     }
   }
 }
@@ -1434,7 +1478,7 @@ __device__ void kmeans_part(const gfs_consumer& k, float* smem, const uint8_t* d
 // All threads, once per launch before the first TB: zero / load the consumer's shared state.
 __device__ void consume_init(const DevCtx& c, float* smem) {
   const gfs_consumer& k = c.cons;
-  const int64_t n = consumer_smem_bytes(k) / 4;
+  const int64_t n = consumer_smem_bytes(k, blockDim.x) / 4;
   if (n == 0) return;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) smem[i] = 0.f;
   if (k.kind == GFS_CONSUME_KMEANS_F32)
@@ -1477,7 +1521,7 @@ __device__ void consume(const DevCtx& c, float* smem, const uint8_t* data, int64
     gemvt_part(k, smem, (const uint4*)data, n >> 2, file_off >> 2, tid, BS);
     gemv_part<BS>(k, (const uint4*)data, n >> 2, file_off >> 2);
   } else if (k.kind == GFS_CONSUME_KMEANS_F32) {
-    kmeans_part(k, smem, data, n / (k.cols * 4), tid, BS);
+    kmeans_part<BS>(k, smem, data, n / (k.cols * 4));
   }
 }
 
@@ -1489,11 +1533,18 @@ __device__ void consume_flush(const DevCtx& c, float* smem, ConsAcc& acc) {
     __syncthreads();
     if (kind == GFS_CONSUME_KMEANS_F32) {
       const int64_t kd = (int64_t)k.k * k.cols;
-      for (int64_t i = threadIdx.x; i < kd; i += BS)
-        if (smem[kd + i] != 0.f) atomicAdd(&k.y[i], smem[kd + i]);
-      const unsigned* cnt = (const unsigned*)(smem + 2 * kd);
-      for (int i = threadIdx.x; i < k.k; i += BS)
-        if (cnt[i]) atomicAdd(&k.out[i], (unsigned long long)cnt[i]);
+      const int nacc = kmeans_warp_acc(k, BS) ? BS / 32 : 1;  // accumulator copies
+      for (int64_t i = threadIdx.x; i < kd; i += BS) {
+        float v = 0.f;
+        for (int w = 0; w < nacc; w++) v += smem[kd + w * kd + i];
+        if (v != 0.f) atomicAdd(&k.y[i], v);
+      }
+      const unsigned* cnt = (const unsigned*)(smem + (1 + nacc) * kd);
+      for (int i = threadIdx.x; i < k.k; i += BS) {
+        unsigned long long v = 0;
+        for (int w = 0; w < nacc; w++) v += cnt[w * k.k + i];
+        if (v) atomicAdd(&k.out[i], v);
+      }
     } else if (k.cols <= GEMVT_SMEM_COLS) {
       for (int64_t i = threadIdx.x; i < k.cols; i += BS)
         if (smem[i] != 0.f) atomicAdd(&k.y2[i], smem[i]);
@@ -1702,7 +1753,7 @@ __global__ void verify_dst_kernel(const uint8_t* buf, const int64_t* segs, const
 // ------------------------------------------------------------------ host-side launchers
 
 cudaError_t launch_gread(const DevCtx& c, int cta_threads, cudaStream_t st) {
-  const size_t smem = (size_t)consumer_smem_bytes(c.cons);
+  const size_t smem = (size_t)consumer_smem_bytes(c.cons, cta_threads == 128 || cta_threads == 512 ? cta_threads : 256);
   switch (cta_threads) {
     case 128: gread_driver<128><<<c.n_ctas, 128, smem, st>>>(c); break;
     case 512: gread_driver<512><<<c.n_ctas, 512, smem, st>>>(c); break;
