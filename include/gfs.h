@@ -80,7 +80,9 @@ typedef struct gfs_config {
   int32_t log;             /* record delivery / RPC / victim logs on the device */
   int32_t verify;          /* check every fetched word against the synthetic law */
   int32_t timeline;        /* record the GFS_LOG_TIMELINE log (mode.timeline) */
-  int32_t reserved[2];
+  int32_t k1_tma;          /* gpu.k1_copy: 1 = span -> frame/user copies by TMA bulk copies
+                              through a shared-memory ring, 0 = 16-byte vector loads/stores */
+  int32_t reserved[1];
 } gfs_config;
 
 /* One gread program set (workloads.py:24-31 programs, flattened).

@@ -40,6 +40,7 @@
 namespace gfs {
 cudaError_t launch_gread(const DevCtx& c, int cta_threads, cudaStream_t st);
 cudaError_t occupancy_gread(int cta_threads, int* blocks_per_sm);
+int64_t gread_tma_offset(const gfs_consumer& k, int cta_threads);
 cudaError_t launch_checksum(const void* buf, uint64_t nbytes, uint64_t word_base,
                             unsigned long long* out, int sms, cudaStream_t st);
 cudaError_t launch_verify_dst(const void* buf, const int64_t* segs, const int64_t* seg_dst,
@@ -881,6 +882,15 @@ extern "C" int gfs_run_consume(gfs_ctx* ctx, const gfs_program* prog, void* dst,
   c.stats = ctx->d_stats;
   if (cons) c.cons = *cons;
   else c.cons.kind = GFS_CONSUME_NONE;
+  c.tma = 0;
+  c.tma_off = 0;
+  if (cfg.k1_tma) {  // the stage ring needs room next to the consumer's shared state
+    const int64_t off = gread_tma_offset(c.cons, cfg.cta_threads);
+    if (off >= 0) {
+      c.tma = 1;
+      c.tma_off = (int32_t)off;
+    }
+  }
   for (int k = 0; k < 5; k++) {
     c.logs[k] = ctx->d_logs[k].p;
     c.log_cap[k] = ctx->log_cap[k];

@@ -70,6 +70,45 @@ __device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned lon
   return *(volatile const unsigned long long*)p;
 }
 
+// ------------------------------------------------------------------ TMA bulk copies
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(unsigned long long* b, int count) {
+  asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+
+// global -> shared bulk copy completing `bytes` of transaction count on `bar` (one thread)
+__device__ __forceinline__ void tma_load(void* sdst, const void* gsrc, uint32_t bytes, unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(sdst)), "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done)
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done)
+                 : "r"(smem_u32(bar)), "r"(parity)
+                 : "memory");
+}
+
+// shared -> global bulk copy in the current bulk group (one thread)
+__device__ __forceinline__ void tma_store(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void tma_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void tma_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  asm volatile("fence.proxy.async.global;" ::: "memory");  // async-proxy writes -> generic readers
+}
+
 // source kinds for K1/K2 loads
 enum { SRC_HBM = 0, SRC_SYS = 1 };
 
@@ -86,7 +125,12 @@ __device__ __forceinline__ uint8_t ld1(const uint8_t* p) {
 
 // ----------------------------------------------------------------- CTA state
 
+constexpr int TMA_NST = 4;        // K1 stage ring: stages
+constexpr int64_t TMA_CH = 8192;  // bytes per stage (one bulk load, 1-2 bulk stores per page)
+
 struct Smem {
+  unsigned long long tma_bar[TMA_NST];  // stage "full" mbarriers (tx-count)
+  unsigned long long tma_seq;           // chunks staged since launch (stage / parity)
   // broadcast from thread 0
   int act;
   int abort;
@@ -1014,6 +1058,73 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
   int bad = 0;
   const uint4* src4 = (const uint4*)(span_buf + s.b.src_off[0]);  // pages are consecutive
   const bool contiguous = s.b.src_off[kk - 1] == s.b.src_off[0] + (int64_t)(kk - 1) * pg;
+  bool full_pages = true;
+  for (int j = 0; j < kk; j++) full_pages &= s.b.nb[j] == pg;
+  const bool use_tma = c.tma && c.transfer != GFS_XFER_ZEROCOPY && contiguous && full_pages &&
+                       (((uintptr_t)src4) & 15) == 0;
+  if (use_tma) {
+    // K1 by TMA: thread 0 streams the batch HBM -> shared-memory stage ring -> frames (and
+    // whole pages -> user buffer) with bulk copies, TMA_NST stages in flight; when the word
+    // check is on, every thread checks each stage while it sits in shared memory.
+    extern __shared__ __align__(128) float cons_smem[];
+    uint8_t* ring = (uint8_t*)cons_smem + c.tma_off;
+    const int64_t total_b = (int64_t)kk * pg;
+    const int nch = (int)((total_b + TMA_CH - 1) / TMA_CH);
+    const unsigned long long G0 = s.tma_seq;
+    const uint8_t* srcb = (const uint8_t*)src4;
+    auto load = [&](int i) {
+      const int st = (int)((G0 + i) % TMA_NST);
+      const int64_t cb = min(TMA_CH, total_b - (int64_t)i * TMA_CH);
+      tma_load(ring + st * TMA_CH, srcb + (int64_t)i * TMA_CH, (uint32_t)cb, &s.tma_bar[st]);
+    };
+    if (tid == 0)
+      for (int i = 0; i < nch && i < TMA_NST; i++) load(i);
+    for (int i = 0; i < nch; i++) {
+      const unsigned long long G = G0 + i;
+      const int st = (int)(G % TMA_NST);
+      const uint32_t par = (uint32_t)((G / TMA_NST) & 1);
+      const int64_t b0 = (int64_t)i * TMA_CH;
+      const int64_t cb = min(TMA_CH, total_b - b0);
+      const uint8_t* sbuf = ring + st * TMA_CH;
+      if (chk || tid == 0) mbar_wait(&s.tma_bar[st], par);
+      if (chk) {
+        const uint4* sv = (const uint4*)sbuf;
+        const int64_t wbase = (p0 * pg + b0) >> 3;
+        for (int64_t v = tid; v < (cb >> 4); v += BS) {
+          const uint4 q = sv[v];
+          const int64_t wi = wbase + 2 * v;
+          const uint64_t tag = block_tag(cid, wi);
+          const uint64_t lo = ((uint64_t)q.y << 32) | q.x, hi = ((uint64_t)q.w << 32) | q.z;
+          bad += (lo != mix64(tag ^ (uint64_t)wi)) + (hi != mix64(tag ^ (uint64_t)(wi + 1)));
+        }
+        __syncthreads();  // every thread is done reading this stage
+      }
+      if (tid == 0) {
+        // the chunk's pieces: page j gets [max(b0, j pg), min(b0 + cb, (j+1) pg))
+        for (int64_t b = b0; b < b0 + cb;) {
+          const int j = (int)(b / pg);
+          const int64_t e = min(b0 + cb, (int64_t)(j + 1) * pg);
+          const int64_t po = b - (int64_t)j * pg;
+          tma_store(c.frames + (int64_t)s.b.frame[j] * pg + po, sbuf + (b - b0), (uint32_t)(e - b));
+          const int64_t ps = (p0 + j) * pg;
+          if (dst_ok && ps >= g_pos && ps + pg <= g_end)
+            tma_store(d0 + (ps - g_pos) + po, sbuf + (b - b0), (uint32_t)(e - b));
+          b = e;
+        }
+        tma_commit();
+        if (i >= 1 && i - 1 + TMA_NST < nch) {  // refill the stage chunk i - 1 used
+          tma_wait_read<1>();                   // its stores have read it (chunk i's may not)
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          load(i - 1 + TMA_NST);
+        }
+      }
+    }
+    if (tid == 0) {
+      tma_wait_all();
+      s.tma_seq = G0 + nch;
+    }
+    __syncthreads();
+  } else {
   // vector v of the batch is vector w of page j: shifts when the page size is a power of 2
   const int vsh = (pg & (pg - 1)) == 0 ? __ffsll(pg) - 1 - 4 : -1;
   for (int64_t v0 = tid; v0 < nvec; v0 += 4 * BS) {
@@ -1050,6 +1161,7 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
       }
     }
   }
+  }  // LDG path
   for (int j = 0; j < kk; j++) {  // EOF page tails that are not a multiple of 16 bytes
     const int64_t nbj = s.b.nb[j];
     if ((nbj & 15) == 0) continue;
@@ -1342,6 +1454,14 @@ __host__ __device__ inline int64_t consumer_smem_bytes(const gfs_consumer& k, in
   return 0;
 }
 
+// Where the K1 stage ring starts in dynamic shared memory, and the launch's total.
+__host__ __device__ inline int64_t tma_ring_offset(const gfs_consumer& k, int bs) {
+  return (consumer_smem_bytes(k, bs) + 127) / 128 * 128;
+}
+inline int64_t gread_smem_bytes(const gfs_consumer& k, int bs, int tma) {
+  return tma ? tma_ring_offset(k, bs) + TMA_NST * TMA_CH : consumer_smem_bytes(k, bs);
+}
+
 // y += A x over the request's rows (cols % 4 == 0: one row per 16-byte vector).
 template <int BS>
 __device__ void gemv_part(const gfs_consumer& k, const uint4* v4, int64_t ne, int64_t e0) {
@@ -1427,27 +1547,30 @@ __device__ void kmeans_part(const gfs_consumer& k, float* smem, const uint8_t* d
     const uint4* pv = (const uint4*)(data + (valid ? p : 0) * (int64_t)D * 4);
     int best = 0;
     if (valid) {
-      float d[GFS_KMEANS_MAX_K];
+      // centroids in groups of 4 (4 running sums in registers; the point's vectors are
+      // re-read from L1 per group): no local-memory spills under the 64-register cap
+      float bd = 0.f;
+      for (int c0 = 0; c0 < K; c0 += 4) {
+        float d[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int j = 0; j < D; j += 4) {
+          const uint4 u = __ldcg(pv + (j >> 2));
+          const float v[4] = {decode_f32(u.x), decode_f32(u.y), decode_f32(u.z), decode_f32(u.w)};
 #pragma unroll
-      for (int c = 0; c < GFS_KMEANS_MAX_K; c++) d[c] = 0.f;
-      for (int j = 0; j < D; j += 4) {
-        const uint4 u = __ldcg(pv + (j >> 2));
-        const float v[4] = {decode_f32(u.x), decode_f32(u.y), decode_f32(u.z), decode_f32(u.w)};
+          for (int cc = 0; cc < 4; cc++) {
+            if (c0 + cc < K) {
+              const float* ce = cent + (c0 + cc) * D + j;
 #pragma unroll
-        for (int c = 0; c < GFS_KMEANS_MAX_K; c++) {
-          if (c < K) {
-#pragma unroll
-            for (int q = 0; q < 4; q++) {
-              const float df = __fsub_rn(v[q], cent[c * D + j + q]);
-              d[c] = __fadd_rn(d[c], __fmul_rn(df, df));
+              for (int q = 0; q < 4; q++) {
+                const float df = __fsub_rn(v[q], ce[q]);
+                d[cc] = __fadd_rn(d[cc], __fmul_rn(df, df));
+              }
             }
           }
         }
-      }
-      float bd = d[0];
 #pragma unroll
-      for (int c = 1; c < GFS_KMEANS_MAX_K; c++)
-        if (c < K && d[c] < bd) { bd = d[c]; best = c; }
+        for (int cc = 0; cc < 4; cc++)
+          if (c0 + cc < K && (c0 + cc == 0 || d[cc] < bd)) { bd = d[cc]; best = c0 + cc; }
+      }
     }
     const uint32_t* pw = (const uint32_t*)pv;
     float* row = acc + best * D;
@@ -1640,6 +1763,11 @@ __global__ void __launch_bounds__(BS, 4) gread_driver(DevCtx c) {
   if (tid == 0) {
     for (int i = 0; i < GFS_NSTATS; i++) s.st[i] = 0;
     s.pull_n = 0;
+    s.tma_seq = 0;
+    if (c.tma) {
+      for (int i = 0; i < TMA_NST; i++) mbar_init(&s.tma_bar[i], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     // ring base for this launch: the daemon's completed-request count
     if (atomicCAS(&c.g->base_state, 0, 1) == 0) {
       c.g->req_base = ld_acquire_sys64(c.host_served);
@@ -1650,7 +1778,7 @@ __global__ void __launch_bounds__(BS, 4) gread_driver(DevCtx c) {
       __threadfence();
     }
   }
-  extern __shared__ float cons_smem[];  // consumer state (consumer_smem_bytes)
+  extern __shared__ __align__(128) float cons_smem[];  // consumer state, then the K1 stage ring
   consume_init(c, cons_smem);
   int bad_words = 0;
   ConsAcc acc;
@@ -1753,13 +1881,20 @@ __global__ void verify_dst_kernel(const uint8_t* buf, const int64_t* segs, const
 // ------------------------------------------------------------------ host-side launchers
 
 cudaError_t launch_gread(const DevCtx& c, int cta_threads, cudaStream_t st) {
-  const size_t smem = (size_t)consumer_smem_bytes(c.cons, cta_threads == 128 || cta_threads == 512 ? cta_threads : 256);
+  const size_t smem = (size_t)gread_smem_bytes(c.cons, cta_threads, c.tma);
   switch (cta_threads) {
     case 128: gread_driver<128><<<c.n_ctas, 128, smem, st>>>(c); break;
     case 512: gread_driver<512><<<c.n_ctas, 512, smem, st>>>(c); break;
     default: gread_driver<256><<<c.n_ctas, 256, smem, st>>>(c); break;
   }
   return cudaGetLastError();
+}
+
+// K1 stage ring placement for this launch: offset (bytes), or -1 when the consumer state
+// and the ring together would not fit the dynamic shared memory available without opt-in.
+int64_t gread_tma_offset(const gfs_consumer& k, int cta_threads) {
+  const int64_t off = tma_ring_offset(k, cta_threads);
+  return off + TMA_NST * TMA_CH <= CONS_SMEM_MAX ? off : -1;
 }
 
 cudaError_t occupancy_gread(int cta_threads, int* blocks_per_sm) {

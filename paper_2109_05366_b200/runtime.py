@@ -58,6 +58,9 @@ def native_config(cfg: ExperimentConfig, max_request_bytes: int = 0) -> native.G
     c.log = int(bool(cfg["mode.deterministic"]))
     c.verify = int(bool(cfg["mode.verify"]))
     c.timeline = int(bool(cfg["mode.timeline"]))
+    if cfg["gpu.k1_copy"] not in ("tma", "ldg"):
+        raise GfsError(f"gpu.k1_copy must be tma or ldg, not {cfg['gpu.k1_copy']!r}")
+    c.k1_tma = int(cfg["gpu.k1_copy"] == "tma")
     return c
 
 

@@ -47,6 +47,7 @@ def random_case(k: int) -> dict:
         "gpu.sm_count": 1, "gpu.max_threads_per_sm": 2048, "gpu.threads_per_tb": 2048,
         "io.transfer": TRANSFERS[k % len(TRANSFERS)], "seed": 7 + k,
         "io.ra_init_bytes": page * r.below(6),
+        "gpu.k1_copy": ("tma", "ldg")[k % 2],
     }
 
 

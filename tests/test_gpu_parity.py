@@ -42,10 +42,12 @@ def oracle_checksum(cfg, seed):
 
 
 @pytest.mark.parametrize("name", gu.case_names())
-@pytest.mark.parametrize("transfer", ["zerocopy", "bounce", "dma", "mapped", "mapped_dma"])
+@pytest.mark.parametrize("transfer", ["zerocopy", "bounce", "dma", "mapped", "mapped_dma", "mapped_dma+ldg"])
 def test_golden_case_on_device(name, transfer, synth_dir):
     g = gu.load(name)
-    sim, rep = run_sim(g["overrides"], g["seed"], synth_dir, **{"io.transfer": transfer})
+    transfer, _, k1 = transfer.partition("+")  # K1 copies by TMA (default) or vector loads
+    sim, rep = run_sim(g["overrides"], g["seed"], synth_dir,
+                       **{"io.transfer": transfer, "gpu.k1_copy": k1 or "tma"})
     st = sim.result.stats
     errs = gu.compare(g, st, sim.result.deliveries, sim.result.rpcs, sim.result.victims)
     assert not errs, f"{name}/{transfer}: " + "; ".join(errs)
