@@ -1434,7 +1434,7 @@ __device__ __forceinline__ float decode_f32(uint32_t u) { return (float)(u >> 8)
 constexpr int GEMV_ROWS = 1024;          // rows of one request accumulated in shared memory
 constexpr int GEMVT_SMEM_COLS = 8192;    // A^T x2 accumulated per CTA in shared memory up to this
 
-constexpr int64_t CONS_SMEM_MAX = 48 * 1024;  // dynamic shared memory without the opt-in
+constexpr int64_t CONS_SMEM_MAX = 48 * 1024;  // dynamic shared memory cap: 4 CTAs/SM still fit
 
 // Kmeans keeps one private [k, cols] accumulator (and counts) per warp when it fits: lanes
 // then update distinct words with plain shared stores, no atomics.  Needs cols >= 32.
@@ -1882,6 +1882,15 @@ __global__ void verify_dst_kernel(const uint8_t* buf, const int64_t* segs, const
 
 cudaError_t launch_gread(const DevCtx& c, int cta_threads, cudaStream_t st) {
   const size_t smem = (size_t)gread_smem_bytes(c.cons, cta_threads, c.tma);
+  if (smem > 0) {  // beyond the default dynamic limit (48 KiB minus the static Smem) needs opt-in
+    cudaError_t e = cudaSuccess;
+    switch (cta_threads) {
+      case 128: e = cudaFuncSetAttribute(gread_driver<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); break;
+      case 512: e = cudaFuncSetAttribute(gread_driver<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); break;
+      default: e = cudaFuncSetAttribute(gread_driver<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); break;
+    }
+    if (e != cudaSuccess) return e;
+  }
   switch (cta_threads) {
     case 128: gread_driver<128><<<c.n_ctas, 128, smem, st>>>(c); break;
     case 512: gread_driver<512><<<c.n_ctas, 512, smem, st>>>(c); break;

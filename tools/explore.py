@@ -40,6 +40,9 @@ def main():
             path = bench.ensure_file(cfg, dist)
         try:
             t0 = time.time()
+            if dst is not None and dst.numel() < cfg["workload.total_bytes"]:
+                dst = None  # a larger workload than the last variant: fresh user buffer
+                torch.cuda.empty_cache()
             r = bench.run_arm(cfg, path, 0, 0, a.steps, 1, dst=dst)
             dst = r["dst"]
             st = r["stats"][-1]
