@@ -156,7 +156,7 @@ struct Smem {
   long long st[GFS_NSTATS];
   // batched page walk (gread_batch): one entry per page of the batch
   struct {
-    int n_empty, k, status, nvict, nret, ret_lane0, own_lane0;
+    int n_empty, k, status, nvict, nret, ret_lane0, own_lane0, j0;
     int64_t rpc_n;
     unsigned long long ret_pos;
     int64_t own_head0, own_tail0;
@@ -479,6 +479,44 @@ __device__ int64_t pb_take(Smem& s, int64_t fid, int64_t page) {
   }
   ST(pb_misses)++;
   return 0;
+}
+
+// Consecutive private-buffer entries present from `page` on (at most maxn), by bitmap
+// words: the run pb_has() would walk page by page.
+__device__ int pb_run(const Smem& s, int64_t fid, int64_t page, int maxn) {
+  if (s.pb_count <= 0 || fid != s.pb_fid) return 0;
+  const int64_t i = page - s.pb_base;
+  if (i < 1 || i > s.pb_count) return 0;
+  const int64_t lim = min((int64_t)maxn, s.pb_count - i + 1);
+  int64_t n = 0;
+  while (n < lim) {
+    const int64_t k = i + n;
+    const uint32_t w = s.pb_absent[k >> 5] >> (k & 31);  // bit set = absent
+    if (w) {
+      n += __ffs(w) - 1;
+      break;
+    }
+    n += 32 - (k & 31);
+  }
+  return (int)min(n, lim);
+}
+
+// pb_take (prefetcher.py:52-61) of n consecutive present entries from `page`, at once:
+// the same counters as n single takes.  Returns their bytes.
+__device__ int64_t pb_take_run(Smem& s, int64_t page, int n) {
+  const int64_t i = page - s.pb_base;
+  for (int64_t k = i; k < i + n;) {
+    const int b = (int)(k & 31);
+    const int m = (int)min((int64_t)(32 - b), i + n - k);
+    s.pb_absent[k >> 5] |= (m == 32 ? 0xFFFFFFFFu : ((1u << m) - 1u)) << b;
+    k += m;
+  }
+  int64_t bytes = (int64_t)n * s.page_size_cached;
+  if (i + n - 1 == s.pb_count) bytes += s.pb_last_nb - s.page_size_cached;
+  s.pb_filled -= bytes;
+  ST(pb_hits) += n;
+  ST(pb_consumed_bytes) += bytes;
+  return bytes;
 }
 
 // request_span (prefetcher.py:13-25) + the adaptive window (io.readahead=adaptive)
@@ -926,7 +964,7 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
   if (tid == 0) {
     int kp = 1;
     if (pb_has(s, fid, p0)) {
-      while (kp < kc && pb_has(s, fid, p0 + kp)) kp++;
+      kp = max(1, pb_run(s, fid, p0, kc));
     } else {
       int64_t win;
       const int64_t span = span_peek(c, s, fid, p0, seg_end, &win);
@@ -998,54 +1036,66 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
   if (has_error(c)) return -1;
 
   // (D) thread 0: lookups/misses, the private-buffer walk and the RPC (prefetcher.py)
+  // Page 0 of the batch is a private-buffer hit or the RPC's own page; every later page
+  // is a private-buffer hit (planned in (B)), taken as one run.
   if (tid == 0) {
-    int status = 0;
-    for (int j = 0; j < kk; j++) {
-      ST(pc_lookups)++;
-      ST(pc_misses)++;
-      const int64_t page = p0 + j;
-      int64_t nb = pb_take(s, fid, page);
-      if (nb > 0) {
-        s.b.nb[j] = (int32_t)nb;
-        s.b.src_off[j] = (page - s.pb_base) * pg;
-        continue;
-      }
-      if (j > 0) {  // planned as a private-buffer page but absent: file shrank under us
-        set_error(c, ERR_IO, (int)fid, (unsigned long long)page);
-        status = 2;
-        break;
-      }
+    int status = 0, j0 = 0;
+    ST(pc_lookups) += kk;
+    ST(pc_misses) += kk;
+    if (!pb_has(s, fid, p0)) {
+      const int64_t page = p0;
+      ST(pb_misses)++;
+      j0 = 1;
       const int64_t span = rpc_span(c, s, fid, page, seg_end);
       const int64_t n = span > 0 ? rpc_call(c, s, fid, page * pg, span) : 0;
       if (n < 0) {
         status = 2;
-        break;
+      } else {
+        log_rec(c, GFS_LOG_RPCS, s.tb, fid, page * pg, span);
+        ST(rpc_count)++;
+        ST(rpc_requested_bytes) += span;
+        account_transfer(c, s, n);
+        if (n == 0) {
+          set_error(c, ERR_IO, (int)fid, (unsigned long long)page);
+          status = 2;
+        }
       }
-      log_rec(c, GFS_LOG_RPCS, s.tb, fid, page * pg, span);
-      ST(rpc_count)++;
-      ST(rpc_requested_bytes) += span;
-      account_transfer(c, s, n);
-      if (n == 0) {
-        set_error(c, ERR_IO, (int)fid, (unsigned long long)page);
+      if (status == 0) {
+        const int64_t nb0 = n < pg ? n : pg;
+        s.b.nb[0] = (int32_t)nb0;
+        s.b.src_off[0] = 0;
+        const int64_t m = (n + pg - 1) / pg;
+        if (m > 1) pb_fill(c, s, fid, page, m, n - nb0);
+      }
+    }
+    if (status == 0 && j0 < kk) {
+      if (pb_run(s, fid, p0 + j0, kk - j0) < kk - j0) {  // planned but absent: file shrank
+        set_error(c, ERR_IO, (int)fid, (unsigned long long)(p0 + j0));
         status = 2;
-        break;
+      } else {
+        pb_take_run(s, p0 + j0, kk - j0);
       }
-      const int64_t nb0 = n < pg ? n : pg;
-      s.b.nb[0] = (int32_t)nb0;
-      s.b.src_off[0] = 0;
-      const int64_t m = (n + pg - 1) / pg;
-      if (m > 1) pb_fill(c, s, fid, page, m, n - nb0);
     }
     s.b.status = status;
-    // bind frames to their pages (installed below)
-    if (status == 0)
-      for (int j = 0; j < kk; j++) c.fkey[s.b.frame[j]] = page_key(fid, p0 + j);
-    const uint64_t t1 = globaltimer();
-    ST(meta_ns) += (long long)(t1 - t_start);
-    s.t_copy0 = t1;
+    s.b.j0 = j0;
   }
   __syncthreads();
   if (s.b.status != 0) return -1;
+  if (w0) {  // private-buffer pages' bytes and span offsets; bind frames to their pages
+    if (lane >= s.b.j0 && lane < kk) {
+      const int64_t i = p0 + lane - s.pb_base;
+      s.b.nb[lane] = (int32_t)(i == s.pb_count ? s.pb_last_nb : pg);
+      s.b.src_off[lane] = i * pg;
+    }
+    if (lane < kk) c.fkey[s.b.frame[lane]] = page_key(fid, p0 + lane);
+    __syncwarp();
+    if (lane == 0) {
+      const uint64_t t1 = globaltimer();
+      ST(meta_ns) += (long long)(t1 - t_start);
+      s.t_copy0 = t1;
+    }
+  }
+  __syncthreads();
   pull_span<BS>(c, s);
 
   // (E) all threads: K1 over the whole batch — span buffer -> frames (+ user buffer)
