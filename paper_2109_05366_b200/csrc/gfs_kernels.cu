@@ -157,6 +157,8 @@ struct Smem {
   // batched page walk (gread_batch): one entry per page of the batch
   struct {
     int n_empty, k, status, nvict, nret, ret_lane0, own_lane0, j0;
+    unsigned tail_mask, part_mask;  // pages with a sub-16 B EOF tail / a partial delivery
+    int64_t total;                  // bytes this batch delivers
     int64_t rpc_n;
     unsigned long long ret_pos;
     int64_t own_head0, own_tail0;
@@ -1089,7 +1091,25 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
     }
     if (lane < kk) c.fkey[s.b.frame[lane]] = page_key(fid, p0 + lane);
     __syncwarp();
+    // which pages need the byte-wise tail copy or a partial delivery, and the batch's bytes
+    const int64_t in0b = g_pos - p0 * pg;
+    const bool dok = d0 != nullptr && ((((uintptr_t)d0 - (uintptr_t)in0b)) & 15) == 0;
+    long long want = 0;
+    bool tail = false, part = false;
+    if (lane < kk) {
+      const int64_t ps = (p0 + lane) * pg, nbj = s.b.nb[lane];
+      const int64_t lo = ps > g_pos ? ps : g_pos;
+      const int64_t hi = ps + nbj < g_end ? ps + nbj : g_end;
+      want = hi - lo;
+      tail = (nbj & 15) != 0;
+      part = d0 != nullptr && !(dok && ps >= g_pos && ps + nbj <= g_end && !tail);
+    }
+    const unsigned tm = __ballot_sync(0xffffffffu, tail), pm = __ballot_sync(0xffffffffu, part);
+    for (int o = 16; o > 0; o >>= 1) want += __shfl_xor_sync(0xffffffffu, want, o);
     if (lane == 0) {
+      s.b.tail_mask = tm;
+      s.b.part_mask = pm;
+      s.b.total = want;
       const uint64_t t1 = globaltimer();
       ST(meta_ns) += (long long)(t1 - t_start);
       s.t_copy0 = t1;
@@ -1212,9 +1232,9 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
     }
   }
   }  // LDG path
-  for (int j = 0; j < kk; j++) {  // EOF page tails that are not a multiple of 16 bytes
+  for (unsigned m = s.b.tail_mask; m; m &= m - 1) {  // EOF page tails not a multiple of 16 B
+    const int j = __ffs(m) - 1;
     const int64_t nbj = s.b.nb[j];
-    if ((nbj & 15) == 0) continue;
     const uint8_t* sp = span_buf + s.b.src_off[j];
     uint8_t* fp = c.frames + (int64_t)s.b.frame[j] * pg;
     for (int64_t i = (nbj & ~(int64_t)15) + tid; i < nbj; i += BS) {
@@ -1230,17 +1250,15 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
   const int any_bad = __syncthreads_or(bad);
   // partial deliveries (first page entered mid-page, last page cut by the request, EOF
   // tails, misaligned user buffers) from the frames just written
-  int64_t total = 0;
-  for (int j = 0; j < kk; j++) {
+  const int64_t total = s.b.total;
+  for (unsigned m = s.b.part_mask; m; m &= m - 1) {
+    const int j = __ffs(m) - 1;
     const int64_t ps = (p0 + j) * pg, nbj = s.b.nb[j];
     const int64_t lo = ps > g_pos ? ps : g_pos;
     const int64_t hi = ps + nbj < g_end ? ps + nbj : g_end;
-    const int64_t want = hi - lo;
-    total += want;
-    const bool whole = dst_ok && ps >= g_pos && ps + nbj <= g_end && (nbj & 15) == 0;
-    if (d0 && !whole) copy_bytes<BS, SRC_HBM>(d0 + (lo - g_pos), c.frames + (int64_t)s.b.frame[j] * pg + (lo - ps), want);
+    copy_bytes<BS, SRC_HBM>(d0 + (lo - g_pos), c.frames + (int64_t)s.b.frame[j] * pg + (lo - ps), hi - lo);
   }
-  __syncthreads();
+  if (s.b.part_mask) __syncthreads();
 
   // (F) warp 0: install (data, then VALID, then the page-table entry) and deliveries
   if (w0) {
@@ -1249,10 +1267,10 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
       ST(copy_ns) += (long long)(t_in - s.t_copy0);
       s.t_copy0 = t_in;
     }
-    __threadfence();
+    __threadfence();  // frame data before VALID and the PTE (this fence makes the store a release)
     if (lane < kk) {
       atomicOr(&c.fstate[s.b.frame[lane]], FR_VALID);
-      st_release_gpu(&pt[p0 + lane], s.b.frame[lane]);
+      *(volatile uint32_t*)&pt[p0 + lane] = s.b.frame[lane];
     }
     unsigned long long base = 0;
     if (lane == 0) base = log_reserve(c, GFS_LOG_DELIVERIES, kk);
@@ -1597,30 +1615,27 @@ __device__ void kmeans_part(const gfs_consumer& k, float* smem, const uint8_t* d
     const uint4* pv = (const uint4*)(data + (valid ? p : 0) * (int64_t)D * 4);
     int best = 0;
     if (valid) {
-      // centroids in groups of 4 (4 running sums in registers; the point's vectors are
-      // re-read from L1 per group): no local-memory spills under the 64-register cap
-      float bd = 0.f;
-      for (int c0 = 0; c0 < K; c0 += 4) {
-        float d[4] = {0.f, 0.f, 0.f, 0.f};
-        for (int j = 0; j < D; j += 4) {
-          const uint4 u = __ldcg(pv + (j >> 2));
-          const float v[4] = {decode_f32(u.x), decode_f32(u.y), decode_f32(u.z), decode_f32(u.w)};
+      float d[GFS_KMEANS_MAX_K];
 #pragma unroll
-          for (int cc = 0; cc < 4; cc++) {
-            if (c0 + cc < K) {
-              const float* ce = cent + (c0 + cc) * D + j;
+      for (int c = 0; c < GFS_KMEANS_MAX_K; c++) d[c] = 0.f;
+      for (int j = 0; j < D; j += 4) {
+        const uint4 u = __ldcg(pv + (j >> 2));
+        const float v[4] = {decode_f32(u.x), decode_f32(u.y), decode_f32(u.z), decode_f32(u.w)};
 #pragma unroll
-              for (int q = 0; q < 4; q++) {
-                const float df = __fsub_rn(v[q], ce[q]);
-                d[cc] = __fadd_rn(d[cc], __fmul_rn(df, df));
-              }
+        for (int c = 0; c < GFS_KMEANS_MAX_K; c++) {
+          if (c < K) {
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+              const float df = __fsub_rn(v[q], cent[c * D + j + q]);
+              d[c] = __fadd_rn(d[c], __fmul_rn(df, df));
             }
           }
         }
-#pragma unroll
-        for (int cc = 0; cc < 4; cc++)
-          if (c0 + cc < K && (c0 + cc == 0 || d[cc] < bd)) { bd = d[cc]; best = c0 + cc; }
       }
+      float bd = d[0];
+#pragma unroll
+      for (int c = 1; c < GFS_KMEANS_MAX_K; c++)
+        if (c < K && d[c] < bd) { bd = d[c]; best = c; }
     }
     const uint32_t* pw = (const uint32_t*)pv;
     float* row = acc + best * D;
