@@ -121,28 +121,37 @@ static int map_range(HostFile& f, int64_t lo, int64_t hi) {
   if (f.map && f.map_lo <= lo && f.map_lo + f.map_len >= hi) return GFS_OK;
   unmap_file(f);
   const size_t len = (size_t)(hi - lo);
-  void* m = mmap(nullptr, len, PROT_READ, MAP_SHARED | MAP_POPULATE, f.fd_buffered, (off_t)lo);
-  cudaError_t e = m == MAP_FAILED
-                      ? cudaErrorInvalidValue
-                      : cudaHostRegister(m, len, cudaHostRegisterReadOnly | cudaHostRegisterPortable |
-                                                     cudaHostRegisterMapped);
-  if (m != MAP_FAILED && e != cudaSuccess) {
-    // platforms without read-only registration: pin a shared read-write mapping of the
-    // same pages (never written through; needs write permission on the file)
-    cudaGetLastError();
-    munmap(m, len);
-    int rw = open(f.path.c_str(), O_RDWR);
-    m = rw < 0 ? MAP_FAILED
-               : mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_SHARED | MAP_POPULATE, rw, (off_t)lo);
-    if (rw >= 0) close(rw);
+  void* m = MAP_FAILED;
+  cudaError_t e = cudaErrorInvalidValue;
+  // Pinning page-cache pages can fail transiently (the kernel migrating pages while memory
+  // is tight); retry a few times before reporting.
+  for (int attempt = 0; attempt < 4 && e != cudaSuccess; attempt++) {
+    if (attempt) std::this_thread::sleep_for(std::chrono::milliseconds(250 * attempt));
+    m = mmap(nullptr, len, PROT_READ, MAP_SHARED | MAP_POPULATE, f.fd_buffered, (off_t)lo);
     e = m == MAP_FAILED ? cudaErrorInvalidValue
-                        : cudaHostRegister(m, len, cudaHostRegisterPortable | cudaHostRegisterMapped);
+                        : cudaHostRegister(m, len, cudaHostRegisterReadOnly | cudaHostRegisterPortable |
+                                                       cudaHostRegisterMapped);
+    if (m != MAP_FAILED && e != cudaSuccess) {
+      // platforms without read-only registration: pin a shared read-write mapping of the
+      // same pages (never written through; needs write permission on the file)
+      cudaGetLastError();
+      munmap(m, len);
+      int rw = open(f.path.c_str(), O_RDWR);
+      m = rw < 0 ? MAP_FAILED
+                 : mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_SHARED | MAP_POPULATE, rw, (off_t)lo);
+      if (rw >= 0) close(rw);
+      e = m == MAP_FAILED ? cudaErrorInvalidValue
+                          : cudaHostRegister(m, len, cudaHostRegisterPortable | cudaHostRegisterMapped);
+    }
+    if (e != cudaSuccess) {
+      cudaGetLastError();  // do not leave a sticky error for the next launch check
+      if (m != MAP_FAILED) munmap(m, len);
+    }
   }
   if (m == MAP_FAILED || e != cudaSuccess) {
-    cudaGetLastError();  // do not leave a sticky error for the next launch check
-    if (m != MAP_FAILED) munmap(m, len);
-    return fail(GFS_EIO, "mapped transfers need a memory-resident file (tmpfs); %s: %s",
-                f.path.c_str(), m == MAP_FAILED ? strerror(errno) : cudaGetErrorString(e));
+    return fail(GFS_EIO, "mapped transfers need a memory-resident file (tmpfs); pinning %s [%lld, %lld) failed: %s",
+                f.path.c_str(), (long long)lo, (long long)hi,
+                m == MAP_FAILED ? strerror(errno) : cudaGetErrorString(e));
   }
   void* dp = nullptr;
   if (cudaHostGetDevicePointer(&dp, m, 0) != cudaSuccess) {

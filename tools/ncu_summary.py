@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--user-bytes", type=int, required=True)
     ap.add_argument("--tag", default="gread")
     ap.add_argument("--workload", default="")
+    ap.add_argument("--source-top", type=int, default=25)
     a = ap.parse_args()
     raw = subprocess.run(["ncu", "-i", a.rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True, check=True).stdout
@@ -57,6 +58,30 @@ def main():
         "metrics": out,
     }
     os.makedirs(a.outdir, exist_ok=True)
+    with open(os.path.join(a.outdir, f"ncu_{a.tag}_summary.json"), "w") as fh:
+        json.dump(summary, fh, indent=1)
+    # stall stack by reason and the hottest source lines (warp-state samples)
+    summary["stall_samples"] = {k.replace("smsp__pcsamp_warps_issue_stalled_", ""): int(num(v))
+                                for k, v in zip(hdr, vals)
+                                if k.startswith("smsp__pcsamp_warps_issue_stalled_")
+                                and not k.endswith("_not_issued") and num(v) not in ("", 0, 0.0)}
+    src = subprocess.run(["ncu", "-i", a.rep, "--page", "source", "--csv", "--print-source=cuda,sass"],
+                         capture_output=True, text=True).stdout
+    srows = list(csv.reader(io.StringIO(src)))
+    hot = []
+    if len(srows) > 3 and "Warp Stall Sampling (All Samples)" in srows[2]:
+        iS = srows[2].index("Warp Stall Sampling (All Samples)")
+        for r in srows[3:]:
+            if len(r) > iS and r[0] not in ("", "-") and r[2] == "-":
+                try:
+                    hot.append((int(r[iS]), int(r[0]), r[1].strip()[:100]))
+                except ValueError:
+                    pass
+        tot = sum(h[0] for h in hot) or 1
+        hot.sort(reverse=True)
+        summary["hot_source_lines"] = [{"line": f"gfs_kernels.cu:{ln}", "samples": n,
+                                        "share": round(n / tot, 4), "source": sl}
+                                       for n, ln, sl in hot[:a.source_top]]
     with open(os.path.join(a.outdir, f"ncu_{a.tag}_summary.json"), "w") as fh:
         json.dump(summary, fh, indent=1)
     det = subprocess.run(["ncu", "-i", a.rep, "--page", "details", "--csv"], capture_output=True,
