@@ -218,13 +218,12 @@ def fit_size(directory: str, size: int, n: int) -> int:
 
 
 def ensure_file(cfg, dist: Dist) -> str:
-    from paper_2109_05366_b200.runtime import ensure_synthetic
+    from paper_2109_05366_b200.runtime import ensure_synthetic, ensure_synthetic_shard
     d, size = cfg["io.dir"], cfg["workload.file_bytes"]
-    path = None
-    if dist.rank == 0:
-        path = ensure_synthetic(d, 0, size)
-    dist.barrier()
-    return path or ensure_synthetic(d, 0, size)
+    if dist.world > 1:  # each rank writes its own shard from its GPU's local CPUs
+        return ensure_synthetic_shard(d, 0, size, dist.rank, dist.world, dist.barrier,
+                                      device=dist.local)
+    return ensure_synthetic(d, 0, size)
 
 
 def run_arm(cfg, path: str, rank: int, device: int, steps: int, warmup: int, dst=None,

@@ -82,7 +82,7 @@ typedef struct gfs_config {
   int32_t timeline;        /* record the GFS_LOG_TIMELINE log (mode.timeline) */
   int32_t k1_tma;          /* gpu.k1_copy: 1 = span -> frame/user copies by TMA bulk copies
                               through a shared-memory ring, 0 = 16-byte vector loads/stores */
-  int32_t reserved[1];
+  int32_t numa_pin;        /* io.numa_pin: daemon threads on the CPUs local to the GPU's PCIe root */
 } gfs_config;
 
 /* One gread program set (workloads.py:24-31 programs, flattened).
@@ -188,6 +188,10 @@ int gfs_verify_dst(gfs_ctx* ctx, const gfs_program* prog, const void* dev_buf, u
 
 /* ---- synthetic files (K6): write W(content_id, i) words, multi-threaded ---- */
 int gfs_gen_file(const char* path, int64_t content_id, int64_t size, int threads);
+/* the same words for [offset, offset+length) of a file of `size` bytes (created/extended
+ * as needed): ranks of a sharded run write their own shards from GPU-local CPUs */
+int gfs_gen_file_range(const char* path, int64_t content_id, int64_t size, int64_t offset,
+                       int64_t length, int threads);
 
 /* ---- comparison arms and roofline probes (bench.py; not on the gread path) ---- */
 /* parallel sequential read of [offset, offset+size) of path; wall seconds */

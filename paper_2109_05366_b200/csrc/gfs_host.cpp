@@ -17,7 +17,9 @@
 #include <errno.h>
 #include <fcntl.h>
 #include <immintrin.h>
+#include <ctype.h>
 #include <pthread.h>
+#include <sched.h>
 #include <stdarg.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -225,6 +227,7 @@ struct gfs_ctx {
 
   // daemon
   std::vector<std::thread> workers;
+  std::vector<int> local_cpus;  // daemon threads pinned here (empty = no pinning)
   std::vector<cudaStream_t> worker_streams;  // copy streams (shared by the workers)
   std::vector<cudaStream_t> bell_streams;    // doorbell streams
   std::vector<cudaEvent_t> bell_ev;          // per worker: "this copy is done"
@@ -284,7 +287,50 @@ static int64_t do_pread(gfs_ctx* ctx, const HostFile& f, int64_t off, int64_t si
   return std::min(got, n);
 }
 
+// Host CPUs attached to the GPU's PCIe root (sysfs local_cpulist), limited to the CPUs this
+// process may use; empty when unknown or when that is every usable CPU anyway.
+static std::vector<int> gpu_local_cpus(int device) {
+  char bus[64] = {0};
+  if (cudaDeviceGetPCIBusId(bus, sizeof bus, device) != cudaSuccess) {
+    cudaGetLastError();
+    return {};
+  }
+  std::string id(bus);
+  for (auto& ch : id) ch = (char)tolower(ch);
+  const size_t colon = id.find(':');
+  if (colon != std::string::npos && colon > 4) id = id.substr(colon - 4);  // 8-digit domain
+  FILE* fp = fopen(("/sys/bus/pci/devices/" + id + "/local_cpulist").c_str(), "r");
+  if (!fp) return {};
+  char line[4096] = {0};
+  const bool ok = fgets(line, sizeof line, fp) != nullptr;
+  fclose(fp);
+  if (!ok) return {};
+  cpu_set_t allowed;
+  CPU_ZERO(&allowed);
+  if (sched_getaffinity(0, sizeof allowed, &allowed) != 0) return {};
+  std::vector<int> out;
+  for (char* tok = strtok(line, ",\n"); tok; tok = strtok(nullptr, ",\n")) {
+    int a = -1, b = -1;
+    if (sscanf(tok, "%d-%d", &a, &b) == 2) {
+    } else if (sscanf(tok, "%d", &a) == 1) {
+      b = a;
+    } else {
+      continue;
+    }
+    for (int c = a; c <= b && c < CPU_SETSIZE; c++)
+      if (c >= 0 && CPU_ISSET(c, &allowed)) out.push_back(c);
+  }
+  if ((int)out.size() >= CPU_COUNT(&allowed)) return {};  // no narrower than what we have
+  return out;
+}
+
 static void worker_main(gfs_ctx* ctx, int wid) {
+  if (!ctx->local_cpus.empty()) {  // NUMA-local to the GPU's PCIe root (north_star)
+    cpu_set_t set;
+    CPU_ZERO(&set);
+    for (int c : ctx->local_cpus) CPU_SET(c, &set);
+    pthread_setaffinity_np(pthread_self(), sizeof set, &set);
+  }
   const uint32_t mask = ctx->ring_size - 1;
   const bool dma = ctx->cfg.transfer == GFS_XFER_DMA;
   const bool bounce = ctx->cfg.transfer == GFS_XFER_BOUNCE;
@@ -593,6 +639,7 @@ extern "C" int gfs_create(const gfs_config* cfg_in, gfs_ctx** out) {
   }
   TRY(cudaDeviceSynchronize());
 #undef TRY
+  if (cfg.numa_pin) ctx->local_cpus = gpu_local_cpus(cfg.device);
   for (int w = 0; w < cfg.io_workers; w++) ctx->workers.emplace_back(worker_main, ctx, w);
   *out = ctx;
   return GFS_OK;
@@ -1060,13 +1107,25 @@ extern "C" int gfs_gen_file(const char* path, int64_t content_id, int64_t size, 
   if (!path || size < 0 || content_id < 0) return fail(GFS_EINVAL, "gfs_gen_file: bad argument");
   int fd = open(path, O_CREAT | O_WRONLY | O_TRUNC, 0644);
   if (fd < 0) return fail(GFS_EIO, "create %s: %s", path, strerror(errno));
-  if (ftruncate(fd, (off_t)size) != 0) {
+  close(fd);
+  return gfs_gen_file_range(path, content_id, size, 0, size, threads);
+}
+
+extern "C" int gfs_gen_file_range(const char* path, int64_t content_id, int64_t size, int64_t offset,
+                                  int64_t length, int threads) {
+  if (!path || size < 0 || content_id < 0 || offset < 0 || length < 0 || offset + length > size ||
+      offset % 8)
+    return fail(GFS_EINVAL, "gfs_gen_file_range: bad argument");
+  int fd = open(path, O_CREAT | O_WRONLY, 0644);
+  if (fd < 0) return fail(GFS_EIO, "create %s: %s", path, strerror(errno));
+  struct stat sb;
+  if (fstat(fd, &sb) != 0 || (sb.st_size != size && ftruncate(fd, (off_t)size) != 0)) {
     close(fd);
     return fail(GFS_EIO, "truncate %s: %s", path, strerror(errno));
   }
   if (threads < 1) threads = 1;
   const int64_t chunk = 8 << 20;
-  const int64_t nchunks = (size + chunk - 1) / chunk;
+  const int64_t nchunks = (length + chunk - 1) / chunk;
   std::atomic<int64_t> next{0};
   std::atomic<int> err{0};
   auto body = [&]() {
@@ -1074,7 +1133,7 @@ extern "C" int gfs_gen_file(const char* path, int64_t content_id, int64_t size, 
     for (;;) {
       int64_t k = next.fetch_add(1);
       if (k >= nchunks || err.load()) return;
-      const int64_t off = k * chunk, n = std::min(chunk, size - off);
+      const int64_t off = offset + k * chunk, n = std::min(chunk, offset + length - off);
       const int64_t w0 = off >> 3, nw = (n + 7) >> 3;
       for (int64_t i = 0; i < nw; i++) {
         int64_t wi = w0 + i;

@@ -30,7 +30,7 @@ EXPORTS = ["gfs_create", "gfs_destroy", "gfs_gopen", "gfs_gclose", "gfs_file_siz
            "gfs_log_len", "gfs_log_copy", "gfs_checksum", "gfs_verify_dst", "gfs_gen_file",
            "gfs_last_error", "gfs_abi_version", "gfs_stat_count", "gfs_stat_name",
            "gfs_resident_ctas", "gfs_bench_storage", "gfs_bench_h2d", "gfs_bench_read_memcpy",
-           "gfs_replay"]
+           "gfs_replay", "gfs_gen_file_range"]
 
 
 class GfsConfig(C.Structure):
@@ -43,7 +43,7 @@ class GfsConfig(C.Structure):
         ("device", C.c_int32), ("cta_threads", C.c_int32), ("max_ctas", C.c_int32),
         ("raw_mode", C.c_int32), ("pcie_disabled", C.c_int32), ("log", C.c_int32),
         ("verify", C.c_int32), ("timeline", C.c_int32), ("k1_tma", C.c_int32),
-        ("reserved", C.c_int32 * 1),
+        ("numa_pin", C.c_int32),
     ]
 
 
@@ -96,6 +96,7 @@ def load(path: str = LIB_PATH):
     L.gfs_checksum.argtypes = [vp, vp, u64, u64, C.POINTER(u64)]
     L.gfs_verify_dst.argtypes = [vp, C.POINTER(GfsProgram), vp, u64, C.POINTER(i64)]
     L.gfs_gen_file.argtypes = [C.c_char_p, i64, i64, i32]
+    L.gfs_gen_file_range.argtypes = [C.c_char_p, i64, i64, i64, i64, i32]
     L.gfs_last_error.restype = C.c_char_p
     L.gfs_stat_name.restype = C.c_char_p
     L.gfs_stat_name.argtypes = [i32]
@@ -108,7 +109,8 @@ def load(path: str = LIB_PATH):
                              C.POINTER(i64), C.POINTER(i64), dp]
     for name in ("gfs_create", "gfs_gopen", "gfs_gclose", "gfs_file_size", "gfs_run",
                  "gfs_log_len", "gfs_log_copy", "gfs_checksum", "gfs_verify_dst", "gfs_gen_file",
-                 "gfs_bench_storage", "gfs_bench_h2d", "gfs_bench_read_memcpy", "gfs_replay"):
+                 "gfs_bench_storage", "gfs_bench_h2d", "gfs_bench_read_memcpy", "gfs_replay",
+                 "gfs_gen_file_range"):
         getattr(L, name).restype = i32
     _lib = L
     return L
@@ -132,6 +134,13 @@ def gen_file(path: str, content_id: int, size: int, threads: int | None = None) 
     L = load()
     check(L.gfs_gen_file(os.fsencode(path), content_id, size, threads or os.cpu_count() or 4),
           f"gfs_gen_file({path})")
+
+
+def gen_file_range(path: str, content_id: int, size: int, offset: int, length: int,
+                   threads: int | None = None) -> None:
+    L = load()
+    check(L.gfs_gen_file_range(os.fsencode(path), content_id, size, offset, length,
+                               threads or os.cpu_count() or 4), f"gfs_gen_file_range({path})")
 
 
 def bench_storage(path: str, offset: int, size: int, threads: int, chunk: int, direct: bool) -> float:

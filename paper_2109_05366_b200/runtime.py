@@ -61,6 +61,7 @@ def native_config(cfg: ExperimentConfig, max_request_bytes: int = 0) -> native.G
     if cfg["gpu.k1_copy"] not in ("tma", "ldg"):
         raise GfsError(f"gpu.k1_copy must be tma or ldg, not {cfg['gpu.k1_copy']!r}")
     c.k1_tma = int(cfg["gpu.k1_copy"] == "tma")
+    c.numa_pin = int(bool(cfg["io.numa_pin"]))
     return c
 
 
@@ -285,6 +286,75 @@ def ensure_synthetic(directory: str, content_id: int, size: int) -> str:
     native.gen_file(path, content_id, size)
     with open(stamp, "w") as fh:
         fh.write(SYNTH_VERSION)
+    return path
+
+
+def synthetic_path(directory: str, content_id: int, size: int) -> str:
+    return os.path.join(directory, f"gfs_synth_c{content_id}_{size}.bin")
+
+
+def synthetic_ready(path: str, size: int) -> bool:
+    stamp = path + ".ok"
+    if not (os.path.exists(path) and os.path.exists(stamp) and os.path.getsize(path) == size):
+        return False
+    with open(stamp) as fh:
+        return fh.read().strip() == SYNTH_VERSION
+
+
+def gpu_local_cpus(device: int) -> list[int]:
+    """Host CPUs on the GPU's PCIe root (sysfs local_cpulist) that this process may use;
+    all usable CPUs when that is unknown."""
+    allowed = sorted(os.sched_getaffinity(0))
+    try:
+        import torch
+        p = torch.cuda.get_device_properties(device)
+        bus = f"{p.pci_domain_id:04x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+        with open(f"/sys/bus/pci/devices/{bus}/local_cpulist") as fh:
+            text = fh.read().strip()
+    except Exception:
+        return allowed
+    cpus = set()
+    for part in text.split(","):
+        a, _, b = part.partition("-")
+        if a.strip():
+            cpus.update(range(int(a), int(b or a) + 1))
+    local = [c for c in allowed if c in cpus]
+    return local or allowed
+
+
+def ensure_synthetic_shard(directory: str, content_id: int, size: int, rank: int, world: int,
+                           barrier, device: int | None = None) -> str:
+    """Sharded runs: every rank writes its own contiguous 1/world of the file from the CPUs
+    local to its GPU, so tmpfs places each shard's pages on the NUMA node that DMAs them
+    (first touch).  `barrier` synchronises the ranks."""
+    os.makedirs(directory, exist_ok=True)
+    path = synthetic_path(directory, content_id, size)
+    ready = synthetic_ready(path, size)
+    barrier()
+    if ready:
+        return path
+    if rank == 0:
+        for p in (path + ".ok", path):
+            if os.path.exists(p):
+                os.remove(p)
+        with open(path, "wb") as fh:
+            fh.truncate(size)
+    barrier()
+    shard = size // world // 8 * 8
+    lo = rank * shard
+    hi = size if rank == world - 1 else lo + shard
+    old = os.sched_getaffinity(0)
+    cpus = gpu_local_cpus(device) if device is not None else sorted(old)
+    try:
+        os.sched_setaffinity(0, cpus)
+        native.gen_file_range(path, content_id, size, lo, hi - lo, threads=len(cpus))
+    finally:
+        os.sched_setaffinity(0, old)
+    barrier()
+    if rank == 0:
+        with open(path + ".ok", "w") as fh:
+            fh.write(SYNTH_VERSION)
+    barrier()
     return path
 
 

@@ -92,3 +92,33 @@ def test_sharded_ranks_tile_the_file_and_reduce_checksums():
     cfg = _cfg()
     base = orc.run_oracle(cfg, _shard(cfg, 0))
     assert np.array_equal(base.rpcs, r0)
+
+
+def _shard_worker(rank, world, d, size, port):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2109_05366_b200.runtime import ensure_synthetic_shard
+    path = ensure_synthetic_shard(d, 7, size, rank, world, dist.barrier)
+    dist.barrier()
+    dist.destroy_process_group()
+    return path
+
+
+def test_sharded_generation_equals_whole_file(tmp_path):
+    """Ranks writing their own shards (gfs_gen_file_range) produce the same bytes as one
+    writer (W-law content), and the ready stamp appears only once all shards are done."""
+    import torch.multiprocessing as tmp
+    from paper_2109_05366_b200 import native
+    from paper_2109_05366_b200 import rng as grng
+    from paper_2109_05366_b200.runtime import synthetic_path, synthetic_ready
+    size = (3 << 20) + 4104  # not a multiple of the shard count: last rank takes the rest
+    d = str(tmp_path)
+    tmp.spawn(_shard_worker, args=(2, d, size, 29631), nprocs=2, join=True)
+    path = synthetic_path(d, 7, size)
+    assert synthetic_ready(path, size)
+    got = open(path, "rb").read()
+    assert got == grng.content(7, 0, size)
+    whole = str(tmp_path / "whole.bin")
+    native.gen_file(whole, 7, size)
+    assert open(whole, "rb").read() == got
