@@ -596,6 +596,7 @@ def consumer_arm(cfg, path: str, device: int, dst) -> dict:
     from paper_2109_05366_b200.workloads import ProgramTable, gen_sequential_strided
     n_tb, unit = 128, 128 * 4096
     total = 950_000_000 // unit * unit
+    cfg = cfg.copy_with({"workload.n_tb": n_tb, "workload.total_bytes": total})
     wl = gen_sequential_strided([cfg["workload.file_bytes"]], n_tb, total, 64 * KiB, 4096)
     table = ProgramTable.from_programs(wl.programs)
     cols = 4096

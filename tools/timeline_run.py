@@ -57,9 +57,12 @@ def main():
         res["headline_pass"] = s
         timeline.chrome_trace(rr.timeline, os.path.join(a.out, "timeline_headline.json"), 100_000)
         gz(os.path.join(a.out, "timeline_headline.json"))
-        # (2) gesummv shape with the fused GEMV consumer (and without, for the I/O-only rate)
-        n_tb, unit = 128, 128 * 4096
-        total = 950_000_000 // unit * unit
+    # (2) gesummv shape with the fused GEMV consumer (and without, for the I/O-only rate)
+    n_tb, unit = 128, 128 * 4096
+    total = 950_000_000 // unit * unit
+    cfg2 = cfg.copy_with({"workload.n_tb": n_tb, "workload.total_bytes": total})
+    with GpuFS(cfg2, max_request_bytes=64 * KiB) as fs:
+        fs.gopen(path, content_id=0)
         wl2 = gen_sequential_strided([cfg["workload.file_bytes"]], n_tb, total, 64 * KiB, 4096)
         t2 = ProgramTable.from_programs(wl2.programs)
         cols = 4096
