@@ -98,3 +98,50 @@ def test_checksum_law_python_vs_oracle():
     L = orc.lib()
     buf = np.frombuffer(grng.content(0, 4096, 65536), dtype=np.uint8).copy()
     assert L.orc_checksum(buf.ctypes.data, len(buf), 3) == grng.checksum(buf, 3)
+
+
+def test_auto_transfer_and_first_window_rules(monkeypatch, tmp_path):
+    """auto: tmpfs + adaptive -> mapped_dma, tmpfs + static -> mapped, disk -> bounce,
+    never a copy-engine mode under a kernel profiler; the first copy-engine window is the
+    whole cap when TBs outnumber resident slots, <= half a stride otherwise."""
+    from paper_2109_05366_b200 import config as gcfg
+    monkeypatch.delenv("GFS_PROFILER", raising=False)
+    for k in [k for k in os.environ if "INJECTION" in k]:
+        monkeypatch.delenv(k, raising=False)
+    KiB, MiB = 1 << 10, 1 << 20
+    base = {"workload.kind": "strided", "workload.n_tb": 1024, "workload.file_bytes": 16 << 30,
+            "gpu.sm_count": 148, "gpu.threads_per_tb": 512, "gpufs.prefetch_bytes": 60 * KiB}
+    monkeypatch.setattr(gcfg, "on_tmpfs", lambda p: True)
+    c = ExperimentConfig({**base, "io.readahead": "adaptive"})
+    assert c.transfer() == "mapped_dma" and c.ra_init() == c.ra_max() == 16 * MiB
+    assert ExperimentConfig({**base, "io.readahead": "static"}).transfer() == "mapped"
+    few = ExperimentConfig({**base, "io.readahead": "adaptive", "workload.n_tb": 128,
+                            "workload.total_bytes": 949485568})
+    assert few.ra_init() == 2 * MiB  # largest power of two <= half of a 7.4 MB stride
+    assert ExperimentConfig({**base, "io.readahead": "adaptive", "io.ra_init_bytes": 64 * KiB}).ra_init() == 64 * KiB
+    monkeypatch.setenv("GFS_PROFILER", "1")
+    assert ExperimentConfig({**base, "io.readahead": "adaptive"}).transfer() == "mapped"
+    monkeypatch.delenv("GFS_PROFILER")
+    monkeypatch.setattr(gcfg, "on_tmpfs", lambda p: False)
+    assert ExperimentConfig({**base, "io.readahead": "adaptive"}).transfer() == "bounce"
+
+
+def test_io_workers_split_across_local_ranks(monkeypatch):
+    cores = len(os.sched_getaffinity(0))
+    monkeypatch.setenv("LOCAL_WORLD_SIZE", "1")
+    one = ExperimentConfig().io_workers()
+    monkeypatch.setenv("LOCAL_WORLD_SIZE", "8")
+    eight = ExperimentConfig().io_workers()
+    assert one == max(4, cores) and eight == max(4, cores // 8)
+    assert ExperimentConfig({"io.workers": 3}).io_workers() == 3
+
+
+def test_gen_file_range_composes_the_whole_file(lib, tmp_path):
+    size = (1 << 20) + 808
+    a, b = str(tmp_path / "a.bin"), str(tmp_path / "b.bin")
+    native.gen_file(a, 4, size)
+    native.gen_file_range(b, 4, size, 520, size - 520, threads=3)  # tail first, then the head
+    native.gen_file_range(b, 4, size, 0, 520, threads=1)
+    assert open(a, "rb").read() == open(b, "rb").read() == grng.content(4, 0, size)
+    with pytest.raises(GfsError):
+        native.gen_file_range(b, 4, size, 3, 8)  # offsets are word aligned
