@@ -168,6 +168,7 @@ struct Smem {
     int32_t vict[32];  // 1 = frame must be evicted before reuse
   } b;
   int64_t pb_last_nb;        // bytes of the last private-buffer entry
+  int fresh_done;            // this CTA saw the never-used frames run out (they never return)
   int64_t page_size_cached;  // c.page_size, for the smem-only pb_take
   uint32_t pb_absent[MAX_PB_ENTRIES / 32];  // private-buffer entries consumed / dropped
 };
@@ -818,8 +819,9 @@ __device__ int plan_per_tb(const DevCtx& c, Smem& s, int k) {
   const int64_t len0 = s.own_len;
   const int a = (int)min((int64_t)k, max((int64_t)0, c.quota - len0));
   int g = 0;
-  if (a > 0 && ld_volatile_u64(&c.g->fresh_next) < (unsigned long long)c.nframes) {
+  if (a > 0 && !s.fresh_done) {
     unsigned long long old = atomicAdd(&c.g->fresh_next, (unsigned long long)a);
+    if (old + a >= (unsigned long long)c.nframes) s.fresh_done = 1;
     if (old < (unsigned long long)c.nframes)
       g = (int)min((unsigned long long)a, (unsigned long long)c.nframes - old);
     for (int j = 0; j < g; j++) s.b.frame[j] = (uint32_t)(old + j);
@@ -862,8 +864,9 @@ __device__ int plan_per_tb(const DevCtx& c, Smem& s, int k) {
 // global lock (gpu_cache.py:126-147).  Victims are unmapped here (vict = 0 afterwards).
 __device__ int plan_global(const DevCtx& c, Smem& s, int k) {
   int g = 0;
-  if (ld_volatile_u64(&c.g->fresh_next) < (unsigned long long)c.nframes) {
+  if (!s.fresh_done) {
     unsigned long long old = atomicAdd(&c.g->fresh_next, (unsigned long long)k);
+    if (old + k >= (unsigned long long)c.nframes) s.fresh_done = 1;
     if (old < (unsigned long long)c.nframes)
       g = (int)min((unsigned long long)k, (unsigned long long)c.nframes - old);
     for (int j = 0; j < g; j++) s.b.frame[j] = (uint32_t)(old + j);
@@ -949,10 +952,8 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
 
   // (A) warp 0: look up and claim the leading run of uncached pages
   if (w0) {
-    bool ok = lane < nmax && ld_acquire_gpu(&pt[p0 + lane]) == PT_EMPTY;
-    unsigned m = __ballot_sync(0xffffffffu, ok);
-    int run = (~m == 0u) ? 32 : __ffs(~m) - 1;
-    ok = lane < run && atomicCAS(&pt[p0 + lane], PT_EMPTY, PT_CLAIMED) == PT_EMPTY;
+    // claim straight away (one round trip): the batch is the leading run of claimed pages
+    bool ok = lane < nmax && atomicCAS(&pt[p0 + lane], PT_EMPTY, PT_CLAIMED) == PT_EMPTY;
     unsigned got = __ballot_sync(0xffffffffu, ok);
     int kc = (~got == 0u) ? 32 : __ffs(~got) - 1;
     if (ok && lane >= kc) st_release_gpu(&pt[p0 + lane], PT_EMPTY);  // beyond a raced page
@@ -1829,6 +1830,7 @@ __global__ void __launch_bounds__(BS, 4) gread_driver(DevCtx c) {
     for (int i = 0; i < GFS_NSTATS; i++) s.st[i] = 0;
     s.pull_n = 0;
     s.tma_seq = 0;
+    s.fresh_done = 0;
     if (c.tma) {
       for (int i = 0; i < TMA_NST; i++) mbar_init(&s.tma_bar[i], 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
