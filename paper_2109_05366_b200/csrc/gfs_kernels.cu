@@ -66,8 +66,12 @@ __device__ __forceinline__ uint64_t ld_acquire_sys64(const unsigned long long* p
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
   asm volatile("st.release.sys.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// device-memory counters shared by CTAs: relaxed loads at GPU scope (no system-scope
+// strong load needed: the host never writes them while the kernel runs)
 __device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
-  return *(volatile const unsigned long long*)p;
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
 }
 
 // ------------------------------------------------------------------ TMA bulk copies
@@ -185,7 +189,9 @@ __device__ void set_error(const DevCtx& c, int code, int info, unsigned long lon
 }
 
 __device__ __forceinline__ bool has_error(const DevCtx& c) {
-  return *(volatile int*)&c.g->error != 0;
+  int v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(&c.g->error) : "memory");
+  return v != 0;
 }
 
 // spin helper: true while waiting may continue (no error, no timeout)
@@ -833,13 +839,23 @@ __device__ int plan_per_tb(const DevCtx& c, Smem& s, int k) {
   }
   for (int j = 0; j < g; j++) s.b.vict[j] = 0;
   int r = 0;
-  while (g + r < a) {  // retired frames, oldest first: one contiguous range
+  if (g < a) {  // retired frames, oldest first: one contiguous range
+    // a failed CAS returns the current head: retry from it (one round trip per attempt),
+    // re-reading the tail only when the head seems to have caught up with it
     unsigned long long h = ld_volatile_u64(&c.g->ret_head), t = ld_volatile_u64(&c.g->ret_tail);
-    if (h >= t) break;
-    unsigned long long take = t - h < (unsigned long long)(a - g) ? t - h : (unsigned long long)(a - g);
-    if (atomicCAS(&c.g->ret_head, h, h + take) == h) {
-      s.b.ret_pos = h;
-      r = (int)take;
+    for (;;) {
+      if (h >= t) {
+        t = ld_volatile_u64(&c.g->ret_tail);
+        if (h >= t) break;
+      }
+      const unsigned long long take = t - h < (unsigned long long)(a - g) ? t - h : (unsigned long long)(a - g);
+      const unsigned long long prev = atomicCAS(&c.g->ret_head, h, h + take);
+      if (prev == h) {
+        s.b.ret_pos = h;
+        r = (int)take;
+        break;
+      }
+      h = prev;
     }
   }
   int hd = k - g - r;  // own-head remaps
