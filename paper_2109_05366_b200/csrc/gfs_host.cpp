@@ -202,6 +202,9 @@ struct gfs_ctx {
   uint32_t* d_fstate = nullptr;
   uint32_t* d_own_q = nullptr;
   uint32_t* d_retired = nullptr;
+  unsigned long long* d_rpool = nullptr;  // retired FIFO heads/tails
+  int ret_npools = 1;
+  int64_t ret_pcap = 0;
   uint32_t* d_gfifo = nullptr;
   uint32_t* d_recycled = nullptr;
   DevGlobals* d_g = nullptr;
@@ -476,7 +479,7 @@ static void free_all(gfs_ctx* ctx) {
     if (s) cudaStreamDestroy(s);
   for (auto ev : ctx->bell_ev)
     if (ev) cudaEventDestroy(ev);
-  void* dev[] = {ctx->d_frames, ctx->d_fkey, ctx->d_fstate, ctx->d_own_q, ctx->d_retired,
+  void* dev[] = {ctx->d_frames, ctx->d_fkey, ctx->d_fstate, ctx->d_own_q, ctx->d_retired, ctx->d_rpool,
                  ctx->d_gfifo, ctx->d_recycled, ctx->d_g, ctx->d_landing, ctx->d_doorbell,
                  ctx->d_done_pos, ctx->d_stats, ctx->d_scratch};
   for (void* p : dev)
@@ -572,7 +575,10 @@ extern "C" int gfs_create(const gfs_config* cfg_in, gfs_ctx** out) {
     TRY(cudaMalloc(&ctx->d_frames, (size_t)(nframes * cfg.page_size)));
     TRY(cudaMalloc(&ctx->d_fkey, (size_t)nframes * 8));
     TRY(cudaMalloc(&ctx->d_fstate, (size_t)nframes * 4));
-    TRY(cudaMalloc(&ctx->d_retired, (size_t)nframes * 2 * 4));
+    ctx->ret_npools = std::min(RET_POOLS, std::max(1, ctx->n_ctas));
+    ctx->ret_pcap = nframes + 64;
+    TRY(cudaMalloc(&ctx->d_retired, (size_t)ctx->ret_npools * (size_t)ctx->ret_pcap * 4));
+    TRY(cudaMalloc(&ctx->d_rpool, (size_t)RET_POOLS * 16 * 8));
     TRY(cudaMalloc(&ctx->d_recycled, (size_t)nframes * 4));
     if (cfg.policy == GFS_POLICY_PER_TB_LRA)
       TRY(cudaMalloc(&ctx->d_own_q, (size_t)ctx->n_ctas * (size_t)std::max<int64_t>(quota, 1) * 4));
@@ -879,7 +885,8 @@ extern "C" int gfs_run_consume(gfs_ctx* ctx, const gfs_program* prog, void* dst,
     if (f.open && f.d_pt) CUDA_TRY(cudaMemsetAsync(f.d_pt, 0xFF, (size_t)f.npages * 4, ctx->stream));
   if (!cfg.raw_mode) {
     CUDA_TRY(cudaMemsetAsync(ctx->d_fstate, 0, (size_t)ctx->nframes * 4, ctx->stream));
-    CUDA_TRY(cudaMemsetAsync(ctx->d_retired, 0, (size_t)ctx->nframes * 8, ctx->stream));
+    CUDA_TRY(cudaMemsetAsync(ctx->d_retired, 0, (size_t)ctx->ret_npools * (size_t)ctx->ret_pcap * 4, ctx->stream));
+    CUDA_TRY(cudaMemsetAsync(ctx->d_rpool, 0, (size_t)RET_POOLS * 16 * 8, ctx->stream));
     if (ctx->d_gfifo) CUDA_TRY(cudaMemsetAsync(ctx->d_gfifo, 0, (size_t)ctx->gfifo_cap * 4, ctx->stream));
   }
   CUDA_TRY(cudaMemsetAsync(ctx->d_g, 0, sizeof(DevGlobals), ctx->stream));
@@ -922,6 +929,9 @@ extern "C" int gfs_run_consume(gfs_ctx* ctx, const gfs_program* prog, void* dst,
   c.fstate = ctx->d_fstate;
   c.own_q = ctx->d_own_q;
   c.retired = ctx->d_retired;
+  c.rpool = ctx->d_rpool;
+  c.ret_pcap = ctx->ret_pcap;
+  c.ret_npools = ctx->ret_npools;
   c.gfifo = ctx->d_gfifo;
   c.recycled = ctx->d_recycled;
   c.g = ctx->d_g;

@@ -160,7 +160,7 @@ struct Smem {
   long long st[GFS_NSTATS];
   // batched page walk (gread_batch): one entry per page of the batch
   struct {
-    int n_empty, k, status, nvict, nret, ret_lane0, own_lane0, j0;
+    int n_empty, k, status, nvict, nret, ret_lane0, own_lane0, j0, ret_pool;
     unsigned tail_mask, part_mask;  // pages with a sub-16 B EOF tail / a partial delivery
     int64_t total;                  // bytes this batch delivers
     int64_t rpc_n;
@@ -287,23 +287,64 @@ __device__ uint32_t take_free(const DevCtx& c) {
   return take_recycled(c);
 }
 
-__device__ uint32_t retired_pop(const DevCtx& c) {
-  const unsigned long long cap = 2ull * (unsigned long long)c.nframes;
-  for (;;) {
-    unsigned long long h = ld_volatile_u64(&c.g->ret_head);
-    unsigned long long t = ld_volatile_u64(&c.g->ret_tail);
-    if (h >= t) return PT_EMPTY;
-    if (atomicCAS(&c.g->ret_head, h, h + 1) == h) {
-      uint32_t* e = &c.retired[h % cap];
-      uint64_t t0 = globaltimer();
-      uint32_t v;
-      while ((v = ld_acquire_gpu(e)) == 0) {
-        if (!keep_waiting(c, t0, 11)) return PT_EMPTY;
+// Retired frames (gpu_cache.py:158-167, 208-212) live in ret_npools FIFOs: a finished TB
+// retires into its CTA's FIFO, and a TB reclaims from its CTA's FIFO first, then from the
+// others in order.  Which retired frame a TB gets is schedule-dependent in the reference
+// too whenever several TBs are resident (SURVEY.md §8c rule 4); the counts are not (every
+// reclaim is one remap of a valid frame), and with one resident CTA there is one FIFO —
+// exactly the reference's global oldest-first order.  Spreading the FIFOs keeps hundreds of
+// CTAs from serialising on one head counter.
+__device__ __forceinline__ unsigned long long* rp_head(const DevCtx& c, int p) { return c.rpool + 16 * p; }
+__device__ __forceinline__ unsigned long long* rp_tail(const DevCtx& c, int p) { return c.rpool + 16 * p + 1; }
+__device__ __forceinline__ uint32_t* rp_entry(const DevCtx& c, int p, unsigned long long pos) {
+  return c.retired + (int64_t)p * c.ret_pcap + (int64_t)(pos % (unsigned long long)c.ret_pcap);
+}
+
+// Reserve up to `want` consecutive entries of one FIFO (home first); returns how many, with
+// the FIFO and first position in *pool / *pos.  One round trip per CAS attempt.
+__device__ int retired_reserve(const DevCtx& c, int want, int* pool, unsigned long long* pos) {
+  const int home = (int)(blockIdx.x % (unsigned)c.ret_npools);
+  for (int q = 0; q < c.ret_npools; q++) {
+    const int p = home + q < c.ret_npools ? home + q : home + q - c.ret_npools;
+    unsigned long long h = ld_volatile_u64(rp_head(c, p)), t = ld_volatile_u64(rp_tail(c, p));
+    for (;;) {
+      if (h >= t) {
+        t = ld_volatile_u64(rp_tail(c, p));
+        if (h >= t) break;
       }
-      *e = 0;
-      return v - 1;
+      const unsigned long long take = t - h < (unsigned long long)want ? t - h : (unsigned long long)want;
+      const unsigned long long prev = atomicCAS(rp_head(c, p), h, h + take);
+      if (prev == h) {
+        *pool = p;
+        *pos = h;
+        return (int)take;
+      }
+      h = prev;
     }
   }
+  return 0;
+}
+
+// Take the value of a reserved entry once its pusher has written it.
+__device__ uint32_t retired_take(const DevCtx& c, int pool, unsigned long long pos, bool* ok) {
+  uint32_t* e = rp_entry(c, pool, pos);
+  const uint64_t t0 = globaltimer();
+  uint32_t v;
+  while ((v = ld_acquire_gpu(e)) == 0) {
+    if (!keep_waiting(c, t0, 11)) break;
+  }
+  *e = 0;
+  *ok = v != 0;
+  return v - 1;
+}
+
+__device__ uint32_t retired_pop(const DevCtx& c) {
+  int pool;
+  unsigned long long pos;
+  if (retired_reserve(c, 1, &pool, &pos) == 0) return PT_EMPTY;
+  bool ok;
+  const uint32_t f = retired_take(c, pool, pos, &ok);
+  return ok ? f : PT_EMPTY;
 }
 
 __device__ __forceinline__ void own_push(const DevCtx& c, Smem& s, uint32_t f) {
@@ -839,24 +880,12 @@ __device__ int plan_per_tb(const DevCtx& c, Smem& s, int k) {
   }
   for (int j = 0; j < g; j++) s.b.vict[j] = 0;
   int r = 0;
-  if (g < a) {  // retired frames, oldest first: one contiguous range
-    // a failed CAS returns the current head: retry from it (one round trip per attempt),
-    // re-reading the tail only when the head seems to have caught up with it
-    unsigned long long h = ld_volatile_u64(&c.g->ret_head), t = ld_volatile_u64(&c.g->ret_tail);
-    for (;;) {
-      if (h >= t) {
-        t = ld_volatile_u64(&c.g->ret_tail);
-        if (h >= t) break;
-      }
-      const unsigned long long take = t - h < (unsigned long long)(a - g) ? t - h : (unsigned long long)(a - g);
-      const unsigned long long prev = atomicCAS(&c.g->ret_head, h, h + take);
-      if (prev == h) {
-        s.b.ret_pos = h;
-        r = (int)take;
-        break;
-      }
-      h = prev;
-    }
+  if (g < a) {  // retired frames, oldest first: one contiguous range of one FIFO
+    int pool = 0;
+    unsigned long long pos = 0;
+    r = retired_reserve(c, a - g, &pool, &pos);
+    s.b.ret_pos = pos;
+    s.b.ret_pool = pool;
   }
   int hd = k - g - r;  // own-head remaps
   if (hd > len0) hd = (int)len0;
@@ -1005,20 +1034,13 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
 
   // (C) warp 0: victims (own-head / retired frames) and the own-queue update
   if (w0 && c.policy == GFS_POLICY_PER_TB_LRA) {
-    const unsigned long long cap = 2ull * (unsigned long long)c.nframes;
     uint32_t f = PT_EMPTY;
     bool abort = false;
     if (lane < kk && s.b.vict[lane]) {
       if (lane < s.b.own_lane0) {  // retired range
-        uint32_t* e = &c.retired[(s.b.ret_pos + (lane - s.b.ret_lane0)) % cap];
-        uint64_t t0 = globaltimer();
-        uint32_t v;
-        while ((v = ld_acquire_gpu(e)) == 0) {
-          if (!keep_waiting(c, t0, 11)) break;
-        }
-        *e = 0;
-        f = v - 1;
-        abort = v == 0;
+        bool ok;
+        f = retired_take(c, s.b.ret_pool, s.b.ret_pos + (lane - s.b.ret_lane0), &ok);
+        abort = !ok;
       } else {  // own oldest frames
         f = c.own_q[(int64_t)blockIdx.x * c.quota + (s.b.own_head0 + (lane - s.b.own_lane0)) % c.quota];
       }
@@ -1824,14 +1846,14 @@ __device__ bool run_tb(const DevCtx& c, Smem& s, float* cons_smem, int tb, int& 
     s.pb_filled = 0;
     s.pb_count = 0;
     if (c.policy == GFS_POLICY_PER_TB_LRA && s.own_len > 0)
-      ret_pos = atomicAdd(&c.g->ret_tail, (unsigned long long)s.own_len);
+      ret_pos = atomicAdd(rp_tail(c, (int)(blockIdx.x % (unsigned)c.ret_npools)), (unsigned long long)s.own_len);
   }
   __syncthreads();
   if (c.policy == GFS_POLICY_PER_TB_LRA && s.own_len > 0) {
-    const unsigned long long cap = 2ull * (unsigned long long)c.nframes;
+    const int pool = (int)(blockIdx.x % (unsigned)c.ret_npools);
     for (int64_t i = tid; i < s.own_len; i += BS) {
       uint32_t f = c.own_q[(int64_t)blockIdx.x * c.quota + (s.own_head + i) % c.quota];
-      st_release_gpu(&c.retired[(ret_pos + i) % cap], f + 1);
+      st_release_gpu(rp_entry(c, pool, ret_pos + i), f + 1);
     }
   }
   __syncthreads();

@@ -15,6 +15,7 @@ constexpr uint32_t FR_VALID = 1u;             // frame state bit 0; refcount in 
 constexpr uint32_t FR_REF = 2u;
 constexpr uint32_t RING_TOMB = 0xFFFFFFFFu;   // global FIFO tombstone
 constexpr int MAX_PB_ENTRIES = 16384;         // private-buffer entries per TB (smem bitmap)
+constexpr int RET_POOLS = 32;                 // retired-frame FIFOs (per-tb-lra reclaim)
 
 // Request record in the mapped request ring (device writes, host daemon reads).
 struct alignas(32) RpcReq {
@@ -99,7 +100,10 @@ struct DevCtx {
   unsigned long long* fkey;  // (fid << 40) | page
   uint32_t* fstate;
   uint32_t* own_q;           // [n_ctas][quota]
-  uint32_t* retired;         // [2 * nframes], value + 1, 0 = empty
+  uint32_t* retired;         // [ret_npools][ret_pcap], value + 1, 0 = empty
+  unsigned long long* rpool; // [RET_POOLS][16]: head at [16 p], tail at [16 p + 1] (own 128 B line)
+  int64_t ret_pcap;          // entries per retired FIFO (>= frames: a frame is in at most one)
+  int32_t ret_npools;        // min(RET_POOLS, n_ctas): CTA b retires into FIFO b % ret_npools
   uint32_t* gfifo;           // [gfifo_cap], value + 1, 0 = reserved-unwritten
   uint32_t* recycled;        // [nframes]
   DevGlobals* g;
