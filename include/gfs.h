@@ -83,6 +83,9 @@ typedef struct gfs_config {
   int32_t k1_tma;          /* gpu.k1_copy: 1 = span -> frame/user copies by TMA bulk copies
                               through a shared-memory ring, 0 = 16-byte vector loads/stores */
   int32_t numa_pin;        /* io.numa_pin: daemon threads on the CPUs local to the GPU's PCIe root */
+  int32_t lookahead;       /* gpu.lookahead: a page batch may run past a page-aligned request to
+                              the TB's segment end (the next greads find their bytes delivered) */
+  int32_t reserved[1];
 } gfs_config;
 
 /* One gread program set (workloads.py:24-31 programs, flattened).

@@ -911,6 +911,7 @@ extern "C" int gfs_run_consume(gfs_ctx* ctx, const gfs_program* prog, void* dst,
   c.raw_mode = cfg.raw_mode;
   c.log = cfg.log;
   c.timeline = cfg.timeline;
+  c.lookahead = cfg.lookahead;
   c.verify = cfg.verify;
   c.pcie_disabled = cfg.pcie_disabled;
   c.n_files = (int32_t)ctx->files.size();

@@ -173,6 +173,8 @@ struct Smem {
   } b;
   int64_t pb_last_nb;        // bytes of the last private-buffer entry
   int fresh_done;            // this CTA saw the never-used frames run out (they never return)
+  // lookahead: file bytes [la_lo, la_hi) of la_fid were delivered ahead of their gread
+  int64_t la_fid, la_lo, la_hi;
   int64_t page_size_cached;  // c.page_size, for the smem-only pb_take
   uint32_t pb_absent[MAX_PB_ENTRIES / 32];  // private-buffer entries consumed / dropped
 };
@@ -1368,8 +1370,20 @@ __device__ int64_t gread(const DevCtx& c, Smem& s, int64_t fid, int64_t offset, 
   int64_t g_pos = offset;
   const int64_t g_end = offset + size;
   uint32_t* pt = F.pt;
+  // Lookahead (gpu.lookahead): with page-aligned requests a batch may run past this request
+  // to the end of the TB's segment — the pages the TB's next greads would walk, in the same
+  // order, with the same lookups, allocations, private-buffer takes, installs and
+  // deliveries (straight into their user-buffer positions).  Those greads then find their
+  // bytes delivered.  Every counter and log is what the request-by-request walk produces.
+  const bool la = c.lookahead && (offset % pg) == 0 && (c.request_bytes % pg) == 0;
+  const int64_t d_end = la ? (seg_end < fs ? seg_end : fs) : g_end;
+  if (fid == s.la_fid && offset >= s.la_lo && offset < s.la_hi) {
+    const int64_t covered = (s.la_hi < g_end ? s.la_hi : g_end) - offset;
+    if (covered >= size) return size;
+    g_pos = offset + covered;
+  }
   for (;;) {
-    if (g_pos >= g_end || g_pos >= fs) return g_pos - offset;
+    if (g_pos >= g_end || g_pos >= fs) return (g_pos < g_end ? g_pos : g_end) - offset;
     const int64_t page = g_pos / pg;
     const int64_t page_end = (page + 1) * pg < fs ? (page + 1) * pg : fs;
     int64_t want = (g_end < page_end ? g_end : page_end) - g_pos;
@@ -1377,11 +1391,19 @@ __device__ int64_t gread(const DevCtx& c, Smem& s, int64_t fid, int64_t offset, 
     const unsigned long long key = page_key(fid, page);
 
     {  // cold run of pages: batched walk
-      const int64_t got = gread_batch<BS>(c, s, fid, g_pos, g_end, seg_end,
+      const int64_t got = gread_batch<BS>(c, s, fid, g_pos, d_end, seg_end,
                                           dst ? dst + (g_pos - offset) : nullptr, bad_words, span_buf);
       if (got < 0) return -1;
       if (got > 0) {
         g_pos += got;
+        if (g_pos > g_end) {  // delivered ahead: remember for the next greads of this TB
+          if (tid == 0) {
+            s.la_fid = fid;
+            s.la_lo = g_end;
+            s.la_hi = g_pos;
+          }
+          __syncthreads();
+        }
         continue;
       }
     }
@@ -1808,6 +1830,8 @@ __device__ bool run_tb(const DevCtx& c, Smem& s, float* cons_smem, int tb, int& 
     s.ra_next_fid = -1;
     s.ra_next_page = -1;
     s.last_gfifo_pos = -1;
+    s.la_fid = -1;
+    s.la_lo = s.la_hi = 0;
   }
   __syncthreads();
   int64_t pos = c.dst_off[tb];
@@ -1817,6 +1841,10 @@ __device__ bool run_tb(const DevCtx& c, Smem& s, float* cons_smem, int tb, int& 
     if (fid < 0 || fid >= c.n_files) {
       if (tid == 0) set_error(c, ERR_BAD_PROGRAM, tb, (unsigned long long)sg);
       return false;
+    }
+    if (c.lookahead && sg > s0) {  // bytes delivered ahead belong to the segment that fetched them
+      if (tid == 0) s.la_fid = -1;
+      __syncthreads();
     }
     int64_t seg_off = 0;
     while (seg_off < len) {

@@ -62,6 +62,7 @@ def native_config(cfg: ExperimentConfig, max_request_bytes: int = 0) -> native.G
         raise GfsError(f"gpu.k1_copy must be tma or ldg, not {cfg['gpu.k1_copy']!r}")
     c.k1_tma = int(cfg["gpu.k1_copy"] == "tma")
     c.numa_pin = int(bool(cfg["io.numa_pin"]))
+    c.lookahead = int(bool(cfg["gpu.lookahead"]))
     return c
 
 

@@ -48,10 +48,32 @@ def test_stat_names_match_oracle_counters(lib):
         assert k in names
 
 
-def test_struct_sizes_match_header(lib):
-    # gfs_config: 7 int64 + 13 int32 + 3 reserved int32 = 56 + 64 = 120 bytes
-    assert C.sizeof(native.GfsConfig) == 120
-    assert C.sizeof(native.GfsProgram) == 48
+def test_struct_layouts_match_header(lib, tmp_path):
+    """The ctypes mirrors have the C structs' sizes and field offsets (compiled from
+    include/gfs.h with the host compiler)."""
+    import shutil
+    import subprocess
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        pytest.skip("no host C compiler")
+    checks = {"gfs_config": native.GfsConfig, "gfs_program": native.GfsProgram,
+              "gfs_consumer": native.GfsConsumer}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "gfs.h"', "int main(void) {"]
+    for cname, py in checks.items():
+        lines.append(f'printf("{cname} %zu\\n", sizeof({cname}));')
+        for fname, _t in py._fields_:
+            lines.append(f'printf("{cname}.{fname} %zu\\n", offsetof({cname}, {fname}));')
+    lines.append("return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run([cc, "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    got = dict(l.split() for l in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                  check=True).stdout.splitlines())
+    for cname, py in checks.items():
+        assert int(got[cname]) == C.sizeof(py), cname
+        for fname, _t in py._fields_:
+            assert int(got[f"{cname}.{fname}"]) == getattr(py, fname).offset, (cname, fname)
 
 
 def test_gen_file_matches_content_law(lib, tmp_path):
