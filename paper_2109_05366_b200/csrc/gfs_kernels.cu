@@ -1642,6 +1642,40 @@ __device__ void gemvt_part(const gfs_consumer& k, float* acc, const uint4* v4, i
   const bool sm = M <= GEMVT_SMEM_COLS;
   const int64_t row_lo = e0 / M;
   const uint32_t r0 = (uint32_t)(e0 - row_lo * M), M32 = (uint32_t)M;
+  if (sm && M % (4 * bs) == 0 && M / (4 * bs) <= 4) {
+    // Each thread meets the same <= 4 column quads in every row of the request (the
+    // vector stride 4 bs divides the row): sum them in registers, then add them to the
+    // CTA accumulator once — threads own disjoint columns, so plain shared adds.
+    const int nq = (int)(M / (4 * bs));
+    float a[4][4] = {};
+    const int64_t nv = ne >> 2;
+    for (int64_t i0 = tid; i0 < nv; i0 += (int64_t)bs * nq) {
+#pragma unroll
+      for (int m = 0; m < 4; m++) {  // static indices: a[][] stays in registers
+        const int64_t i = i0 + (int64_t)m * bs;
+        if (m < nq && i < nv) {
+          const uint4 u = __ldcg(v4 + i);
+          const uint32_t l = r0 + 4 * (uint32_t)i;
+          const float xr = k.x2[row_lo + l / M32];
+          a[m][0] += decode_f32(u.x) * xr;
+          a[m][1] += decode_f32(u.y) * xr;
+          a[m][2] += decode_f32(u.z) * xr;
+          a[m][3] += decode_f32(u.w) * xr;
+        }
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < 4; m++) {
+      if (m < nq) {
+        const uint32_t col = (r0 + 4 * (uint32_t)(tid + m * bs)) % M32;
+        acc[col + 0] += a[m][0];
+        acc[col + 1] += a[m][1];
+        acc[col + 2] += a[m][2];
+        acc[col + 3] += a[m][3];
+      }
+    }
+    return;
+  }
   for (int64_t i = tid; i < (ne >> 2); i += bs) {
     const uint4 u = __ldcg(v4 + i);
     const uint32_t l = r0 + 4 * (uint32_t)i;
@@ -1658,8 +1692,10 @@ __device__ void gemvt_part(const gfs_consumer& k, float* acc, const uint4* v4, i
 
 // Kmeans assignment + accumulation, one thread per point.  Distances are summed over the
 // features in order with IEEE round-to-nearest steps and no contraction (the bits a
-// float32 reference gets); the features are read once, as 16-byte vectors.  Warp-uniform
-// loop: a warp takes 32 consecutive points per step.
+// float32 reference gets).  Warp-uniform loop: a warp takes 32 consecutive points per
+// step.  The point bytes were just delivered into the user buffer (never read by this SM
+// before), so L1-cached loads are coherent here: the distance pass brings the lines into
+// L1 and the accumulation pass re-reads them from there instead of from L2.
 template <int BS>
 __device__ void kmeans_part(const gfs_consumer& k, float* smem, const uint8_t* data, int64_t np) {
   const int K = k.k;
@@ -1680,7 +1716,7 @@ __device__ void kmeans_part(const gfs_consumer& k, float* smem, const uint8_t* d
 #pragma unroll
       for (int c = 0; c < GFS_KMEANS_MAX_K; c++) d[c] = 0.f;
       for (int j = 0; j < D; j += 4) {
-        const uint4 u = __ldcg(pv + (j >> 2));
+        const uint4 u = __ldca(pv + (j >> 2));
         const float v[4] = {decode_f32(u.x), decode_f32(u.y), decode_f32(u.z), decode_f32(u.w)};
 #pragma unroll
         for (int c = 0; c < GFS_KMEANS_MAX_K; c++) {
@@ -1710,7 +1746,7 @@ __device__ void kmeans_part(const gfs_consumer& k, float* smem, const uint8_t* d
       for (int t = 0; t < D; t++) {
         int j = lane + t;
         if (j >= D) j -= D;
-        if (valid) row[j] += decode_f32(__ldcg(pw + j));
+        if (valid) row[j] += decode_f32(__ldca(pw + j));
         __syncwarp();
       }
     } else if (valid) {
@@ -1718,7 +1754,7 @@ __device__ void kmeans_part(const gfs_consumer& k, float* smem, const uint8_t* d
       for (int t = 0; t < D; t++) {
         int j = lane + t;
         while (j >= D) j -= D;
-        atomicAdd(&row[j], decode_f32(__ldcg(pw + j)));
+        atomicAdd(&row[j], decode_f32(__ldca(pw + j)));
       }
     }
   }
