@@ -1743,7 +1743,25 @@ __device__ void kmeans_part(const gfs_consumer& k, float* smem, const uint8_t* d
       }
       // lanes start at different features (cols >= 32), so in every step the 32 lanes
       // touch 32 distinct words of this warp's accumulator: plain read-modify-write
-      for (int t = 0; t < D; t++) {
+      // (the point's words are re-read 8 at a time so one memory latency covers 8 steps)
+      int t = 0;
+      for (; t + 8 <= D; t += 8) {
+        float v[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+          int j = lane + t + u;
+          if (j >= D) j -= D;
+          v[u] = valid ? decode_f32(__ldca(pw + j)) : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+          int j = lane + t + u;
+          if (j >= D) j -= D;
+          if (valid) row[j] += v[u];
+          __syncwarp();
+        }
+      }
+      for (; t < D; t++) {
         int j = lane + t;
         if (j >= D) j -= D;
         if (valid) row[j] += decode_f32(__ldca(pw + j));
@@ -1751,7 +1769,21 @@ __device__ void kmeans_part(const gfs_consumer& k, float* smem, const uint8_t* d
       }
     } else if (valid) {
       atomicAdd(&cnt[best], 1u);
-      for (int t = 0; t < D; t++) {
+      int t = 0;
+      for (; t + 4 <= D; t += 4) {  // 4 loads in flight per latency
+        float v[4];
+        int jj[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          int j = lane + t + u;
+          while (j >= D) j -= D;
+          jj[u] = j;
+          v[u] = decode_f32(__ldca(pw + j));
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u++) atomicAdd(&row[jj[u]], v[u]);
+      }
+      for (; t < D; t++) {
         int j = lane + t;
         while (j >= D) j -= D;
         atomicAdd(&row[j], decode_f32(__ldca(pw + j)));
