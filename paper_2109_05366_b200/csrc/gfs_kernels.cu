@@ -90,6 +90,10 @@ __device__ __forceinline__ void tma_load(void* sdst, const void* gsrc, uint32_t 
                : "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
   uint32_t done = 0;
   while (!done)
@@ -133,8 +137,11 @@ constexpr int TMA_NST = 4;        // K1 stage ring: stages
 constexpr int64_t TMA_CH = 8192;  // bytes per stage (one bulk load, 1-2 bulk stores per page)
 
 struct Smem {
-  unsigned long long tma_bar[TMA_NST];  // stage "full" mbarriers (tx-count)
-  unsigned long long tma_seq;           // chunks staged since launch (stage / parity)
+  unsigned long long tma_bar[TMA_NST];    // stage "full" mbarriers (tx-count)
+  unsigned long long tma_empty[TMA_NST];  // stage "checked" mbarriers (one arrival per checker warp)
+  unsigned long long tma_seq;             // chunks staged since launch (stage / parity)
+  uint32_t tma_epend;                     // bit st: stage st awaits its checkers before reuse
+  uint32_t tma_epar;                      // bit st: parity of that pending phase
   // broadcast from thread 0
   int act;
   int abort;
@@ -1175,16 +1182,25 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
                        (((uintptr_t)src4) & 15) == 0;
   if (use_tma) {
     // K1 by TMA: thread 0 streams the batch HBM -> shared-memory stage ring -> frames (and
-    // whole pages -> user buffer) with bulk copies, TMA_NST stages in flight; when the word
-    // check is on, every thread checks each stage while it sits in shared memory.
+    // whole pages -> user buffer) with bulk copies, TMA_NST stages in flight.  With the
+    // word check on, warps 1.. check each stage while it sits in shared memory and arrive on
+    // its "checked" mbarrier; thread 0 waits for that only before refilling the stage —
+    // producer and checkers never meet at a block barrier inside the batch.
     extern __shared__ __align__(128) float cons_smem[];
     uint8_t* ring = (uint8_t*)cons_smem + c.tma_off;
     const int64_t total_b = (int64_t)kk * pg;
     const int nch = (int)((total_b + TMA_CH - 1) / TMA_CH);
     const unsigned long long G0 = s.tma_seq;
     const uint8_t* srcb = (const uint8_t*)src4;
-    auto load = [&](int i) {
+    const int warp = tid >> 5;
+    auto load = [&](int i) {  // thread 0
       const int st = (int)((G0 + i) % TMA_NST);
+      if (s.tma_epend & (1u << st)) {  // the stage's last chunk must be checked before reuse
+        mbar_wait(&s.tma_empty[st], (s.tma_epar >> st) & 1u);
+        s.tma_epend &= ~(1u << st);
+        s.tma_epar ^= 1u << st;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       const int64_t cb = min(TMA_CH, total_b - (int64_t)i * TMA_CH);
       tma_load(ring + st * TMA_CH, srcb + (int64_t)i * TMA_CH, (uint32_t)cb, &s.tma_bar[st]);
     };
@@ -1197,20 +1213,22 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
       const int64_t b0 = (int64_t)i * TMA_CH;
       const int64_t cb = min(TMA_CH, total_b - b0);
       const uint8_t* sbuf = ring + st * TMA_CH;
-      if (chk || tid == 0) mbar_wait(&s.tma_bar[st], par);
-      if (chk) {
+      if (chk && warp > 0) {  // checkers
+        mbar_wait(&s.tma_bar[st], par);
         const uint4* sv = (const uint4*)sbuf;
         const int64_t wbase = (p0 * pg + b0) >> 3;
-        for (int64_t v = tid; v < (cb >> 4); v += BS) {
+        for (int64_t v = tid - 32; v < (cb >> 4); v += BS - 32) {
           const uint4 q = sv[v];
           const int64_t wi = wbase + 2 * v;
           const uint64_t tag = block_tag(cid, wi);
           const uint64_t lo = ((uint64_t)q.y << 32) | q.x, hi = ((uint64_t)q.w << 32) | q.z;
           bad += (lo != mix64(tag ^ (uint64_t)wi)) + (hi != mix64(tag ^ (uint64_t)(wi + 1)));
         }
-        __syncthreads();  // every thread is done reading this stage
+        __syncwarp();
+        if ((tid & 31) == 0) mbar_arrive(&s.tma_empty[st]);
       }
-      if (tid == 0) {
+      if (tid == 0) {  // producer
+        mbar_wait(&s.tma_bar[st], par);
         // the chunk's pieces: page j gets [max(b0, j pg), min(b0 + cb, (j+1) pg))
         for (int64_t b = b0; b < b0 + cb;) {
           const int j = (int)(b / pg);
@@ -1223,9 +1241,9 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
           b = e;
         }
         tma_commit();
+        if (chk) s.tma_epend |= 1u << st;
         if (i >= 1 && i - 1 + TMA_NST < nch) {  // refill the stage chunk i - 1 used
           tma_wait_read<1>();                   // its stores have read it (chunk i's may not)
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           load(i - 1 + TMA_NST);
         }
       }
@@ -1965,8 +1983,13 @@ __global__ void __launch_bounds__(BS, 4) gread_driver(DevCtx c) {
     s.pull_n = 0;
     s.tma_seq = 0;
     s.fresh_done = 0;
+    s.tma_epend = 0;
+    s.tma_epar = 0;
     if (c.tma) {
-      for (int i = 0; i < TMA_NST; i++) mbar_init(&s.tma_bar[i], 1);
+      for (int i = 0; i < TMA_NST; i++) {
+        mbar_init(&s.tma_bar[i], 1);
+        mbar_init(&s.tma_empty[i], BS / 32 - 1);  // the checker warps
+      }
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     // ring base for this launch: the daemon's completed-request count
