@@ -1248,11 +1248,9 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
         }
       }
     }
-    if (tid == 0) {
-      tma_wait_all();
-      s.tma_seq = G0 + nch;
-    }
-    __syncthreads();
+    if (tid == 0) tma_wait_all();
+    __syncthreads();  // every thread has read G0 and is done with the ring
+    if (tid == 0) s.tma_seq = G0 + nch;  // read again only after later block barriers
   } else {
   // vector v of the batch is vector w of page j: shifts when the page size is a power of 2
   const int vsh = (pg & (pg - 1)) == 0 ? __ffsll(pg) - 1 - 4 : -1;
