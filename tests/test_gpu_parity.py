@@ -230,3 +230,30 @@ def test_timeline_log(synth_dir):
     assert (d["t1"] >= d["t0"]).all()
     s = timeline.summary(sim.result.timeline)
     assert 0 < s["io_busy_frac"] <= 1 and s["ctas"] == min(32, sim.result.stats["ctas"])
+
+
+@pytest.mark.parametrize("request_bytes,readahead", [(4 * KiB, "static"), (16 * KiB, "adaptive"),
+                                                      (64 * KiB, "static"), (10_000, "static")])
+def test_lookahead_is_invisible(request_bytes, readahead, synth_dir):
+    """gpu.lookahead (batches running past page-aligned requests) changes nothing the
+    reference can observe: counters, per-TB deliveries, RPC traces, victims and the user
+    buffer are identical with it on and off (unaligned requests simply do not use it)."""
+    from paper_2109_05366_b200.runtime import Simulation
+    over = {"workload.n_tb": 12, "workload.file_bytes": 12 * MiB + 40960, "workload.total_bytes": 12 * MiB,
+            "workload.request_bytes": request_bytes, "gpufs.prefetch_bytes": 60 * KiB,
+            "gpufs.cache_bytes": 3 * MiB, "gpufs.policy": "per-tb-lra", "gpu.sm_count": 1,
+            "gpu.max_threads_per_sm": 2048, "gpu.threads_per_tb": 2048, "io.readahead": readahead,
+            "io.ra_max_bytes": 256 * KiB, "io.dir": synth_dir, "mode.deterministic": True}
+    res = []
+    for la in (True, False):
+        sim = Simulation(ExperimentConfig({**over, "gpu.lookahead": la}), 42)
+        sim.run(keep_output=True)
+        res.append(sim)
+    a, b = res
+    for k in ("user_bytes", "greads", "pc_lookups", "pc_hits", "pc_misses", "pb_hits", "pb_misses",
+              "rpc_count", "rpc_requested_bytes", "pc_allocs", "pc_remaps", "victims",
+              "pb_filled_bytes", "pb_discarded_bytes", "pb_consumed_bytes", "cache_hit_user_bytes"):
+        assert a.result.stats[k] == b.result.stats[k], k
+    for log in ("deliveries", "rpcs", "victims"):
+        assert np.array_equal(getattr(a.result, log), getattr(b.result, log)), log
+    assert a.checksum == b.checksum and a.mismatched_words == b.mismatched_words == 0
