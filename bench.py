@@ -217,6 +217,26 @@ def fit_size(directory: str, size: int, n: int) -> int:
     return fit
 
 
+def prune_synthetic(directory: str, want_bytes: int) -> None:
+    """When the file system cannot hold the run's file, drop this package's other synthetic
+    files there (gfs_synth_c*_<size>.bin from runs at other GPU counts) first."""
+    import glob
+    target = os.path.join(directory, f"gfs_synth_c0_{want_bytes}.bin")
+    try:
+        st = os.statvfs(directory)
+    except OSError:
+        return
+    free = st.f_bavail * st.f_frsize + (os.path.getsize(target) if os.path.exists(target) else 0)
+    if free >= want_bytes + GiB:
+        return
+    for f in sorted(glob.glob(os.path.join(directory, "gfs_synth_c*_*.bin"))):
+        if f != target:
+            for g in (f, f + ".ok"):
+                if os.path.exists(g):
+                    os.remove(g)
+            print(f"bench: removed {f} to make room for {want_bytes / GiB:.0f} GiB", file=sys.stderr)
+
+
 def ensure_file(cfg, dist: Dist) -> str:
     from paper_2109_05366_b200.runtime import ensure_synthetic, ensure_synthetic_shard
     d, size = cfg["io.dir"], cfg["workload.file_bytes"]
@@ -409,6 +429,8 @@ def main() -> None:
     native.load()
     device = dist.local
     torch.cuda.set_device(device)
+    if dist.rank == 0:
+        prune_synthetic(args.dir, int(args.size_gib * GiB) * dist.world)
     dist.barrier()  # every rank sizes the shard before rank 0 starts writing the file
     size = int(dist.reduce([float(fit_size(args.dir, int(args.size_gib * GiB), dist.world))], "MIN")[0])
     cfg = make_cfg({**headline_overrides(size, dist.world, args.dir), "gpu.device": device}, args.set)
