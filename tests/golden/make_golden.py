@@ -206,7 +206,8 @@ def fuzz_cases() -> dict:
         if over["io.readahead"] != "static":
             continue
         seed = over.pop("seed")
-        over = {kk: v for kk, v in over.items() if not kk.startswith("io.") and kk != "gpu.k1_copy"}
+        over = {kk: v for kk, v in over.items()
+                if not kk.startswith("io.") and kk not in ("gpu.k1_copy", "gpu.cta_threads")}
         out[f"fuzz_{k:02d}"] = (over, seed, "global", "global")
     return out
 

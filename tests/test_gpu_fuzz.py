@@ -48,6 +48,7 @@ def random_case(k: int) -> dict:
         "io.transfer": TRANSFERS[k % len(TRANSFERS)], "seed": 7 + k,
         "io.ra_init_bytes": page * r.below(6),
         "gpu.k1_copy": ("tma", "ldg")[k % 2],
+        "gpu.cta_threads": (256, 128, 512)[k % 3],
     }
 
 
