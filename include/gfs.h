@@ -85,7 +85,8 @@ typedef struct gfs_config {
   int32_t numa_pin;        /* io.numa_pin: daemon threads on the CPUs local to the GPU's PCIe root */
   int32_t lookahead;       /* gpu.lookahead: a page batch may run past a page-aligned request to
                               the TB's segment end (the next greads find their bytes delivered) */
-  int32_t reserved[1];
+  int32_t async_ra;        /* io.async_readahead: copy-engine transfers submit the next window's
+                              request while the current window is consumed (not with logs) */
 } gfs_config;
 
 /* One gread program set (workloads.py:24-31 programs, flattened).

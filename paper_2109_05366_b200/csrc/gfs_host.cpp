@@ -204,6 +204,7 @@ struct gfs_ctx {
   uint32_t* d_retired = nullptr;
   unsigned long long* d_rpool = nullptr;  // retired FIFO heads/tails
   int ret_npools = 1;
+  int landing_halves = 1;  // 2: asynchronous readahead fills one half while the CTA reads the other
   int64_t ret_pcap = 0;
   uint32_t* d_gfifo = nullptr;
   uint32_t* d_recycled = nullptr;
@@ -368,7 +369,7 @@ static void worker_main(gfs_ctx* ctx, int wid) {
     ctx->t_idle.fetch_add((int64_t)(t0 - t_wait), std::memory_order_relaxed);
     ctx->w_phase[wid].store(1, std::memory_order_relaxed);
     const int64_t off = e->offset, size = e->size;
-    const int fid = e->fid, slot = e->slot;
+    const int fid = e->fid, slot = e->slot & 0x3FFFFFFF, half = (e->slot >> 30) & 1;
     int64_t n;
     uint8_t* buf;
     int b = 0;
@@ -418,7 +419,7 @@ static void worker_main(gfs_ctx* ctx, int wid) {
       const bool copy = !hybrid || n >= ce_min;  // hybrid: small spans are pulled by the CTA
       cudaError_t ce = cudaSuccess;
       if (n > 0 && copy) {
-        ce = cudaMemcpyAsync(ctx->d_landing + (int64_t)slot * ctx->slot_bytes, buf, (size_t)n,
+        ce = cudaMemcpyAsync(ctx->d_landing + ((int64_t)slot * ctx->landing_halves + half) * ctx->slot_bytes, buf, (size_t)n,
                              cudaMemcpyHostToDevice, st);
         if (ce == cudaSuccess && dma) ce = cudaEventRecord(ctx->bounce_ev[b], st);
       }
@@ -616,7 +617,8 @@ extern "C" int gfs_create(const gfs_config* cfg_in, gfs_ctx** out) {
   memset(ctx->h_served, 0, 64);
   if (cfg.transfer == GFS_XFER_DMA || cfg.transfer == GFS_XFER_MAPPED ||
       cfg.transfer == GFS_XFER_MAPPED_HYBRID) {
-    TRY(cudaMalloc(&ctx->d_landing, (size_t)(ctx->n_ctas * ctx->slot_bytes)));
+    ctx->landing_halves = (cfg.async_ra && !cfg.raw_mode && cfg.transfer != GFS_XFER_MAPPED_HYBRID) ? 2 : 1;
+    TRY(cudaMalloc(&ctx->d_landing, (size_t)(ctx->n_ctas * ctx->landing_halves * ctx->slot_bytes)));
     TRY(cudaMalloc(&ctx->d_doorbell, (size_t)ctx->n_ctas * 8));
     TRY(cudaMemset(ctx->d_doorbell, 0, (size_t)ctx->n_ctas * 8));
     void* fn = nullptr;
@@ -912,6 +914,8 @@ extern "C" int gfs_run_consume(gfs_ctx* ctx, const gfs_program* prog, void* dst,
   c.log = cfg.log;
   c.timeline = cfg.timeline;
   c.lookahead = cfg.lookahead;
+  c.landing_halves = ctx->landing_halves;
+  c.async_ra = ctx->landing_halves > 1 && !cfg.log;
   c.verify = cfg.verify;
   c.pcie_disabled = cfg.pcie_disabled;
   c.n_files = (int32_t)ctx->files.size();

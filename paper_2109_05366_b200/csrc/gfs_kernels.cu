@@ -182,6 +182,12 @@ struct Smem {
   int fresh_done;            // this CTA saw the never-used frames run out (they never return)
   // lookahead: file bytes [la_lo, la_hi) of la_fid were delivered ahead of their gread
   int64_t la_fid, la_lo, la_hi;
+  // asynchronous readahead: the landing half holding the current span, and the next
+  // window's request in flight into the other half
+  int span_half, ar_pending, ar_half;
+  int64_t ar_fid, ar_page, ar_span;
+  uint32_t ar_seq;
+  unsigned long long ar_pos;
   int64_t page_size_cached;  // c.page_size, for the smem-only pb_take
   uint32_t pb_absent[MAX_PB_ENTRIES / 32];  // private-buffer entries consumed / dropped
 };
@@ -628,9 +634,10 @@ __device__ __forceinline__ void account_transfer(const DevCtx& c, Smem& s, int64
   }
 }
 
-// Submit one request for this CTA's slot and wait for its completion (thread 0).
-// Returns bytes read, or -1 on abort.  rpc.py:82-102 (submit), 192-229 (service).
-__device__ int64_t rpc_call(const DevCtx& c, Smem& s, int64_t fid, int64_t off, int64_t size) {
+// Submit one request for this CTA's slot into landing half `half` (thread 0): rpc.py:82-102.
+// Returns false on abort; *seq_out / *pos_out identify it for rpc_wait.
+__device__ bool rpc_submit(const DevCtx& c, Smem& s, int64_t fid, int64_t off, int64_t size, int half,
+                           uint32_t* seq_out, unsigned long long* pos_out) {
   const unsigned slot = blockIdx.x;
   const unsigned long long Q = (unsigned long long)c.ring_mask + 1;
   const unsigned long long local = atomicAdd(&c.g->req_local, 1ull);
@@ -639,7 +646,7 @@ __device__ int64_t rpc_call(const DevCtx& c, Smem& s, int64_t fid, int64_t off, 
   if (local >= Q) {  // ring position pos - Q (same entry) must have completed, i.e. been read
     const unsigned long long need = pos - Q + 1;
     while (ld_volatile_u64(&c.done_pos[pos & c.ring_mask]) < need) {
-      if (!keep_waiting(c, t0, 20)) return -1;
+      if (!keep_waiting(c, t0, 20)) return false;
       __nanosleep(200);
     }
   }
@@ -649,11 +656,22 @@ __device__ int64_t rpc_call(const DevCtx& c, Smem& s, int64_t fid, int64_t off, 
   ve->offset = off;
   ve->size = size;
   ve->fid = (int32_t)fid;
-  ve->slot = (int32_t)slot;
+  ve->slot = (int32_t)(slot | ((unsigned)half << 30));  // landing half in bit 30
   ve->tb = s.tb;
   const uint32_t seq = (uint32_t)(pos + 1);
   __threadfence_system();
   st_release_sys(&e->seq, seq);
+  *seq_out = seq;
+  *pos_out = pos;
+  return true;
+}
+
+// Wait for the completion of request (seq, pos) of file `fid` at `off` (thread 0):
+// rpc.py:192-229.  Returns bytes read, or -1 on abort.
+__device__ int64_t rpc_wait(const DevCtx& c, Smem& s, int64_t fid, int64_t off, uint32_t seq,
+                            unsigned long long pos) {
+  const unsigned slot = blockIdx.x;
+  const uint64_t t0 = globaltimer();
   const uint64_t tw = globaltimer();
   int64_t n;
   if (c.transfer == GFS_XFER_DMA || c.transfer == GFS_XFER_MAPPED) {
@@ -731,6 +749,85 @@ __device__ int64_t rpc_call(const DevCtx& c, Smem& s, int64_t fid, int64_t off, 
   return n;
 }
 
+// Where the current span (page 0 + private-buffer pages) lives.
+__device__ __forceinline__ const uint8_t* span_base(const DevCtx& c, const Smem& s) {
+  if (c.transfer == GFS_XFER_ZEROCOPY) return c.staging + (int64_t)blockIdx.x * c.slot_bytes;
+  return c.landing + ((int64_t)blockIdx.x * c.landing_halves + s.span_half) * c.slot_bytes;
+}
+
+// Submit and wait (the reference's synchronous RPC).
+__device__ int64_t rpc_call(const DevCtx& c, Smem& s, int64_t fid, int64_t off, int64_t size, int half = 0) {
+  uint32_t seq;
+  unsigned long long pos;
+  if (!rpc_submit(c, s, fid, off, size, half, &seq, &pos)) return -1;
+  return rpc_wait(c, s, fid, off, seq, pos);
+}
+
+// A readahead the TB did not consume (it left the stream): wait for it, count its bytes
+// as moved (they show up as prefetch waste).
+__device__ int drain_readahead(const DevCtx& c, Smem& s) {
+  if (!s.ar_pending) return 0;
+  const int64_t n = rpc_wait(c, s, s.ar_fid, s.ar_page * c.page_size, s.ar_seq, s.ar_pos);
+  s.ar_pending = 0;
+  if (n < 0) return -1;
+  account_transfer(c, s, n);
+  return 0;
+}
+
+// The span starting at `page` (thread 0): request_span + RPC (prefetcher.py:13-25,
+// rpc.py:82-229).  With asynchronous readahead (copy-engine transfers, adaptive windows)
+// the request for the window after it is submitted as soon as this one lands, into the
+// other landing half, and adopted when the TB reaches its first page — the same requests,
+// the same windows and counters, issued one window earlier.  Returns bytes, -1 on abort.
+__device__ int64_t fetch_span(const DevCtx& c, Smem& s, int64_t fid, int64_t page, int64_t seg_end,
+                              int64_t* span_out) {
+  const int64_t pg = c.page_size;
+  int64_t span, n;
+  if (s.ar_pending && s.ar_fid == fid && s.ar_page == page) {  // adopt the readahead
+    span = s.ar_span;
+    n = rpc_wait(c, s, fid, page * pg, s.ar_seq, s.ar_pos);
+    s.ar_pending = 0;
+    s.span_half = s.ar_half;
+  } else {
+    if (drain_readahead(c, s) < 0) return -1;
+    span = rpc_span(c, s, fid, page, seg_end);
+    const int h = c.landing_halves > 1 ? (s.span_half ^ 1) : 0;
+    n = span > 0 ? rpc_call(c, s, fid, page * pg, span, h) : 0;
+    if (n >= 0) {
+      log_rec(c, GFS_LOG_RPCS, s.tb, fid, page * pg, span);
+      ST(rpc_count)++;
+      ST(rpc_requested_bytes) += span;
+    }
+    s.span_half = h;
+  }
+  *span_out = span;
+  if (n < 0) return -1;
+  account_transfer(c, s, n);
+  if (c.async_ra && n > 0 && n == span) {
+    const int64_t next = page + (n + pg - 1) / pg;
+    if (next * pg < seg_end && next * pg < c.files[fid].size) {
+      const int64_t span2 = rpc_span(c, s, fid, next, seg_end);
+      if (span2 > 0) {
+        const int h2 = s.span_half ^ 1;
+        uint32_t seq;
+        unsigned long long pos;
+        if (!rpc_submit(c, s, fid, next * pg, span2, h2, &seq, &pos)) return -1;
+        log_rec(c, GFS_LOG_RPCS, s.tb, fid, next * pg, span2);
+        ST(rpc_count)++;
+        ST(rpc_requested_bytes) += span2;
+        s.ar_pending = 1;
+        s.ar_fid = fid;
+        s.ar_page = next;
+        s.ar_span = span2;
+        s.ar_half = h2;
+        s.ar_seq = seq;
+        s.ar_pos = pos;
+      }
+    }
+  }
+  return n;
+}
+
 // ------------------------------------------------------------------ copies (all threads)
 
 // Generic congruence-aware copy of n bytes (K2 and partial deliveries).
@@ -768,7 +865,7 @@ __device__ void copy_bytes(uint8_t* dst, const uint8_t* src, int64_t n) {
 template <int BS>
 __device__ void pull_span(const DevCtx& c, Smem& s) {
   if (s.pull_n <= 0) return;
-  copy_bytes<BS, SRC_SYS>(c.landing + (int64_t)blockIdx.x * c.slot_bytes, s.pull_src, s.pull_n);
+  copy_bytes<BS, SRC_SYS>((uint8_t*)span_base(c, s), s.pull_src, s.pull_n);
   __syncthreads();  // every load has returned: the buffer may be reused
   if (threadIdx.x == 0) {
     if (s.pull_buf >= 0) {
@@ -1096,19 +1193,13 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
       const int64_t page = p0;
       ST(pb_misses)++;
       j0 = 1;
-      const int64_t span = rpc_span(c, s, fid, page, seg_end);
-      const int64_t n = span > 0 ? rpc_call(c, s, fid, page * pg, span) : 0;
+      int64_t span;
+      const int64_t n = fetch_span(c, s, fid, page, seg_end, &span);
       if (n < 0) {
         status = 2;
-      } else {
-        log_rec(c, GFS_LOG_RPCS, s.tb, fid, page * pg, span);
-        ST(rpc_count)++;
-        ST(rpc_requested_bytes) += span;
-        account_transfer(c, s, n);
-        if (n == 0) {
-          set_error(c, ERR_IO, (int)fid, (unsigned long long)page);
-          status = 2;
-        }
+      } else if (n == 0) {
+        set_error(c, ERR_IO, (int)fid, (unsigned long long)page);
+        status = 2;
       }
       if (status == 0) {
         const int64_t nb0 = n < pg ? n : pg;
@@ -1131,6 +1222,7 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
   }
   __syncthreads();
   if (s.b.status != 0) return -1;
+  span_buf = span_base(c, s);  // an RPC may have switched landing halves
   if (w0) {  // private-buffer pages' bytes and span offsets; bind frames to their pages
     if (lane >= s.b.j0 && lane < kk) {
       const int64_t i = p0 + lane - s.pb_base;
@@ -1355,8 +1447,7 @@ __device__ int64_t gread(const DevCtx& c, Smem& s, int64_t fid, int64_t offset, 
   const int64_t pg = c.page_size;
   const DevFile& F = c.files[fid];
   const int64_t fs = F.size;
-  uint8_t* span_buf = (c.transfer != GFS_XFER_ZEROCOPY ? c.landing : c.staging) +
-                      (int64_t)blockIdx.x * c.slot_bytes;
+  const uint8_t* span_buf = span_base(c, s);
   if (tid == 0) ST(greads)++;
 
   if (c.raw_mode) {  // gpu_exec.py:114-119, 131-138: whole request, no page cache
@@ -1479,13 +1570,9 @@ __device__ int64_t gread(const DevCtx& c, Smem& s, int64_t fid, int64_t offset, 
             s.nb = nb;
             s.src_off = (page - s.pb_base) * pg;
           } else {
-            int64_t span = rpc_span(c, s, fid, page, seg_end);
-            int64_t n = span > 0 ? rpc_call(c, s, fid, page * pg, span) : 0;
+            int64_t span;
+            int64_t n = fetch_span(c, s, fid, page, seg_end, &span);
             if (n >= 0) {
-              log_rec(c, GFS_LOG_RPCS, s.tb, fid, page * pg, span);
-              ST(rpc_count)++;
-              ST(rpc_requested_bytes) += span;
-              account_transfer(c, s, n);
               act = A_RPC;
               s.n = n;
               s.nb = n < pg ? n : pg;
@@ -1535,7 +1622,7 @@ __device__ int64_t gread(const DevCtx& c, Smem& s, int64_t fid, int64_t offset, 
       want = (g_end < pend ? g_end : pend) - g_pos;
     }
     const bool whole = d && in_page == 0 && want == nb && (((uintptr_t)d & 15) == 0);
-    const uint8_t* src = span_buf + s.src_off;
+    const uint8_t* src = span_base(c, s) + s.src_off;
     int bad = c.transfer != GFS_XFER_ZEROCOPY
                   ? copy_page_in<BS, SRC_HBM>(fmem, whole ? d : nullptr, src, nb, page * pg,
                                               c.verify ? F.content_id : -1)
@@ -1954,6 +2041,7 @@ __device__ bool run_tb(const DevCtx& c, Smem& s, float* cons_smem, int tb, int& 
   // TB done: drain the private buffer, retire own frames (pages stay hittable)
   __shared__ unsigned long long ret_pos;
   if (tid == 0) {
+    if (drain_readahead(c, s) < 0) set_error(c, ERR_IO, -1, 0);
     ST(pb_discarded_bytes) += s.pb_filled;
     s.pb_filled = 0;
     s.pb_count = 0;
@@ -1979,6 +2067,8 @@ __global__ void __launch_bounds__(BS, 4) gread_driver(DevCtx c) {
   if (tid == 0) {
     for (int i = 0; i < GFS_NSTATS; i++) s.st[i] = 0;
     s.pull_n = 0;
+    s.span_half = 0;
+    s.ar_pending = 0;
     s.tma_seq = 0;
     s.fresh_done = 0;
     s.tma_epend = 0;

@@ -84,6 +84,8 @@ struct DevCtx {
   int32_t policy, readahead, transfer, raw_mode, log, verify, pcie_disabled, timeline;
   int32_t tma;               // K1 by TMA bulk copies through the shared-memory stage ring
   int32_t lookahead;         // batches may run past a page-aligned request (gpu.lookahead)
+  int32_t async_ra;          // submit the next window while the current one is consumed
+  int32_t landing_halves;    // landing slots per CTA (2 with async readahead)
   int32_t tma_off;           // byte offset of the stage ring in dynamic shared memory
   int32_t n_files, n_tb, n_ctas;
   uint32_t ring_mask;

@@ -43,7 +43,7 @@ class GfsConfig(C.Structure):
         ("device", C.c_int32), ("cta_threads", C.c_int32), ("max_ctas", C.c_int32),
         ("raw_mode", C.c_int32), ("pcie_disabled", C.c_int32), ("log", C.c_int32),
         ("verify", C.c_int32), ("timeline", C.c_int32), ("k1_tma", C.c_int32),
-        ("numa_pin", C.c_int32), ("lookahead", C.c_int32), ("reserved", C.c_int32 * 1),
+        ("numa_pin", C.c_int32), ("lookahead", C.c_int32), ("async_ra", C.c_int32),
     ]
 
 

@@ -257,3 +257,28 @@ def test_lookahead_is_invisible(request_bytes, readahead, synth_dir):
     for log in ("deliveries", "rpcs", "victims"):
         assert np.array_equal(getattr(a.result, log), getattr(b.result, log)), log
     assert a.checksum == b.checksum and a.mismatched_words == b.mismatched_words == 0
+
+
+@pytest.mark.parametrize("transfer", ["mapped_dma", "dma"])
+@pytest.mark.parametrize("n_tb,ra_max", [(8, 256 * KiB), (48, 1 * MiB), (200, 512 * KiB)])
+def test_async_readahead_is_invisible(transfer, n_tb, ra_max, synth_dir):
+    """io.async_readahead submits each next window while the current one is consumed; the
+    requests, windows, private-buffer accounting and bytes are those of the synchronous
+    walk (sequential strides: every readahead is adopted), and the user buffer verifies."""
+    from paper_2109_05366_b200.runtime import Simulation
+    over = {"workload.n_tb": n_tb, "workload.file_bytes": 48 * MiB, "workload.request_bytes": 64 * KiB,
+            "gpufs.prefetch_bytes": 60 * KiB, "gpufs.cache_bytes": 16 * MiB, "gpufs.policy": "per-tb-lra",
+            "gpu.sm_count": 16, "io.readahead": "adaptive", "io.ra_max_bytes": ra_max,
+            "io.ra_init_bytes": 64 * KiB, "io.transfer": transfer, "io.dir": synth_dir, "io.workers": 8}
+    res = []
+    for ar in (True, False):
+        sim = Simulation(ExperimentConfig({**over, "io.async_readahead": ar}), 42)
+        rep = sim.run()
+        res.append((sim, rep))
+    (a, ra), (b, rb) = res
+    for k in ("user_bytes", "greads", "pc_misses", "pb_hits", "pb_misses", "rpc_count",
+              "rpc_requested_bytes", "pc_allocs", "pc_remaps", "victims", "pb_filled_bytes",
+              "pb_discarded_bytes", "pcie_bytes"):
+        assert a.result.stats[k] == b.result.stats[k], k
+    assert a.checksum == b.checksum and a.mismatched_words == b.mismatched_words == 0
+    assert ra["user_bytes"] == 48 * MiB
