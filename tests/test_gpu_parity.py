@@ -260,7 +260,7 @@ def test_lookahead_is_invisible(request_bytes, readahead, synth_dir):
 
 
 @pytest.mark.parametrize("transfer", ["mapped_dma", "dma"])
-@pytest.mark.parametrize("n_tb,ra_max", [(8, 256 * KiB), (48, 1 * MiB), (200, 512 * KiB)])
+@pytest.mark.parametrize("n_tb,ra_max", [(8, 256 * KiB), (48, 1 * MiB), (192, 512 * KiB)])
 def test_async_readahead_is_invisible(transfer, n_tb, ra_max, synth_dir):
     """io.async_readahead submits each next window while the current one is consumed; the
     requests, windows, private-buffer accounting and bytes are those of the synchronous

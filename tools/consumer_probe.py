@@ -55,6 +55,21 @@ def main():
                     "consume_p50_us": round(float(np.percentile((d["t1"][con] - d["t0"][con]), 50)) / 1e3, 2)
                     if con.any() else None}
             print(json.dumps(line), flush=True)
+            if name == "kmeans_D32_K8":  # where a TB's time goes: waits vs compute
+                per = {}
+                for k in range(len(d["t0"])):
+                    cta = int(d["cta"][k])
+                    e = per.setdefault(cta, {"rpc_wait": 0, "consume": 0, "gread": 0, "first": None, "last": 0})
+                    dur = int(d["t1"][k] - d["t0"][k])
+                    kind = int(d["kind"][k])
+                    e[("rpc_wait", "gread", "consume")[kind]] += dur
+                    e["first"] = int(d["t0"][k]) if e["first"] is None else min(e["first"], int(d["t0"][k]))
+                    e["last"] = max(e["last"], int(d["t1"][k]))
+                t0 = int(d["t0"].min())
+                ends = sorted((v["last"] - t0) / 1e6 for v in per.values())
+                avg = {k: round(float(np.mean([v[k] for v in per.values()])) / 1e6, 2) for k in ("rpc_wait", "consume", "gread")}
+                print(json.dumps({"kmeans_per_cta_ms": avg, "cta_end_ms_p0_p50_p100": [ends[0], ends[len(ends) // 2], ends[-1]],
+                                  "span_ms": (int(d["t1"].max()) - t0) / 1e6}), flush=True)
 
 
 if __name__ == "__main__":
