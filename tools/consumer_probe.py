@@ -2,7 +2,7 @@
 per consumer variant (GB/s, CTA time computing, per-request consume p50).  Not a
 benchmark of record.
 
-    python tools/consumer_probe.py
+    python tools/consumer_probe.py [key=value ...]
 """
 
 import json
@@ -26,13 +26,14 @@ def main():
     n_tb, unit = 128, 128 * 4096
     total = 950_000_000 // unit * unit
     cfg = bench.make_cfg({**bench.headline_overrides(16 * GiB, 1, "/dev/shm"), "mode.timeline": True,
-                          "workload.n_tb": n_tb, "workload.total_bytes": total}, sys.argv[1:])
+                          "workload.n_tb": n_tb, "workload.total_bytes": total},
+                         [x for x in sys.argv[1:] if "=" in x])
     path = bench.ensure_file(cfg, bench.Dist(1))
     wl = gen_sequential_strided([cfg["workload.file_bytes"]], n_tb, total, 64 * KiB, 4096)
     table = ProgramTable.from_programs(wl.programs)
     dst = torch.empty(total, dtype=torch.uint8, device="cuda")
     variants = {"none": None}
-    for D, K in ((32, 1), (32, 4), (32, 8), (16, 8), (64, 8)):
+    for D, K in ((32, 8),):
         variants[f"kmeans_D{D}_K{K}"] = Consumer("kmeans_f32", x=torch.rand(K, D, device="cuda"),
                                                  y=torch.zeros(K, D, device="cuda"),
                                                  out=torch.zeros(K, dtype=torch.int64, device="cuda"),
