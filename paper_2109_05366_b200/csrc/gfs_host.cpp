@@ -629,9 +629,11 @@ extern "C" int gfs_create(const gfs_config* cfg_in, gfs_ctx** out) {
     ctx->write_value64 = (CUresult(*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int))fn;
     // a few copy streams shared by the workers (streams are thread-safe): every extra
     // stream risks sharing a hardware queue with the persistent kernel's stream
-    ctx->worker_streams.resize((size_t)std::min(cfg.io_workers, 2), nullptr);
+    int nstreams = 2;
+    if (const char* e = getenv("GFS_COPY_STREAMS")) nstreams = std::max(1, std::min(16, atoi(e)));  // experiments
+    ctx->worker_streams.resize((size_t)std::min(cfg.io_workers, nstreams), nullptr);
     for (auto& s : ctx->worker_streams) TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    ctx->bell_streams.resize((size_t)std::min(cfg.io_workers, 2), nullptr);
+    ctx->bell_streams.resize((size_t)std::min(cfg.io_workers, nstreams), nullptr);
     for (auto& s : ctx->bell_streams) TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     ctx->bell_ev.resize((size_t)cfg.io_workers, nullptr);
     for (auto& ev : ctx->bell_ev) TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
