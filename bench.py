@@ -449,10 +449,10 @@ def main() -> None:
     total_bytes = nbytes * len(st) * dist.world
     csum = dist.reduce_u64_sum(res["checksum"])
     arms = {}
-    probes = {}
     cpu_base = None
+    probes = roofline_probes(path, size, device, dist) if not args.quick else {}
     if dist.rank == 0 and dist.world == 1 and not args.quick:
-        probes, arms, cpu_base = comparison_arms(cfg, path, device, res)
+        arms, cpu_base = comparison_arms(cfg, path, device, res, probes)
     if dist.rank != 0:
         dist.close()
         return
@@ -483,11 +483,13 @@ def main() -> None:
                    "parallelism": f"{dist.world} GPU shard(s), no data-path collective"},
         "per_gpu_gbps": round(per_gpu, 3),
         "roofline": {"bound": "pcie_h2d" if (h2d and (not stor or h2d <= stor)) else "storage",
-                     "achieved": round(per_gpu, 3), "peak": round(io_peak, 3) if io_peak else None,
-                     "unit": "GB/s", "frac": round(per_gpu / io_peak, 4) if io_peak else None,
+                     "achieved": round(value, 3), "peak": round(io_peak, 3) if io_peak else None,
+                     "unit": "GB/s", "frac": round(value / io_peak, 4) if io_peak else None,
                      "traffic": st[-1]["pcie_bytes"],
+                     "scope": probes.get("scope"),
                      "note": "north_star roofline min(O_DIRECT storage, pinned H2D), both measured "
-                             "in this run; traffic = PCIe bytes per launch"},
+                             "in this run (with N GPUs: every rank at once, summed); traffic = PCIe "
+                             "bytes per launch per GPU"},
         "hbm_roofline": {"bound": "hbm", "achieved": round(gbps(hbm_alg, ms_step / 1e3), 3),
                          "peak": pk.get("hbm_gbs"), "unit": "GB/s",
                          "frac": round(gbps(hbm_alg, ms_step / 1e3) / pk["hbm_gbs"], 5)
@@ -518,6 +520,28 @@ def main() -> None:
     dist.close()
 
 
+def roofline_probes(path: str, size: int, device: int, dist: Dist) -> dict:
+    """The north_star roofline, measured in this run on this box: O_DIRECT read of the
+    shard and pinned host->HBM copy bandwidth.  With N ranks every rank measures at the
+    same time (its own shard, its own GPU) and the probes are summed: the aggregate under
+    the host's real PCIe-switch / memory topology."""
+    from paper_2109_05366_b200 import native
+    dist.barrier()
+    if dist.world == 1:
+        best, how = storage_probe(path, size)
+    else:
+        th = max(4, len(os.sched_getaffinity(0)) // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", "1"))))
+        t = native.bench_storage(path, dist.rank * size, size, th, 4 * MiB, True)
+        best, how = gbps(size, t), f"{th} threads x 4096 KiB O_DIRECT per rank, all ranks at once"
+    dist.barrier()
+    h2d = gbps(GiB, native.bench_h2d(device, 1 * GiB, 5))
+    dist.barrier()
+    stor, h2d_all = dist.reduce([best, h2d], "SUM") if dist.world > 1 else (best, h2d)
+    return {"storage_odirect_gbps": round(stor, 3), "storage_probe": how,
+            "pcie_h2d_gbps": round(h2d_all, 3),
+            "scope": "one GPU" if dist.world == 1 else f"sum over {dist.world} ranks measured concurrently"}
+
+
 def storage_probe(path: str, size: int) -> tuple[float, str]:
     """Best O_DIRECT sequential read bandwidth of `path` over a few reader shapes."""
     from paper_2109_05366_b200 import native
@@ -529,17 +553,12 @@ def storage_probe(path: str, size: int) -> tuple[float, str]:
     return best, how
 
 
-def comparison_arms(cfg, path: str, device: int, head) -> tuple[dict, dict, dict]:
-    """Roofline probes, the paper's comparison arms and the CPU oracle baseline (N=1)."""
+def comparison_arms(cfg, path: str, device: int, head, probes: dict) -> tuple[dict, dict]:
+    """The paper's comparison arms and the CPU oracle baseline (N=1)."""
     from paper_2109_05366_b200 import native
     size = cfg["workload.total_bytes"]
     threads = os.cpu_count() or 1
-    probes, arms = {}, {}
-    best, how = storage_probe(path, size)
-    probes["storage_odirect_gbps"] = round(best, 3)
-    probes["storage_probe"] = how
-    t = native.bench_h2d(device, 1 * GiB, 5)
-    probes["pcie_h2d_gbps"] = round(gbps(GiB, t), 3)
+    arms = {}
     dst = head["dst"]
     variants = {
         # the north_star daemon path: O_DIRECT pread into pinned staging, then to HBM
@@ -605,7 +624,7 @@ def comparison_arms(cfg, path: str, device: int, head) -> tuple[dict, dict, dict
         cpu_base = cpu_oracle_sample(path, cfg, size, threads)  # the whole shard
     except Exception as e:
         cpu_base = {"error": str(e)[:300]}
-    return probes, arms, cpu_base
+    return arms, cpu_base
 
 
 def consumer_arm(cfg, path: str, device: int, dst) -> dict:
