@@ -1823,10 +1823,12 @@ __device__ void kmeans_part(const gfs_consumer& k, float* smem, const uint8_t* d
         const float v[4] = {decode_f32(u.x), decode_f32(u.y), decode_f32(u.z), decode_f32(u.w)};
 #pragma unroll
         for (int c = 0; c < GFS_KMEANS_MAX_K; c++) {
-          if (c < K) {
+          if (c < K) {  // one 16-byte broadcast load of the centroid's 4 features (D % 4 == 0)
+            const float4 cv = *(const float4*)(cent + c * D + j);
+            const float cq[4] = {cv.x, cv.y, cv.z, cv.w};
 #pragma unroll
             for (int q = 0; q < 4; q++) {
-              const float df = __fsub_rn(v[q], cent[c * D + j + q]);
+              const float df = __fsub_rn(v[q], cq[q]);
               d[c] = __fadd_rn(d[c], __fmul_rn(df, df));
             }
           }
