@@ -205,6 +205,8 @@ struct gfs_ctx {
   unsigned long long* d_rpool = nullptr;  // retired FIFO heads/tails
   int ret_npools = 1;
   int landing_halves = 1;  // 2: asynchronous readahead fills one half while the CTA reads the other
+  bool stream_pieces = false;  // copy-engine windows land piece by piece
+  unsigned long long* d_landed = nullptr;
   int64_t ret_pcap = 0;
   uint32_t* d_gfifo = nullptr;
   uint32_t* d_recycled = nullptr;
@@ -418,9 +420,30 @@ static void worker_main(gfs_ctx* ctx, int wid) {
     if (dma || mapped_ce || hybrid) {
       const bool copy = !hybrid || n >= ce_min;  // hybrid: small spans are pulled by the CTA
       cudaError_t ce = cudaSuccess;
-      if (n > 0 && copy) {
-        ce = cudaMemcpyAsync(ctx->d_landing + ((int64_t)slot * ctx->landing_halves + half) * ctx->slot_bytes, buf, (size_t)n,
-                             cudaMemcpyHostToDevice, st);
+      cudaStream_t bs = ctx->bell_streams[(size_t)wid % ctx->bell_streams.size()];
+      const int64_t li = (int64_t)slot * ctx->landing_halves + half;
+      const bool streamed = copy && n >= STREAM_SPLIT && ctx->stream_pieces;
+      if (n > 0 && copy && !streamed) {
+        ce = cudaMemcpyAsync(ctx->d_landing + li * ctx->slot_bytes, buf, (size_t)n, cudaMemcpyHostToDevice, st);
+        if (ce == cudaSuccess && dma) ce = cudaEventRecord(ctx->bounce_ev[b], st);
+      }
+      if (streamed) {
+        // the window in pieces: after each, a landed marker; after the first, the doorbell —
+        // the CTA starts on the first piece while the others copy
+        for (int64_t o = 0; o < n && ce == cudaSuccess; o += STREAM_PIECE) {
+          const int64_t len = std::min(STREAM_PIECE, n - o);
+          ce = cudaMemcpyAsync(ctx->d_landing + li * ctx->slot_bytes + o, buf + o, (size_t)len,
+                               cudaMemcpyHostToDevice, st);
+          if (ce != cudaSuccess) break;
+          cudaEventRecord(ctx->bell_ev[wid], st);
+          cudaStreamWaitEvent(bs, ctx->bell_ev[wid], 0);
+          const uint64_t pages = (uint64_t)((o + len + 4095) / 4096);
+          CUresult cr = ctx->write_value64((CUstream)bs, (CUdeviceptr)(ctx->d_landed + li), (cuuint64_t)((pages << 32) | seq), 0);
+          if (cr == CUDA_SUCCESS && o == 0)
+            cr = ctx->write_value64((CUstream)bs, (CUdeviceptr)(ctx->d_doorbell + slot),
+                                    (cuuint64_t)(((uint64_t)n << 32) | seq), 0);
+          if (cr != CUDA_SUCCESS) ce = cudaErrorUnknown;
+        }
         if (ce == cudaSuccess && dma) ce = cudaEventRecord(ctx->bounce_ev[b], st);
       }
       if (ce != cudaSuccess) {
@@ -431,13 +454,14 @@ static void worker_main(gfs_ctx* ctx, int wid) {
       if (!copy) v |= 1ull << 63;  // "not copied: pull it from the mapping"
       // The doorbell goes on a separate stream that waits for this copy: copy streams then
       // carry back-to-back copies only, so the engine never idles behind a memory op.
-      cudaStream_t bs = ctx->bell_streams[(size_t)wid % ctx->bell_streams.size()];
-      if (copy) {
-        cudaEventRecord(ctx->bell_ev[wid], st);
-        cudaStreamWaitEvent(bs, ctx->bell_ev[wid], 0);
+      if (!streamed || n < 0) {
+        if (copy && n > 0) {
+          cudaEventRecord(ctx->bell_ev[wid], st);
+          cudaStreamWaitEvent(bs, ctx->bell_ev[wid], 0);
+        }
+        CUresult cr = ctx->write_value64((CUstream)bs, (CUdeviceptr)(ctx->d_doorbell + slot), (cuuint64_t)v, 0);
+        if (cr != CUDA_SUCCESS) ctx->worker_error.store(EIO);
       }
-      CUresult cr = ctx->write_value64((CUstream)bs, (CUdeviceptr)(ctx->d_doorbell + slot), (cuuint64_t)v, 0);
-      if (cr != CUDA_SUCCESS) ctx->worker_error.store(EIO);
       // The driver may hold freshly enqueued work in its push buffer until the next call on
       // the stream; this worker may not make one for a while (it spins on the ring), and
       // the persistent kernel is waiting on exactly this doorbell.  Kick both streams.
@@ -480,7 +504,7 @@ static void free_all(gfs_ctx* ctx) {
     if (s) cudaStreamDestroy(s);
   for (auto ev : ctx->bell_ev)
     if (ev) cudaEventDestroy(ev);
-  void* dev[] = {ctx->d_frames, ctx->d_fkey, ctx->d_fstate, ctx->d_own_q, ctx->d_retired, ctx->d_rpool,
+  void* dev[] = {ctx->d_frames, ctx->d_fkey, ctx->d_fstate, ctx->d_own_q, ctx->d_retired, ctx->d_rpool, ctx->d_landed,
                  ctx->d_gfifo, ctx->d_recycled, ctx->d_g, ctx->d_landing, ctx->d_doorbell,
                  ctx->d_done_pos, ctx->d_stats, ctx->d_scratch};
   for (void* p : dev)
@@ -619,6 +643,9 @@ extern "C" int gfs_create(const gfs_config* cfg_in, gfs_ctx** out) {
       cfg.transfer == GFS_XFER_MAPPED_HYBRID) {
     ctx->landing_halves = (cfg.async_ra && !cfg.raw_mode && cfg.transfer != GFS_XFER_MAPPED_HYBRID) ? 2 : 1;
     TRY(cudaMalloc(&ctx->d_landing, (size_t)(ctx->n_ctas * ctx->landing_halves * ctx->slot_bytes)));
+    ctx->stream_pieces = !cfg.raw_mode && cfg.transfer != GFS_XFER_MAPPED_HYBRID && ctx->slot_bytes >= STREAM_SPLIT;
+    TRY(cudaMalloc(&ctx->d_landed, (size_t)ctx->n_ctas * ctx->landing_halves * 8));
+    TRY(cudaMemset(ctx->d_landed, 0, (size_t)ctx->n_ctas * ctx->landing_halves * 8));
     TRY(cudaMalloc(&ctx->d_doorbell, (size_t)ctx->n_ctas * 8));
     TRY(cudaMemset(ctx->d_doorbell, 0, (size_t)ctx->n_ctas * 8));
     void* fn = nullptr;
@@ -917,6 +944,8 @@ extern "C" int gfs_run_consume(gfs_ctx* ctx, const gfs_program* prog, void* dst,
   c.timeline = cfg.timeline;
   c.lookahead = cfg.lookahead;
   c.landing_halves = ctx->landing_halves;
+  c.stream_pieces = ctx->stream_pieces ? 1 : 0;
+  c.landed = ctx->d_landed;
   c.async_ra = ctx->landing_halves > 1 && !cfg.log;
   c.verify = cfg.verify;
   c.pcie_disabled = cfg.pcie_disabled;

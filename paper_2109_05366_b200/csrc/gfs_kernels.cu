@@ -185,6 +185,9 @@ struct Smem {
   // asynchronous readahead: the landing half holding the current span, and the next
   // window's request in flight into the other half
   int span_half, ar_pending, ar_half;
+  // streamed windows, per landing half: the last request into it and how much has landed
+  uint32_t st_seq[2];
+  int64_t st_n[2], st_landed[2];
   int64_t ar_fid, ar_page, ar_span;
   uint32_t ar_seq;
   unsigned long long ar_pos;
@@ -669,7 +672,7 @@ __device__ bool rpc_submit(const DevCtx& c, Smem& s, int64_t fid, int64_t off, i
 // Wait for the completion of request (seq, pos) of file `fid` at `off` (thread 0):
 // rpc.py:192-229.  Returns bytes read, or -1 on abort.
 __device__ int64_t rpc_wait(const DevCtx& c, Smem& s, int64_t fid, int64_t off, uint32_t seq,
-                            unsigned long long pos) {
+                            unsigned long long pos, int half) {
   const unsigned slot = blockIdx.x;
   const uint64_t t0 = globaltimer();
   const uint64_t tw = globaltimer();
@@ -739,6 +742,11 @@ __device__ int64_t rpc_wait(const DevCtx& c, Smem& s, int64_t fid, int64_t off, 
     }
   }
   atomicMax(&c.done_pos[pos & c.ring_mask], pos + 1);
+  if (c.stream_pieces && n > 0) {  // the doorbell comes after the first piece
+    s.st_seq[half] = seq;
+    s.st_n[half] = n;
+    s.st_landed[half] = n >= STREAM_SPLIT ? STREAM_PIECE : n;
+  }
   const uint64_t tr = globaltimer();
   ST(wait_ns) += (long long)(tr - tw);
   tl_rec(c, GFS_TL_RPC, s.tb, n, tw, tr);
@@ -747,6 +755,26 @@ __device__ int64_t rpc_wait(const DevCtx& c, Smem& s, int64_t fid, int64_t off, 
     return -1;
   }
   return n;
+}
+
+// Streamed windows (thread 0): wait until the first `need` bytes of the last request into
+// landing half `h` have landed.  False on abort.
+__device__ bool wait_landed(const DevCtx& c, Smem& s, int h, int64_t need) {
+  if (!c.stream_pieces || need <= s.st_landed[h]) return true;
+  if (need > s.st_n[h]) need = s.st_n[h];
+  const unsigned long long* p = &c.landed[(int64_t)blockIdx.x * c.landing_halves + h];
+  const uint64_t t0 = globaltimer();
+  while (need > s.st_landed[h]) {
+    const uint64_t v = ld_acquire_sys64(p);
+    if ((uint32_t)v == s.st_seq[h]) {
+      const int64_t got = (int64_t)(v >> 32) * 4096;
+      s.st_landed[h] = got < s.st_n[h] ? got : s.st_n[h];
+      if (need <= s.st_landed[h]) break;
+    }
+    if (!keep_waiting(c, t0, 24)) return false;
+    __nanosleep(128);
+  }
+  return true;
 }
 
 // Where the current span (page 0 + private-buffer pages) lives.
@@ -759,17 +787,18 @@ __device__ __forceinline__ const uint8_t* span_base(const DevCtx& c, const Smem&
 __device__ int64_t rpc_call(const DevCtx& c, Smem& s, int64_t fid, int64_t off, int64_t size, int half = 0) {
   uint32_t seq;
   unsigned long long pos;
+  if (!wait_landed(c, s, half, s.st_n[half])) return -1;  // the half's previous window is in
   if (!rpc_submit(c, s, fid, off, size, half, &seq, &pos)) return -1;
-  return rpc_wait(c, s, fid, off, seq, pos);
+  return rpc_wait(c, s, fid, off, seq, pos, half);
 }
 
 // A readahead the TB did not consume (it left the stream): wait for it, count its bytes
 // as moved (they show up as prefetch waste).
 __device__ int drain_readahead(const DevCtx& c, Smem& s) {
   if (!s.ar_pending) return 0;
-  const int64_t n = rpc_wait(c, s, s.ar_fid, s.ar_page * c.page_size, s.ar_seq, s.ar_pos);
+  const int64_t n = rpc_wait(c, s, s.ar_fid, s.ar_page * c.page_size, s.ar_seq, s.ar_pos, s.ar_half);
   s.ar_pending = 0;
-  if (n < 0) return -1;
+  if (n < 0 || !wait_landed(c, s, s.ar_half, n)) return -1;
   account_transfer(c, s, n);
   return 0;
 }
@@ -785,7 +814,7 @@ __device__ int64_t fetch_span(const DevCtx& c, Smem& s, int64_t fid, int64_t pag
   int64_t span, n;
   if (s.ar_pending && s.ar_fid == fid && s.ar_page == page) {  // adopt the readahead
     span = s.ar_span;
-    n = rpc_wait(c, s, fid, page * pg, s.ar_seq, s.ar_pos);
+    n = rpc_wait(c, s, fid, page * pg, s.ar_seq, s.ar_pos, s.ar_half);
     s.ar_pending = 0;
     s.span_half = s.ar_half;
   } else {
@@ -811,6 +840,7 @@ __device__ int64_t fetch_span(const DevCtx& c, Smem& s, int64_t fid, int64_t pag
         const int h2 = s.span_half ^ 1;
         uint32_t seq;
         unsigned long long pos;
+        if (!wait_landed(c, s, h2, s.st_n[h2])) return -1;
         if (!rpc_submit(c, s, fid, next * pg, span2, h2, &seq, &pos)) return -1;
         log_rec(c, GFS_LOG_RPCS, s.tb, fid, next * pg, span2);
         ST(rpc_count)++;
@@ -1247,6 +1277,10 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
     const unsigned tm = __ballot_sync(0xffffffffu, tail), pm = __ballot_sync(0xffffffffu, part);
     for (int o = 16; o > 0; o >>= 1) want += __shfl_xor_sync(0xffffffffu, want, o);
     if (lane == 0) {
+      // streamed window: the batch's span bytes must have landed
+      int64_t need = 0;
+      for (int j = 0; j < kk; j++) need = max(need, (int64_t)s.b.src_off[j] + s.b.nb[j]);
+      if (!wait_landed(c, s, s.span_half, need)) set_error(c, ERR_TIMEOUT, 24, 0);
       s.b.tail_mask = tm;
       s.b.part_mask = pm;
       s.b.total = want;
@@ -1581,6 +1615,8 @@ __device__ int64_t gread(const DevCtx& c, Smem& s, int64_t fid, int64_t offset, 
           }
         }
       }
+      if ((act == A_PBHIT || act == A_RPC) && !wait_landed(c, s, s.span_half, s.src_off + s.nb))
+        act = A_ABORT;
       if (has_error(c)) act = A_ABORT;
       s.act = act;
       s.frame = f;
@@ -2071,6 +2107,9 @@ __global__ void __launch_bounds__(BS, 4) gread_driver(DevCtx c) {
     s.pull_n = 0;
     s.span_half = 0;
     s.ar_pending = 0;
+    s.st_seq[0] = s.st_seq[1] = 0;
+    s.st_n[0] = s.st_n[1] = 0;
+    s.st_landed[0] = s.st_landed[1] = 0;
     s.tma_seq = 0;
     s.fresh_done = 0;
     s.tma_epend = 0;
