@@ -745,7 +745,7 @@ __device__ int64_t rpc_wait(const DevCtx& c, Smem& s, int64_t fid, int64_t off, 
   if (c.stream_pieces && n > 0) {  // the doorbell comes after the first piece
     s.st_seq[half] = seq;
     s.st_n[half] = n;
-    s.st_landed[half] = n >= STREAM_SPLIT ? STREAM_PIECE : n;
+    s.st_landed[half] = n >= 2 * c.stream_piece ? c.stream_piece : n;
   }
   const uint64_t tr = globaltimer();
   ST(wait_ns) += (long long)(tr - tw);

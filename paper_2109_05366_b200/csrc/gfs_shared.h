@@ -16,10 +16,8 @@ constexpr uint32_t FR_REF = 2u;
 constexpr uint32_t RING_TOMB = 0xFFFFFFFFu;   // global FIFO tombstone
 constexpr int MAX_PB_ENTRIES = 16384;         // private-buffer entries per TB (smem bitmap)
 constexpr int RET_POOLS = 32;                 // retired-frame FIFOs (per-tb-lra reclaim)
-// Copy-engine windows of at least STREAM_SPLIT bytes land in STREAM_PIECE pieces, each
-// followed by a "landed" marker: the CTA starts on the first piece while the rest copy.
-constexpr int64_t STREAM_SPLIT = 8ll << 20;
-constexpr int64_t STREAM_PIECE = 4ll << 20;
+// Copy-engine windows of at least 2 pieces can land piece by piece, each piece followed
+// by a "landed" marker: the CTA starts on the first piece while the rest copy.
 
 // Request record in the mapped request ring (device writes, host daemon reads).
 struct alignas(32) RpcReq {
@@ -91,6 +89,7 @@ struct DevCtx {
   int32_t async_ra;          // submit the next window while the current one is consumed
   int32_t landing_halves;    // landing slots per CTA (2 with async readahead)
   int32_t stream_pieces;     // copy-engine windows land piece by piece (landed markers)
+  int64_t stream_piece;      // piece bytes (windows of >= 2 pieces are streamed)
   unsigned long long* landed;  // [n_ctas * landing_halves]: (4 KiB pages landed << 32) | seq
   int32_t tma_off;           // byte offset of the stage ring in dynamic shared memory
   int32_t n_files, n_tb, n_ctas;
