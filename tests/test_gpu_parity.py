@@ -305,3 +305,31 @@ def test_reference_acceptance_criteria_on_hardware(synth_dir):
     fig10 = {label: gbps(cfg) for label, cfg in PRESETS["fig10micro"](base)}
     lra, glob, basel = (fig10[k]["io_bandwidth_bps"] for k in ("lra-prefetch", "global-prefetch", "baseline-4k"))
     assert lra > glob > basel and lra >= 4 * basel
+
+
+@pytest.mark.timeout(900)
+def test_headline_config_full_size_against_oracle():
+    """BASELINE configs[1] at full size (16 GiB file, 4 GiB cache, 1024 TBs, per-tb-lra,
+    adaptive windows, the bench's transfer): every counter equals the oracle's run of the
+    same 16 GiB workload, every delivered word verifies against the content law, and the
+    closed forms hold (each page missed once, frames allocated once, the rest remapped)."""
+    import shutil
+    import bench
+    d = "/dev/shm"
+    GiB = 1 << 30
+    if not os.path.isdir(d) or shutil.disk_usage(d).free < 20 * GiB:
+        pytest.skip("needs 20 GiB of tmpfs")
+    cfg = bench.make_cfg(bench.headline_overrides(16 * GiB, 1, d), [])
+    path = bench.ensure_file(cfg, bench.Dist(1))
+    res = bench.run_arm(cfg, path, 0, 0, 1, 1)
+    st = res["stats"][-1]
+    wl, _table = bench.shard_table(cfg, 0)
+    ref = orc.run_oracle(cfg, wl, log=False)
+    for k in ("user_bytes", "greads", "pc_lookups", "pc_hits", "pc_misses", "pc_allocs", "pc_remaps",
+              "victims", "pb_hits", "pb_misses", "pb_filled_bytes", "pb_discarded_bytes", "rpc_count",
+              "rpc_requested_bytes", "pcie_bytes"):
+        assert st[k] == ref.stats[k], (k, st[k], ref.stats[k])
+    pages, frames = 16 * GiB // 4096, 4 * GiB // 4096
+    assert st["user_bytes"] == 16 * GiB and st["pc_misses"] == pages
+    assert st["pc_allocs"] == frames and st["pc_remaps"] == st["victims"] == pages - frames
+    assert st["word_mismatches"] == 0 and res["mismatched_words"] == 0
