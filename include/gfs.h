@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define GFS_ABI_VERSION 1
+#define GFS_ABI_VERSION 2  /* 2: gfs_config grew timeline / k1_tma / numa_pin / lookahead / async_ra */
 
 enum { GFS_OK = 0, GFS_EINVAL = -1, GFS_ECUDA = -2, GFS_EIO = -3, GFS_ENOMEM = -4,
        GFS_ETIMEDOUT = -5, GFS_EDEVICE = -6, GFS_ESTATE = -7 };

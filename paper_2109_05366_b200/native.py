@@ -20,6 +20,7 @@ READAHEAD = {"static": 0, "adaptive": 1}
 TRANSFER = {"zerocopy": 0, "dma": 1, "bounce": 2, "mapped_dma": 3, "mapped": 4,
             "mapped_hybrid": 5}
 O_RDONLY, O_RDWR = 0, 2
+ABI_VERSION = 2  # include/gfs.h GFS_ABI_VERSION: the struct layouts below
 LOG_DELIVERIES, LOG_RPCS, LOG_VICTIMS, LOG_WINDOWS, LOG_TIMELINE = 0, 1, 2, 3, 4
 LOG_WIDTH = {LOG_DELIVERIES: 3, LOG_RPCS: 4, LOG_VICTIMS: 3, LOG_WINDOWS: 2, LOG_TIMELINE: 4}
 TL_RPC, TL_GREAD, TL_CONSUME = 0, 1, 2
@@ -112,6 +113,8 @@ def load(path: str = LIB_PATH):
                  "gfs_bench_storage", "gfs_bench_h2d", "gfs_bench_read_memcpy", "gfs_replay",
                  "gfs_gen_file_range"):
         getattr(L, name).restype = i32
+    if L.gfs_abi_version() != ABI_VERSION:
+        raise GfsError(f"{path} has ABI {L.gfs_abi_version()}, this package needs {ABI_VERSION}: rebuild it")
     _lib = L
     return L
 

@@ -36,7 +36,7 @@ def test_header_declares_the_expected_entry_points():
 def test_library_exports_every_declared_symbol(lib):
     for name in header_functions():
         assert hasattr(lib, name), name
-    assert lib.gfs_abi_version() == 1
+    assert lib.gfs_abi_version() == native.ABI_VERSION
 
 
 def test_stat_names_match_oracle_counters(lib):
