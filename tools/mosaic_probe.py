@@ -1,11 +1,26 @@
-import json, os, sys, time
-sys.path.insert(0, os.getcwd())
+"""The Mosaic-style random workload (preset `mosaic`) under a few transfers / TB counts,
+with per-request RPC and gread latencies from the device timeline.  Not a benchmark of
+record.
+
+    python tools/mosaic_probe.py
+"""
+
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
 os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
-import numpy as np
-import bench
-from paper_2109_05366_b200.experiments import PRESETS
-from paper_2109_05366_b200.runtime import Simulation
-from paper_2109_05366_b200 import timeline
+
+import numpy as np  # noqa: E402
+
+import bench  # noqa: E402
+from paper_2109_05366_b200 import timeline  # noqa: E402
+from paper_2109_05366_b200.experiments import PRESETS  # noqa: E402
+from paper_2109_05366_b200.runtime import Simulation  # noqa: E402
+
 base = bench.make_cfg(bench.headline_overrides(16 << 30, 1, "/dev/shm"), [])
 bench.ensure_file(base, bench.Dist(1))
 for label, mcfg in PRESETS["mosaic"](base):
