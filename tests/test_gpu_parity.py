@@ -42,7 +42,8 @@ def oracle_checksum(cfg, seed):
 
 
 @pytest.mark.parametrize("name", gu.case_names())
-@pytest.mark.parametrize("transfer", ["zerocopy", "bounce", "dma", "mapped", "mapped_dma", "mapped_dma+ldg"])
+@pytest.mark.parametrize("transfer", ["zerocopy", "bounce", "dma", "mapped", "mapped_dma", "mapped_dma+ldg",
+                                      "mapped_hybrid"])
 def test_golden_case_on_device(name, transfer, synth_dir):
     g = gu.load(name)
     transfer, _, k1 = transfer.partition("+")  # K1 copies by TMA (default) or vector loads
