@@ -1469,6 +1469,105 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
   return total;
 }
 
+// One batch of cached pages starting at g_pos (all threads): gpu_exec.py:156-166 for a run
+// of up to 32 pages at once — warp 0 looks up and pins the leading run of valid frames,
+// every thread copies frame -> user buffer, warp 0 unpins and delivers.  Same lookups,
+// hits, bytes and delivery log as the page-by-page walk.  Returns delivered bytes, 0 when
+// page p0 is not a valid cached page (the caller takes the per-page path: pending pages,
+// races, misses).
+template <int BS>
+__device__ int64_t gread_hits(const DevCtx& c, Smem& s, int64_t fid, int64_t g_pos, int64_t g_end,
+                              uint8_t* d0) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  const bool w0 = tid < 32;
+  const DevFile& F = c.files[fid];
+  const int64_t pg = c.page_size, fs = F.size;
+  const int64_t p0 = g_pos / pg;
+  const int64_t lim = g_end < fs ? g_end : fs;
+  const int nmax = (int)min((int64_t)32, (lim + pg - 1) / pg - p0);
+  if (w0) {
+    bool ok = false;
+    uint32_t f = 0;
+    if (lane < nmax) {
+      const uint32_t e = ld_acquire_gpu(&F.pt[p0 + lane]);
+      if (e != PT_EMPTY && e != PT_CLAIMED && !(e & PT_INFLIGHT)) {
+        const uint32_t old = atomicAdd(&c.fstate[e], FR_REF);  // pin against eviction
+        if ((old & FR_VALID) && c.fkey[e] == page_key(fid, p0 + lane)) {
+          ok = true;
+          f = e;
+        } else {
+          atomicSub(&c.fstate[e], FR_REF);
+        }
+      }
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, ok);
+    const int run = (~m == 0u) ? 32 : __ffs(~m) - 1;
+    if (ok && lane >= run) atomicSub(&c.fstate[f], FR_REF);  // beyond the run
+    if (lane < run) s.b.frame[lane] = f;
+    if (lane == 0) s.b.k = run;
+  }
+  __syncthreads();
+  const int kh = s.b.k;
+  if (kh == 0) return 0;
+  // copy frames -> user buffer: one flattened vector loop when every page is delivered
+  // whole to a 16 B-aligned destination, else page by page
+  const int64_t end_b = min(lim, (p0 + kh) * pg);
+  const bool whole = d0 != nullptr && g_pos == p0 * pg && end_b == (p0 + kh) * pg && (((uintptr_t)d0) & 15) == 0;
+  if (whole) {
+    const int64_t vpp = pg >> 4, nvec = (int64_t)kh * vpp;
+    const int vsh = (pg & (pg - 1)) == 0 ? __ffsll(pg) - 1 - 4 : -1;
+    for (int64_t v0 = tid; v0 < nvec; v0 += 4 * BS) {
+      uint4 q[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const int64_t v = v0 + u * BS;
+        if (v < nvec) {
+          const int j = (int)(vsh >= 0 ? v >> vsh : v / vpp);
+          q[u] = __ldcg((const uint4*)(c.frames + (int64_t)s.b.frame[j] * pg) + (v - (int64_t)j * vpp));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const int64_t v = v0 + u * BS;
+        if (v < nvec) ((uint4*)d0)[v] = q[u];
+      }
+    }
+  } else if (d0) {
+    for (int j = 0; j < kh; j++) {
+      const int64_t ps = (p0 + j) * pg;
+      const int64_t lo = ps > g_pos ? ps : g_pos;
+      const int64_t pe = ps + pg < fs ? ps + pg : fs;
+      const int64_t hi = pe < g_end ? pe : g_end;
+      copy_bytes<BS, SRC_HBM>(d0 + (lo - g_pos), c.frames + (int64_t)s.b.frame[j] * pg + (lo - ps), hi - lo);
+    }
+  }
+  __syncthreads();
+  if (w0) {
+    long long want = 0;
+    if (lane < kh) {
+      atomicSub(&c.fstate[s.b.frame[lane]], FR_REF);
+      const int64_t ps = (p0 + lane) * pg;
+      const int64_t lo = ps > g_pos ? ps : g_pos;
+      const int64_t pe = ps + pg < fs ? ps + pg : fs;
+      want = (pe < g_end ? pe : g_end) - lo;
+    }
+    for (int o = 16; o > 0; o >>= 1) want += __shfl_xor_sync(0xffffffffu, want, o);
+    unsigned long long base = 0;
+    if (lane == 0) base = log_reserve(c, GFS_LOG_DELIVERIES, kh);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (base != ~0ull && lane < kh) log_put3(c, GFS_LOG_DELIVERIES, base + lane, s.tb, fid, p0 + lane);
+    if (lane == 0) {
+      ST(pc_lookups) += kh;
+      ST(pc_hits) += kh;
+      ST(user_bytes) += want;
+      ST(cache_hit_user_bytes) += want;
+      s.b.total = want;
+    }
+  }
+  __syncthreads();
+  return s.b.total;
+}
+
 // ----------------------------------------------------------------- gread (all threads)
 
 // One gread of `size` bytes at `offset` of `fid` (gpu_exec.py:107-239).  `dst` is the
@@ -1535,8 +1634,10 @@ __device__ int64_t gread(const DevCtx& c, Smem& s, int64_t fid, int64_t offset, 
       const int64_t got = gread_batch<BS>(c, s, fid, g_pos, d_end, seg_end,
                                           dst ? dst + (g_pos - offset) : nullptr, bad_words, span_buf);
       if (got < 0) return -1;
-      if (got > 0) {
-        g_pos += got;
+      const int64_t hits = got > 0 ? 0 : gread_hits<BS>(c, s, fid, g_pos, d_end,
+                                                      dst ? dst + (g_pos - offset) : nullptr);
+      if (got > 0 || hits > 0) {
+        g_pos += got + hits;
         if (g_pos > g_end) {  // delivered ahead: remember for the next greads of this TB
           if (tid == 0) {
             s.la_fid = fid;

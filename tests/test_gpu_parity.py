@@ -334,3 +334,36 @@ def test_headline_config_full_size_against_oracle():
     assert st["user_bytes"] == 16 * GiB and st["pc_misses"] == pages
     assert st["pc_allocs"] == frames and st["pc_remaps"] == st["victims"] == pages - frames
     assert st["word_mismatches"] == 0 and res["mismatched_words"] == 0
+
+
+@pytest.mark.parametrize("request_bytes", [64 * KiB, 10_000])
+def test_second_pass_hits_match_oracle(request_bytes, synth_dir):
+    """Every TB reads its stride twice in one program (file < cache): the second pass is all
+    page-cache hits — batched on the device — and counters, per-TB deliveries, RPC traces
+    and the user buffer must equal the oracle's."""
+    from paper_2109_05366_b200.runtime import GpuFS, ensure_synthetic
+    from paper_2109_05366_b200.workloads import ProgramTable
+    import torch
+    size, n_tb = 16 * MiB, 16
+    stride = size // n_tb
+    path = ensure_synthetic(synth_dir, 0, size)
+    progs = [[(0, t * stride, stride), (0, t * stride, stride)] for t in range(n_tb)]
+    table = ProgramTable.from_programs(progs)
+    cfg = ExperimentConfig({"gpufs.cache_bytes": 32 * MiB, "gpufs.prefetch_bytes": 60 * KiB,
+                            "gpufs.policy": "per-tb-lra", "gpu.sm_count": 1, "gpu.max_threads_per_sm": 2048,
+                            "gpu.threads_per_tb": 2048, "mode.deterministic": True, "io.workers": 4,
+                            "io.dir": synth_dir, "workload.request_bytes": request_bytes})
+    with GpuFS(cfg, max_request_bytes=request_bytes) as fs:
+        fs.gopen(path, content_id=0)
+        dst = torch.empty(table.dst_bytes, dtype=torch.uint8, device="cuda")
+        r = fs.run(table, request_bytes, dst)
+        got = dst.cpu().numpy()
+    from paper_2109_05366_b200.workloads import WorkloadSpec, union_bytes
+    wl = WorkloadSpec("twice", {0: size}, {0: True}, progs, request_bytes, 2 * size, union_bytes(progs))
+    ref = orc.run_oracle(cfg, wl, source=orc.SRC_SYNTH, materialize_dst=True)
+    for k in ("user_bytes", "greads", "pc_lookups", "pc_hits", "pc_misses", "cache_hit_user_bytes",
+              "pb_hits", "rpc_count", "pc_allocs", "pc_remaps"):
+        assert r.stats[k] == ref.stats[k], (k, r.stats[k], ref.stats[k])
+    assert r.stats["pc_hits"] >= size // 4096
+    assert np.array_equal(r.deliveries, ref.deliveries) and np.array_equal(r.rpcs, ref.rpcs)
+    assert np.array_equal(got, ref.dst)
