@@ -25,12 +25,13 @@ def main():
     ap.add_argument("--size-gib", type=float, default=4.0)
     ap.add_argument("--n-tb", type=int, default=1024)
     ap.add_argument("--request-kib", type=int, default=64)
+    ap.add_argument("--set", action="append", default=[])
     a = ap.parse_args()
     GiB, KiB = bench.GiB, bench.KiB
     size = int(a.size_gib * GiB)
     req = a.request_kib * KiB
     cfg = bench.make_cfg({**bench.headline_overrides(size, 1, "/dev/shm"), "gpufs.cache_bytes": 2 * size,
-                          "workload.request_bytes": req}, [])
+                          "workload.request_bytes": req}, a.set)
     path = bench.ensure_file(cfg, bench.Dist(1))
     stride = size // a.n_tb
     once = ProgramTable.from_programs([[(0, t * stride, stride)] for t in range(a.n_tb)])
@@ -40,7 +41,9 @@ def main():
     with GpuFS(cfg, max_request_bytes=req) as fs:
         fs.gopen(path, content_id=0)
         for name, table in (("once", once), ("twice", twice)):
+            print(f"hit_probe: {name} warm-up", file=sys.stderr, flush=True)
             fs.run(table, req, dst)
+            print(f"hit_probe: {name} timed", file=sys.stderr, flush=True)
             r = fs.run(table, req, dst)
             out[name] = {"ms": r.stats["kernel_ns"] / 1e6, "pc_hits": r.stats["pc_hits"],
                          "mism": r.stats["word_mismatches"]}
