@@ -222,6 +222,25 @@ __device__ __forceinline__ bool keep_waiting(const DevCtx& c, uint64_t t0, int i
   return true;
 }
 
+// mbarrier wait with the device timeout: false (error set) instead of spinning forever.
+__device__ bool mbar_wait_t(const DevCtx& c, unsigned long long* bar, uint32_t parity, int info,
+                            unsigned long long arg) {
+  const uint64_t t0 = globaltimer();
+  for (;;) {
+    uint32_t done = 0;
+    for (int k = 0; k < 64 && !done; k++)
+      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                   : "=r"(done)
+                   : "r"(smem_u32(bar)), "r"(parity)
+                   : "memory");
+    if (done) return true;
+    if (!keep_waiting(c, t0, info)) {
+      if (atomicCAS(&c.g->error_arg, 0ull, arg) == 0ull) {}
+      return false;
+    }
+  }
+}
+
 __device__ void log_rec(const DevCtx& c, int kind, long long a, long long b, long long d, long long e) {
   if (!c.log) return;
   unsigned long long i = atomicAdd(&c.g->log_n[kind], 1ull);
@@ -1322,7 +1341,8 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
     auto load = [&](int i) {  // thread 0
       const int st = (int)((G0 + i) % TMA_NST);
       if (s.tma_epend & (1u << st)) {  // the stage's last chunk must be checked before reuse
-        mbar_wait(&s.tma_empty[st], (s.tma_epar >> st) & 1u);
+        mbar_wait_t(c, &s.tma_empty[st], (s.tma_epar >> st) & 1u, 42,
+                    ((G0 + i) << 16) | ((unsigned long long)st << 8) | (unsigned)(i & 0xff));
         s.tma_epend &= ~(1u << st);
         s.tma_epar ^= 1u << st;
       }
@@ -1340,7 +1360,7 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
       const int64_t cb = min(TMA_CH, total_b - b0);
       const uint8_t* sbuf = ring + st * TMA_CH;
       if (chk && warp > 0) {  // checkers
-        mbar_wait(&s.tma_bar[st], par);
+        mbar_wait_t(c, &s.tma_bar[st], par, 41, (G << 16) | ((unsigned long long)st << 8) | (unsigned)(i & 0xff));
         const uint4* sv = (const uint4*)sbuf;
         const int64_t wbase = (p0 * pg + b0) >> 3;
         for (int64_t v = tid - 32; v < (cb >> 4); v += BS - 32) {
@@ -1354,7 +1374,7 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
         if ((tid & 31) == 0) mbar_arrive(&s.tma_empty[st]);
       }
       if (tid == 0) {  // producer
-        mbar_wait(&s.tma_bar[st], par);
+        mbar_wait_t(c, &s.tma_bar[st], par, 40, (G << 16) | ((unsigned long long)st << 8) | (unsigned)(i & 0xff));
         // the chunk's pieces: page j gets [max(b0, j pg), min(b0 + cb, (j+1) pg))
         for (int64_t b = b0; b < b0 + cb;) {
           const int j = (int)(b / pg);
@@ -2153,6 +2173,9 @@ __device__ bool run_tb(const DevCtx& c, Smem& s, float* cons_smem, int tb, int& 
       return false;
     }
     if (c.lookahead && sg > s0) {  // bytes delivered ahead belong to the segment that fetched them
+      // a gread answered from the lookahead range returns without a block barrier: every
+      // thread must have read la_* there before it is cleared
+      __syncthreads();
       if (tid == 0) s.la_fid = -1;
       __syncthreads();
     }

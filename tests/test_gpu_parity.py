@@ -367,3 +367,31 @@ def test_second_pass_hits_match_oracle(request_bytes, synth_dir):
     assert r.stats["pc_hits"] >= size // 4096
     assert np.array_equal(r.deliveries, ref.deliveries) and np.array_equal(r.rpcs, ref.rpcs)
     assert np.array_equal(got, ref.dst)
+
+
+@pytest.mark.parametrize("transfer,k1", [("mapped_dma", "tma"), ("mapped_dma", "ldg"), ("mapped", "tma")])
+def test_lookahead_segment_boundary_many_tbs(transfer, k1, synth_dir):
+    """256 TBs each read their 1 MiB stride twice (two segments) with lookahead on: the last
+    gread of the first segment is answered from the lookahead range without a block barrier,
+    so clearing that range at the segment boundary must wait for every warp (a missing
+    barrier there split the CTA across two code paths: hang / illegal instruction)."""
+    from paper_2109_05366_b200.runtime import GpuFS, ensure_synthetic
+    import torch
+    size, n_tb, req = 256 * MiB, 256, 64 * KiB
+    stride = size // n_tb
+    path = ensure_synthetic(synth_dir, 0, size)
+    table = ProgramTable.from_programs([[(0, t * stride, stride)] * 2 for t in range(n_tb)])
+    cfg = ExperimentConfig({"gpufs.cache_bytes": 2 * size, "gpufs.prefetch_bytes": 60 * KiB,
+                            "gpufs.policy": "per-tb-lra", "io.dir": synth_dir, "io.transfer": transfer,
+                            "io.readahead": "adaptive", "io.ra_init_bytes": 512 * KiB,
+                            "gpu.k1_copy": k1, "gpu.lookahead": True, "mode.verify": True,
+                            "workload.request_bytes": req})
+    with GpuFS(cfg, max_request_bytes=req) as fs:
+        fs.gopen(path, content_id=0)
+        dst = torch.empty(table.dst_bytes, dtype=torch.uint8, device="cuda")
+        for _ in range(3):
+            dst.zero_()
+            r = fs.run(table, req, dst)
+            assert r.stats["user_bytes"] == 2 * size
+            assert r.stats["word_mismatches"] == 0
+            assert fs.verify(table, dst) == 0
