@@ -225,8 +225,9 @@ __device__ bool mbar_wait_t(const DevCtx& c, unsigned long long* bar, uint32_t p
                    : "r"(smem_u32(bar)), "r"(parity)
                    : "memory");
     if (done) return true;
-    if (!keep_waiting(c, t0, info)) {
-      if (atomicCAS(&c.g->error_arg, 0ull, arg) == 0ull) {}
+    if (has_error(c)) return false;
+    if (globaltimer() - t0 > c.timeout_ns) {  // arg: chunk sequence << 16 | stage << 8 | chunk
+      set_error(c, ERR_TIMEOUT, info, arg);
       return false;
     }
   }
