@@ -1967,18 +1967,29 @@ __device__ void kmeans_part(const gfs_consumer& k, float* smem, const uint8_t* d
       float d[GFS_KMEANS_MAX_K];
 #pragma unroll
       for (int c = 0; c < GFS_KMEANS_MAX_K; c++) d[c] = 0.f;
-      for (int j = 0; j < D; j += 4) {
-        const uint4 u = __ldca(pv + (j >> 2));
-        const float v[4] = {decode_f32(u.x), decode_f32(u.y), decode_f32(u.z), decode_f32(u.w)};
+      // 16 features per round: the point's four 16-byte loads are issued together (one L2
+      // round trip instead of four), then summed in feature order
+      for (int j0 = 0; j0 < D; j0 += 16) {
+        uint4 uu[4];
 #pragma unroll
-        for (int c = 0; c < GFS_KMEANS_MAX_K; c++) {
-          if (c < K) {  // one 16-byte broadcast load of the centroid's 4 features (D % 4 == 0)
-            const float4 cv = *(const float4*)(cent + c * D + j);
-            const float cq[4] = {cv.x, cv.y, cv.z, cv.w};
+        for (int r = 0; r < 4; r++)
+          uu[r] = j0 + 4 * r < D ? __ldca(pv + (j0 >> 2) + r) : make_uint4(0, 0, 0, 0);
 #pragma unroll
-            for (int q = 0; q < 4; q++) {
-              const float df = __fsub_rn(v[q], cq[q]);
-              d[c] = __fadd_rn(d[c], __fmul_rn(df, df));
+        for (int r = 0; r < 4; r++) {
+          const int j = j0 + 4 * r;
+          if (j >= D) break;
+          const uint4 u = uu[r];
+          const float v[4] = {decode_f32(u.x), decode_f32(u.y), decode_f32(u.z), decode_f32(u.w)};
+#pragma unroll
+          for (int c = 0; c < GFS_KMEANS_MAX_K; c++) {
+            if (c < K) {  // one 16-byte broadcast load of the centroid's 4 features (D % 4 == 0)
+              const float4 cv = *(const float4*)(cent + c * D + j);
+              const float cq[4] = {cv.x, cv.y, cv.z, cv.w};
+#pragma unroll
+              for (int q = 0; q < 4; q++) {
+                const float df = __fsub_rn(v[q], cq[q]);
+                d[c] = __fadd_rn(d[c], __fmul_rn(df, df));
+              }
             }
           }
         }
@@ -2046,6 +2057,120 @@ __device__ void kmeans_part(const gfs_consumer& k, float* smem, const uint8_t* d
   }
 }
 
+// Kmeans through a per-warp shared-memory stage (the K1 TMA ring, idle between greads): a
+// warp loads its 32 points with coalesced 16-byte loads, all in flight at once, decodes them
+// into rows rotated by the point index (feature f of point p at column (f + p) mod D, so
+// the 32 lanes reading "their" feature j hit distinct banks), then runs the distance and
+// accumulation passes out of shared memory.  One memory round trip per 32 points instead of
+// one per feature group; the arithmetic and its order are those of kmeans_part.
+__host__ __device__ inline bool kmeans_staged_fits(const gfs_consumer& k, int bs) {
+  return (int64_t)(bs / 32) * 32 * k.cols * 4 <= TMA_NST * TMA_CH;
+}
+
+template <int BS>
+__device__ void kmeans_part_staged(const gfs_consumer& k, float* smem, const uint8_t* data, int64_t np,
+                                   float* ring) {
+  const int K = k.k;
+  const int D = (int)k.cols;
+  const int q4 = D >> 2;  // 16-byte vectors per point
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int W = BS / 32;
+  const bool wacc = kmeans_warp_acc(k, BS);
+  const float* cent = smem;
+  float* acc = smem + K * D + (wacc ? warp * K * D : 0);
+  unsigned* cnt = (unsigned*)(smem + K * D + (wacc ? W : 1) * K * D) + (wacc ? warp * K : 0);
+  float* stg = ring + (int64_t)warp * 32 * D;
+  const float* prow = stg + lane * D;
+  const int rot = lane % D;
+  for (int64_t pb = (int64_t)warp * 32; pb < np; pb += BS) {
+    const int64_t p = pb + lane;
+    const bool valid = p < np;
+    const int nq = (int)min((int64_t)32, np - pb) * q4;
+    const uint4* src = (const uint4*)(data + pb * (int64_t)D * 4);
+    __syncwarp();  // the previous step's reads of the stage are done
+    for (int q0 = 0; q0 < nq; q0 += 32 * 8) {
+      uint4 u[8];
+#pragma unroll
+      for (int i = 0; i < 8; i++) {
+        const int q = q0 + lane + 32 * i;
+        if (q < nq) u[i] = __ldcg(src + q);
+      }
+#pragma unroll
+      for (int i = 0; i < 8; i++) {
+        const int q = q0 + lane + 32 * i;
+        if (q < nq) {
+          const int pp = q / q4, f0 = (q - pp * q4) * 4;
+          float* row = stg + pp * D;
+          int col = f0 + pp % D;
+          if (col >= D) col -= D;
+          const float v4[4] = {decode_f32(u[i].x), decode_f32(u[i].y), decode_f32(u[i].z), decode_f32(u[i].w)};
+#pragma unroll
+          for (int r = 0; r < 4; r++) {
+            row[col] = v4[r];
+            if (++col == D) col = 0;
+          }
+        }
+      }
+    }
+    __syncwarp();
+    int best = 0;
+    if (valid) {
+      float d[GFS_KMEANS_MAX_K];
+#pragma unroll
+      for (int c = 0; c < GFS_KMEANS_MAX_K; c++) d[c] = 0.f;
+      int col = rot;
+      for (int j = 0; j < D; j += 4) {
+        float v[4];
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          v[q] = prow[col];
+          if (++col == D) col = 0;
+        }
+#pragma unroll
+        for (int c = 0; c < GFS_KMEANS_MAX_K; c++) {
+          if (c < K) {
+            const float4 cv = *(const float4*)(cent + c * D + j);
+            const float cq[4] = {cv.x, cv.y, cv.z, cv.w};
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+              const float df = __fsub_rn(v[q], cq[q]);
+              d[c] = __fadd_rn(d[c], __fmul_rn(df, df));
+            }
+          }
+        }
+      }
+      float bd = d[0];
+#pragma unroll
+      for (int c = 1; c < GFS_KMEANS_MAX_K; c++)
+        if (c < K && d[c] < bd) { bd = d[c]; best = c; }
+    }
+    float* row = acc + best * D;
+    if (wacc) {
+      for (int c = 0; c < K; c++) {
+        const unsigned m = __ballot_sync(0xffffffffu, valid && best == c);
+        if (lane == 0) cnt[c] += __popc(m);
+      }
+      // lane L adds feature (L + t) mod D in step t: 32 distinct accumulator words per step;
+      // that feature sits at stage column (L + t + L) mod D of the lane's row
+      int j = lane % D, sc = (2 * lane) % D;
+      for (int t = 0; t < D; t++) {
+        if (valid) row[j] += prow[sc];
+        __syncwarp();
+        if (++j == D) j = 0;
+        if (++sc == D) sc = 0;
+      }
+    } else if (valid) {
+      atomicAdd(&cnt[best], 1u);
+      int j = lane % D, sc = (2 * lane) % D;
+      for (int t = 0; t < D; t++) {
+        atomicAdd(&row[j], prow[sc]);
+        if (++j == D) j = 0;
+        if (++sc == D) sc = 0;
+      }
+    }
+  }
+}
+
 // All threads, once per launch before the first TB: zero / load the consumer's shared state.
 __device__ void consume_init(const DevCtx& c, float* smem) {
   const gfs_consumer& k = c.cons;
@@ -2092,7 +2217,10 @@ __device__ void consume(const DevCtx& c, float* smem, const uint8_t* data, int64
     gemvt_part(k, smem, (const uint4*)data, n >> 2, file_off >> 2, tid, BS);
     gemv_part<BS>(k, (const uint4*)data, n >> 2, file_off >> 2);
   } else if (k.kind == GFS_CONSUME_KMEANS_F32) {
-    kmeans_part<BS>(k, smem, data, n / (k.cols * 4));
+    if (c.tma && kmeans_staged_fits(k, BS))  // the K1 ring is free between greads
+      kmeans_part_staged<BS>(k, smem, data, n / (k.cols * 4), (float*)((uint8_t*)smem + c.tma_off));
+    else
+      kmeans_part<BS>(k, smem, data, n / (k.cols * 4));
   }
 }
 

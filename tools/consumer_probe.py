@@ -43,6 +43,9 @@ def main():
                                 y=torch.zeros(total // 4 // cols, device="cuda"), cols=cols)
     variants["gemvt"] = Consumer("gemvt_f32", x2=torch.rand(total // 4 // cols, device="cuda"),
                                  y2=torch.zeros(cols, device="cuda"), cols=cols)
+    only = os.environ.get("GFS_PROBE_ONLY")  # one variant (for ncu: warm-up launch, then the timed one)
+    if only:
+        variants = {only: variants[only]}
     with GpuFS(cfg, max_request_bytes=64 * KiB) as fs:
         fs.gopen(path, content_id=0)
         for name, cons in variants.items():
