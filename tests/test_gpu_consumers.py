@@ -178,3 +178,44 @@ def test_consumer_validation_is_loud(setup):
         fs.run(table, 64 * KiB, dst, consumer=Consumer("kmeans_f32", x=C, y=C, out=C, cols=12, k=2))
     with pytest.raises(GfsError):  # GEMVT without its vectors
         fs.run(table, 64 * KiB, dst, consumer=Consumer("gemvt_f32", cols=1024))
+
+
+@pytest.mark.parametrize("cta_threads", [128, 256, 512])
+@pytest.mark.parametrize("D,K", [(16, 5), (32, 8)])
+def test_kmeans_staged_and_direct_paths_agree(setup, D, K, cta_threads):
+    """The kmeans consumer runs through the per-warp shared-memory stage (K1 ring, TMA K1) or
+    straight from the user buffer (LDG K1, or a stage that does not fit): counts exact
+    against numpy on both, sums within rtol 1e-4 of each other (CTAs flush their partial sums
+    with global float atomics, so the cross-CTA order is free)."""
+    import torch
+    from paper_2109_05366_b200.runtime import Consumer, GpuFS
+    _fs, table, _dst, host, size = setup
+    P = decode(host.view("<u4")).reshape(-1, D)
+    cent = P[np.linspace(0, P.shape[0] - 1, K).astype(np.int64)].copy()
+    d = np.zeros((K, P.shape[0]), dtype=np.float32)
+    for c in range(K):
+        for j in range(D):
+            df = P[:, j] - cent[c, j]
+            d[c] = d[c] + df * df
+    want_counts = np.bincount(np.argmin(d, axis=0), minlength=K).tolist()
+    got = {}
+    for k1 in ("tma", "ldg"):
+        cfg = ExperimentConfig({"gpufs.cache_bytes": 8 * MiB, "gpufs.prefetch_bytes": 60 * KiB,
+                                "gpufs.policy": "per-tb-lra", "gpu.sm_count": 8,
+                                "io.readahead": "adaptive", "io.dir": "/dev/shm/gfs_test",
+                                "gpu.k1_copy": k1, "gpu.cta_threads": cta_threads})
+        with GpuFS(cfg) as fs:
+            fs.gopen(_synth_path(size), content_id=3)
+            dst = torch.empty(size, dtype=torch.uint8, device="cuda")
+            sums = torch.zeros(K, D, dtype=torch.float32, device="cuda")
+            counts = torch.zeros(K, dtype=torch.int64, device="cuda")
+            fs.run(table, 64 * KiB, dst, consumer=Consumer("kmeans_f32", x=torch.from_numpy(cent).cuda(),
+                                                           y=sums, out=counts, cols=D, k=K))
+            assert counts.cpu().numpy().tolist() == want_counts, (k1, cta_threads)
+            got[k1] = sums.cpu().numpy()
+    assert np.allclose(got["tma"], got["ldg"], rtol=1e-4)
+
+
+def _synth_path(size):
+    from paper_2109_05366_b200.runtime import ensure_synthetic
+    return ensure_synthetic("/dev/shm/gfs_test", 3, size)
