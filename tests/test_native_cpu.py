@@ -125,7 +125,7 @@ def test_checksum_law_python_vs_oracle():
 def test_auto_transfer_and_first_window_rules(monkeypatch, tmp_path):
     """auto: tmpfs + adaptive -> mapped_dma, tmpfs + static -> mapped, disk -> bounce,
     never a copy-engine mode under a kernel profiler; the first copy-engine window is the
-    whole cap when TBs outnumber resident slots, <= half a stride otherwise."""
+    whole cap when TBs outnumber resident slots, the largest power of two below a stride otherwise."""
     from paper_2109_05366_b200 import config as gcfg
     monkeypatch.delenv("GFS_PROFILER", raising=False)
     for k in [k for k in os.environ if "INJECTION" in k]:
@@ -139,7 +139,10 @@ def test_auto_transfer_and_first_window_rules(monkeypatch, tmp_path):
     assert ExperimentConfig({**base, "io.readahead": "static"}).transfer() == "mapped"
     few = ExperimentConfig({**base, "io.readahead": "adaptive", "workload.n_tb": 128,
                             "workload.total_bytes": 949485568})
-    assert few.ra_init() == 2 * MiB  # largest power of two <= half of a 7.4 MB stride
+    assert few.ra_init() == 4 * MiB  # largest power of two below a 7.4 MB stride
+    four = ExperimentConfig({**base, "io.readahead": "adaptive", "workload.n_tb": 256,
+                             "workload.file_bytes": 1 << 30})
+    assert four.ra_init() == 2 * MiB  # a 4 MiB stride still gets two windows
     assert ExperimentConfig({**base, "io.readahead": "adaptive", "io.ra_init_bytes": 64 * KiB}).ra_init() == 64 * KiB
     monkeypatch.setenv("GFS_PROFILER", "1")
     assert ExperimentConfig({**base, "io.readahead": "adaptive"}).transfer() == "mapped"
