@@ -1828,11 +1828,18 @@ __host__ __device__ inline bool kmeans_warp_acc(const gfs_consumer& k, int bs) {
 __host__ __device__ inline int64_t consumer_smem_bytes(const gfs_consumer& k, int bs) {
   if ((k.kind == GFS_CONSUME_GEMVT_F32 || k.kind == GFS_CONSUME_BICG_F32) && k.cols <= GEMVT_SMEM_COLS)
     return k.cols * 4;
-  if (k.kind == GFS_CONSUME_KMEANS_F32) {
+  if (k.kind == GFS_CONSUME_KMEANS_F32) {  // + the centroids transposed, [cols][k rounded to 4]
     const int64_t w = bs / 32, kd = (int64_t)k.k * k.cols;
-    return kmeans_warp_acc(k, bs) ? (1 + w) * kd * 4 + w * k.k * 4 : 2 * kd * 4 + k.k * 4;
+    const int64_t base = kmeans_warp_acc(k, bs) ? (1 + w) * kd * 4 + w * k.k * 4 : 2 * kd * 4 + k.k * 4;
+    return (base + 15) / 16 * 16 + (int64_t)k.cols * ((k.k + 3) / 4 * 4) * 4;
   }
   return 0;
+}
+
+// Float offset of the transposed centroid copy in the kmeans consumer's shared memory.
+__host__ __device__ inline int64_t kmeans_ct_off(const gfs_consumer& k, int bs) {
+  const int64_t kp4 = (int64_t)k.cols * ((k.k + 3) / 4 * 4) * 4;
+  return (consumer_smem_bytes(k, bs) - kp4) / 4;
 }
 
 // Where the K1 stage ring starts in dynamic shared memory, and the launch's total.
@@ -2081,6 +2088,8 @@ __device__ void kmeans_part_staged(const gfs_consumer& k, float* smem, const uin
   unsigned* cnt = (unsigned*)(smem + K * D + (wacc ? W : 1) * K * D) + (wacc ? warp * K : 0);
   float* stg = ring + (int64_t)warp * 32 * D;
   const float* prow = stg + lane * D;
+  const int kp = (K + 3) / 4 * 4;
+  const float* ct = smem + kmeans_ct_off(k, BS);
   const int rot = lane % D;
   for (int64_t pb = (int64_t)warp * 32; pb < np; pb += BS) {
     const int64_t p = pb + lane;
@@ -2115,34 +2124,35 @@ __device__ void kmeans_part_staged(const gfs_consumer& k, float* smem, const uin
     __syncwarp();
     int best = 0;
     if (valid) {
-      float d[GFS_KMEANS_MAX_K];
-#pragma unroll
-      for (int c = 0; c < GFS_KMEANS_MAX_K; c++) d[c] = 0.f;
-      int col = rot;
-      for (int j = 0; j < D; j += 4) {
-        float v[4];
-#pragma unroll
-        for (int q = 0; q < 4; q++) {
-          v[q] = prow[col];
+      // four centroids per sweep over the features (one broadcast 16-byte load of their
+      // feature j from the transposed copy, four independent chains), features in order
+      float bd = 0.f;
+      for (int c0 = 0; c0 < K; c0 += 4) {
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+        int col = rot;
+#pragma unroll 4
+        for (int j = 0; j < D; j++) {
+          const float v = prow[col];
           if (++col == D) col = 0;
+          const float4 cv = *(const float4*)(ct + j * kp + c0);
+          float df;
+          df = __fsub_rn(v, cv.x);
+          a0 = __fadd_rn(a0, __fmul_rn(df, df));
+          df = __fsub_rn(v, cv.y);
+          a1 = __fadd_rn(a1, __fmul_rn(df, df));
+          df = __fsub_rn(v, cv.z);
+          a2 = __fadd_rn(a2, __fmul_rn(df, df));
+          df = __fsub_rn(v, cv.w);
+          a3 = __fadd_rn(a3, __fmul_rn(df, df));
         }
+        const float a[4] = {a0, a1, a2, a3};
 #pragma unroll
-        for (int c = 0; c < GFS_KMEANS_MAX_K; c++) {
-          if (c < K) {
-            const float4 cv = *(const float4*)(cent + c * D + j);
-            const float cq[4] = {cv.x, cv.y, cv.z, cv.w};
-#pragma unroll
-            for (int q = 0; q < 4; q++) {
-              const float df = __fsub_rn(v[q], cq[q]);
-              d[c] = __fadd_rn(d[c], __fmul_rn(df, df));
-            }
+        for (int i = 0; i < 4; i++)  // first minimum wins, as in kmeans_part
+          if (c0 + i < K && (c0 + i == 0 || a[i] < bd)) {
+            bd = a[i];
+            best = c0 + i;
           }
-        }
       }
-      float bd = d[0];
-#pragma unroll
-      for (int c = 1; c < GFS_KMEANS_MAX_K; c++)
-        if (c < K && d[c] < bd) { bd = d[c]; best = c; }
     }
     float* row = acc + best * D;
     if (wacc) {
@@ -2177,8 +2187,16 @@ __device__ void consume_init(const DevCtx& c, float* smem) {
   const int64_t n = consumer_smem_bytes(k, blockDim.x) / 4;
   if (n == 0) return;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) smem[i] = 0.f;
-  if (k.kind == GFS_CONSUME_KMEANS_F32)
+  if (k.kind == GFS_CONSUME_KMEANS_F32) {
+    __syncthreads();  // the zeroing above used another thread -> index mapping
     for (int64_t i = threadIdx.x; i < (int64_t)k.k * k.cols; i += blockDim.x) smem[i] = k.x[i];
+    const int kp = (k.k + 3) / 4 * 4;  // transposed copy, zero-padded centroids
+    float* ct = smem + kmeans_ct_off(k, blockDim.x);
+    for (int64_t i = threadIdx.x; i < (int64_t)k.cols * kp; i += blockDim.x) {
+      const int64_t j = i / kp, c = i - j * kp;
+      ct[i] = c < k.k ? k.x[c * k.cols + j] : 0.f;
+    }
+  }
   __syncthreads();
 }
 
