@@ -1,6 +1,7 @@
 """Cache-hit throughput: every TB reads its stride twice in one program (file < cache); the
 second pass is served from the HBM page cache.  Prints the device time of one pass and of
-the two-pass program, and the hit-pass rate.  Not a benchmark of record.
+the two-pass program, and the extra time the hit pass adds (it overlaps other TBs' cold
+windows, so it is not an isolated hit-copy rate).  Not a benchmark of record.
 
     python tools/hit_probe.py [--size-gib 4] [--n-tb 1024] [--request-kib 64]
 """
@@ -47,8 +48,11 @@ def main():
             r = fs.run(table, req, dst)
             out[name] = {"ms": r.stats["kernel_ns"] / 1e6, "pc_hits": r.stats["pc_hits"],
                          "mism": r.stats["word_mismatches"]}
+    # the second pass of early TBs overlaps other TBs' cold windows, so this is the extra
+    # device time the hits cost the whole program, not an isolated hit-copy rate
     hit_s = (out["twice"]["ms"] - out["once"]["ms"]) / 1e3
-    out["hit_pass_gbps"] = round(size / hit_s / 1e9, 1) if hit_s > 0 else None
+    out["hit_pass_extra_ms"] = round(hit_s * 1e3, 3)
+    out["hit_bytes_per_extra_s_gbps"] = round(size / hit_s / 1e9, 1) if hit_s > 0 else None
     out["config"] = {"size": size, "n_tb": a.n_tb, "request": req, "transfer": cfg.transfer()}
     print(json.dumps(out))
 
