@@ -379,6 +379,14 @@ def peaks() -> dict:
     return {"hbm_gbs": 6650.0, "fallback": True}
 
 
+def workload_label(size: int, cfg) -> str:
+    """config.workload: configs[1] at its own size, else what the run actually read."""
+    cache = cfg["gpufs.cache_bytes"]
+    rel = "cache < file" if cache < size else ("cache = file" if cache == size else "cache > file")
+    tag = " (configs[1])" if size == 16 * GiB and cache < size else " (configs[1] shape, resized)"
+    return f"sequential strided gread, {size / GiB:g} GiB/GPU, {rel}{tag}"
+
+
 # ------------------------------------------------------------------ reference arm
 
 def reference_main(args, dist: Dist) -> None:
@@ -401,7 +409,7 @@ def reference_main(args, dist: Dist) -> None:
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(secs / len(runs) * 1e3, 3),
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
-           "data": "synthetic", "config": {"workload": "sequential strided gread, 16 GiB/GPU, cache < file (configs[1]), whole workload per step",
+           "data": "synthetic", "config": {"workload": workload_label(size, cfg) + ", whole workload per step",
                                            "sample_bytes": sample},
            "cpu_baseline": {"value": v, "unit": "GB/s", "cores": threads, "kind": "port",
                             "sample": runs[0]["sample"]},
@@ -470,7 +478,7 @@ def main() -> None:
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
         "data": "synthetic",
-        "config": {"workload": "sequential strided gread, 16 GiB/GPU, cache < file (configs[1])",
+        "config": {"workload": workload_label(size, cfg),
                    "file_bytes": cfg["workload.file_bytes"], "bytes_per_gpu": size,
                    "n_tb": cfg["workload.n_tb"], "stride": size // cfg["workload.n_tb"],
                    "request": cfg["workload.request_bytes"], "page": cfg["gpufs.page_size"],
@@ -479,7 +487,7 @@ def main() -> None:
                    "ra_max": cfg.ra_max(), "transfer": cfg.transfer(),
                    "io_workers": cfg.io_workers(), "resident_tbs": cfg.resident_limit(),
                    "resident_ctas": res["ctas"], "storage": f"tmpfs {cfg['io.dir']} O_DIRECT (ramfs)",
-                   "l2": "inputs 16 GiB/GPU >> 126 MB L2; cold GPU page cache every step",
+                   "l2": f"inputs {size / GiB:g} GiB/GPU >> 126 MB L2; cold GPU page cache every step",
                    "parallelism": f"{dist.world} GPU shard(s), no data-path collective"},
         "per_gpu_gbps": round(per_gpu, 3),
         "roofline": {"bound": "pcie_h2d" if (h2d and (not stor or h2d <= stor)) else "storage",
