@@ -59,7 +59,11 @@ def random_case(k: int):
     return cfg, progs, request
 
 
-@pytest.mark.parametrize("k", range(N_CASES))
+def _case_id(k: int) -> str:
+    return f"{k}-{TRANSFERS[k % len(TRANSFERS)]}-{('tma', 'ldg')[(k // len(TRANSFERS)) % 2]}"
+
+
+@pytest.mark.parametrize("k", range(N_CASES), ids=_case_id)
 def test_random_multisegment_programs_full_residency(k):
     import torch
     from paper_2109_05366_b200.runtime import GpuFS, ensure_synthetic
