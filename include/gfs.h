@@ -223,6 +223,12 @@ int gfs_abi_version(void);
 int gfs_stat_count(void);
 const char* gfs_stat_name(int i);
 int gfs_resident_ctas(gfs_ctx* ctx);
+/* the transfer this context uses: gfs_create probes whether copy-engine streams can make
+ * progress while the persistent kernel runs (they cannot when CUDA_DEVICE_MAX_CONNECTIONS
+ * was too small when CUDA started) and otherwise falls back to the SM-pull sibling
+ * (mapped_dma / mapped_hybrid -> mapped, dma -> bounce); *downgraded_from = the requested
+ * transfer then, else -1 */
+int gfs_transfer(gfs_ctx* ctx, int* transfer, int* downgraded_from);
 
 #ifdef __cplusplus
 }

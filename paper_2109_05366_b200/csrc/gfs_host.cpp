@@ -42,6 +42,8 @@
 namespace gfs {
 cudaError_t launch_gread(const DevCtx& c, int cta_threads, cudaStream_t st);
 cudaError_t occupancy_gread(int cta_threads, int* blocks_per_sm);
+cudaError_t launch_queue_probe(const unsigned long long* flags, int n, uint64_t timeout_ns, int* ok,
+                               cudaStream_t st);
 int64_t gread_tma_offset(const gfs_consumer& k, int cta_threads);
 cudaError_t launch_checksum(const void* buf, uint64_t nbytes, uint64_t word_base,
                             unsigned long long* out, int sms, cudaStream_t st);
@@ -256,6 +258,10 @@ struct gfs_ctx {
   std::atomic<uint64_t> w_pos[256];
   std::atomic<int> w_phase[256];
   bool has_run = false;
+  // a run whose kernel never finished leaves the device and the daemon unusable: later
+  // calls fail fast instead of timing out against workers parked on stale positions
+  bool poisoned = false;
+  int downgraded_from = -1;  // copy-engine transfer replaced by its SM-pull sibling (queue probe)
   // driver entry point resolved through cudart (libgfs does not link libcuda, so it
   // loads on machines without a driver; CUDA calls then fail loudly)
   CUresult (*write_value64)(CUstream, CUdeviceptr, cuuint64_t, unsigned int) = nullptr;
@@ -489,6 +495,29 @@ static void stop_workers(gfs_ctx* ctx) {
   ctx->workers.clear();
 }
 
+// After a device error some ring positions were reserved but never written (rpc_submit
+// gave up) and some bounce buffers were never released: workers stay parked on them and the
+// next launch, whose ring base is the served count, would write positions nobody waits for.
+// Restart the daemon from the served count with a clean ring and free buffers.
+static void reset_daemon(gfs_ctx* ctx) {
+  stop_workers(ctx);
+  for (auto s : ctx->worker_streams)
+    if (s) cudaStreamSynchronize(s);
+  for (auto s : ctx->bell_streams)
+    if (s) cudaStreamSynchronize(s);
+  cudaGetLastError();
+  const uint64_t served = __atomic_load_n(ctx->h_served, __ATOMIC_ACQUIRE);
+  memset(ctx->h_ring, 0, (size_t)ctx->ring_size * sizeof(RpcReq));
+  memset(ctx->h_resp, 0, (size_t)ctx->n_ctas * sizeof(RpcResp));
+  if (ctx->h_release) memset(ctx->h_release, 0, ctx->bounce_last.size() * 4);
+  std::fill(ctx->bounce_last.begin(), ctx->bounce_last.end(), 0u);
+  if (ctx->d_doorbell) cudaMemset(ctx->d_doorbell, 0, (size_t)ctx->n_ctas * 8);
+  if (ctx->d_landed) cudaMemset(ctx->d_landed, 0, (size_t)ctx->n_ctas * ctx->landing_halves * 8);
+  ctx->req_head.store(served);
+  ctx->stop.store(false);
+  for (int w = 0; w < ctx->cfg.io_workers; w++) ctx->workers.emplace_back(worker_main, ctx, w);
+}
+
 // ------------------------------------------------------------------- lifecycle
 
 static void free_all(gfs_ctx* ctx) {
@@ -598,6 +627,65 @@ extern "C" int gfs_create(const gfs_config* cfg_in, gfs_ctx** out) {
   TRY(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
   TRY(cudaEventCreate(&ctx->ev0));
   TRY(cudaEventCreate(&ctx->ev1));
+  if (cfg.transfer == GFS_XFER_DMA || cfg.transfer == GFS_XFER_MAPPED ||
+      cfg.transfer == GFS_XFER_MAPPED_HYBRID) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    TRY(cudaGetDriverEntryPoint("cuStreamWriteValue64", &fn, cudaEnableDefault, &qr));
+    if (!fn || qr != cudaDriverEntryPointSuccess)
+      return bail(fail(GFS_ECUDA, "cuStreamWriteValue64 unavailable (stream memory operations)"));
+    ctx->write_value64 = (CUresult(*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int))fn;
+    // a few copy streams shared by the workers (streams are thread-safe): every extra
+    // stream risks sharing a hardware queue with the persistent kernel's stream
+    int nstreams = 2;
+    if (const char* e = getenv("GFS_COPY_STREAMS")) nstreams = std::max(1, std::min(16, atoi(e)));  // experiments
+    ctx->worker_streams.resize((size_t)std::min(cfg.io_workers, nstreams), nullptr);
+    for (auto& s : ctx->worker_streams) TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    ctx->bell_streams.resize((size_t)std::min(cfg.io_workers, nstreams), nullptr);
+    for (auto& s : ctx->bell_streams) TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    // Copy-engine transfers complete while the persistent kernel runs: their streams must
+    // not share a hardware queue with the kernel's stream (CUDA_DEVICE_MAX_CONNECTIONS too
+    // small, or CUDA initialised before the package could raise it).  Probe it: a kernel on
+    // the run stream waits (bounded) for one value written by each copy / doorbell stream.
+    // If any write queues behind the kernel, fall back to the SM-pull transfer that moves
+    // the same bytes (mapped_dma / mapped_hybrid -> mapped, dma -> bounce).
+    std::vector<cudaStream_t> probe(ctx->worker_streams);
+    probe.insert(probe.end(), ctx->bell_streams.begin(), ctx->bell_streams.end());
+    unsigned long long* d_flags = nullptr;
+    int* d_ok = nullptr;
+    TRY(cudaMalloc(&d_flags, probe.size() * 8 + 8));
+    d_ok = (int*)(d_flags + probe.size());
+    TRY(cudaMemsetAsync(d_flags, 0, probe.size() * 8 + 8, ctx->stream));
+    TRY(launch_queue_probe(d_flags, (int)probe.size(), 500ull * 1000000ull, d_ok, ctx->stream));
+    for (size_t i = 0; i < probe.size(); i++) {
+      if (ctx->write_value64((CUstream)probe[i], (CUdeviceptr)(d_flags + i), 1, 0) != CUDA_SUCCESS) {
+        cudaFree(d_flags);
+        return bail(fail(GFS_ECUDA, "cuStreamWriteValue64 failed on a copy stream"));
+      }
+      cudaStreamQuery(probe[i]);
+    }
+    TRY(cudaStreamSynchronize(ctx->stream));
+    int ok = 0;
+    TRY(cudaMemcpy(&ok, d_ok, 4, cudaMemcpyDeviceToHost));
+    TRY(cudaDeviceSynchronize());
+    cudaFree(d_flags);
+    if (!ok) {
+      const int was = cfg.transfer;
+      cfg.transfer = was == GFS_XFER_DMA ? GFS_XFER_BOUNCE : GFS_XFER_MAPPED_ZC;
+      ctx->cfg.transfer = cfg.transfer;
+      ctx->downgraded_from = was;
+      for (auto s : ctx->worker_streams) cudaStreamDestroy(s);
+      for (auto s : ctx->bell_streams) cudaStreamDestroy(s);
+      ctx->worker_streams.clear();
+      ctx->bell_streams.clear();
+      ctx->write_value64 = nullptr;
+      const char* mc = getenv("CUDA_DEVICE_MAX_CONNECTIONS");
+      fprintf(stderr,
+              "libgfs: copy streams share a hardware queue with the kernel stream "
+              "(CUDA_DEVICE_MAX_CONNECTIONS=%s when CUDA started?): transfer %d -> %d (SM pull)\n",
+              mc ? mc : "unset", was, cfg.transfer);
+    }
+  }
   if (!cfg.raw_mode) {
     TRY(cudaMalloc(&ctx->d_frames, (size_t)(nframes * cfg.page_size)));
     TRY(cudaMalloc(&ctx->d_fkey, (size_t)nframes * 8));
@@ -655,20 +743,6 @@ extern "C" int gfs_create(const gfs_config* cfg_in, gfs_ctx** out) {
     TRY(cudaMemset(ctx->d_landed, 0, (size_t)ctx->n_ctas * ctx->landing_halves * 8));
     TRY(cudaMalloc(&ctx->d_doorbell, (size_t)ctx->n_ctas * 8));
     TRY(cudaMemset(ctx->d_doorbell, 0, (size_t)ctx->n_ctas * 8));
-    void* fn = nullptr;
-    cudaDriverEntryPointQueryResult qr;
-    TRY(cudaGetDriverEntryPoint("cuStreamWriteValue64", &fn, cudaEnableDefault, &qr));
-    if (!fn || qr != cudaDriverEntryPointSuccess)
-      return bail(fail(GFS_ECUDA, "cuStreamWriteValue64 unavailable (stream memory operations)"));
-    ctx->write_value64 = (CUresult(*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int))fn;
-    // a few copy streams shared by the workers (streams are thread-safe): every extra
-    // stream risks sharing a hardware queue with the persistent kernel's stream
-    int nstreams = 2;
-    if (const char* e = getenv("GFS_COPY_STREAMS")) nstreams = std::max(1, std::min(16, atoi(e)));  // experiments
-    ctx->worker_streams.resize((size_t)std::min(cfg.io_workers, nstreams), nullptr);
-    for (auto& s : ctx->worker_streams) TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    ctx->bell_streams.resize((size_t)std::min(cfg.io_workers, nstreams), nullptr);
-    for (auto& s : ctx->bell_streams) TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     ctx->bell_ev.resize((size_t)cfg.io_workers, nullptr);
     for (auto& ev : ctx->bell_ev) TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   }
@@ -698,6 +772,13 @@ extern "C" void gfs_destroy(gfs_ctx* ctx) {
 }
 
 extern "C" int gfs_resident_ctas(gfs_ctx* ctx) { return ctx ? ctx->n_ctas : 0; }
+
+extern "C" int gfs_transfer(gfs_ctx* ctx, int* transfer, int* downgraded_from) {
+  if (!ctx || !transfer) return fail(GFS_EINVAL, "gfs_transfer: null argument");
+  *transfer = ctx->cfg.transfer;
+  if (downgraded_from) *downgraded_from = ctx->downgraded_from;
+  return GFS_OK;
+}
 
 // ------------------------------------------------------------------- files
 
@@ -871,6 +952,8 @@ extern "C" int gfs_run_consume(gfs_ctx* ctx, const gfs_program* prog, void* dst,
                                const gfs_consumer* cons, gfs_stats* out) {
   const uint64_t w0 = now_ns();
   if (!ctx || !prog || !out) return fail(GFS_EINVAL, "gfs_run: null argument");
+  if (ctx->poisoned)
+    return fail(GFS_ESTATE, "context unusable: an earlier run's kernel never finished (destroy it)");
   int rc = validate_program(ctx, prog, dst_bytes, dst != nullptr);
   if (rc) return rc;
   if ((rc = validate_consumer(cons, prog, dst != nullptr))) return rc;
@@ -1021,8 +1104,14 @@ extern "C" int gfs_run_consume(gfs_ctx* ctx, const gfs_program* prog, void* dst,
   for (;;) {
     cudaError_t q = cudaStreamQuery(ctx->stream);
     if (q == cudaSuccess) break;
-    if (q != cudaErrorNotReady) return fail(GFS_ECUDA, "gread kernel failed: %s", cudaGetErrorString(q));
-    if (now_ns() > deadline) return fail(GFS_ETIMEDOUT, "gread kernel did not finish in 600 s");
+    if (q != cudaErrorNotReady) {
+      ctx->poisoned = true;  // sticky CUDA error: the context is gone
+      return fail(GFS_ECUDA, "gread kernel failed: %s", cudaGetErrorString(q));
+    }
+    if (now_ns() > deadline) {
+      ctx->poisoned = true;
+      return fail(GFS_ETIMEDOUT, "gread kernel did not finish in 600 s");
+    }
     // the daemon threads own the host cores while the kernel runs: poll lazily
     std::this_thread::sleep_for(std::chrono::microseconds(500));
   }
@@ -1078,6 +1167,7 @@ extern "C" int gfs_run_consume(gfs_ctx* ctx, const gfs_program* prog, void* dst,
         diag += b;
       }
     }
+    reset_daemon(ctx);  // the next run starts from a clean ring
     return fail(g.error == ERR_IO ? GFS_EIO : (g.error == ERR_TIMEOUT ? GFS_ETIMEDOUT : GFS_EDEVICE),
                 "device error %d: %s (info %d, arg %llu)%s%s%s", g.error, what, g.error_info,
                 (unsigned long long)g.error_arg, werr ? "; daemon errno: " : "",

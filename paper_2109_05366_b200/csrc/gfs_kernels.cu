@@ -50,6 +50,13 @@ __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+// refcount pin with acquire semantics: the frame key read after it cannot be satisfied from
+// a line cached before the pin (the key is then read from L2 with __ldcg)
+__device__ __forceinline__ uint32_t atomic_add_acquire_gpu(uint32_t* p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.acquire.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
 __device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -488,7 +495,7 @@ __device__ void release_frame(const DevCtx& c, Smem& s, uint32_t f, uint32_t* pt
   } else {
     s.own_len--;  // it is the newest own frame
   }
-  c.fstate[f] = 0;
+  atomicAnd(&c.fstate[f], ~FR_VALID);  // keep transient readers' pins (refcount bits)
   st_release_gpu(pte, PT_EMPTY);
   while (atomicCAS(&c.g->recycled_lock, 0, 1) != 0) __nanosleep(32);
   __threadfence();
@@ -907,6 +914,9 @@ template <int BS>
 __device__ void pull_span(const DevCtx& c, Smem& s) {
   if (s.pull_n <= 0) return;
   copy_bytes<BS, SRC_SYS>((uint8_t*)span_base(c, s), s.pull_src, s.pull_n);
+  // the landing slot is read next by cp.async.bulk (async proxy): order these generic-proxy
+  // stores before it (each writing thread fences, the barrier below publishes)
+  asm volatile("fence.proxy.async.global;" ::: "memory");
   __syncthreads();  // every load has returned: the buffer may be reused
   if (threadIdx.x == 0) {
     if (s.pull_buf >= 0) {
@@ -1342,8 +1352,11 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
       const int64_t cb = min(TMA_CH, total_b - (int64_t)i * TMA_CH);
       tma_load(ring + st * TMA_CH, srcb + (int64_t)i * TMA_CH, (uint32_t)cb, &s.tma_bar[st]);
     };
-    if (tid == 0)
+    if (tid == 0) {
+      // landing bytes written by the copy engine / generic proxy, read by the async proxy
+      asm volatile("fence.proxy.async.global;" ::: "memory");
       for (int i = 0; i < nch && i < TMA_NST; i++) load(i);
+    }
     for (int i = 0; i < nch; i++) {
       const unsigned long long G = G0 + i;
       const int st = (int)(G % TMA_NST);
@@ -1503,8 +1516,8 @@ __device__ int64_t gread_hits(const DevCtx& c, Smem& s, int64_t fid, int64_t g_p
     if (lane < nmax) {
       const uint32_t e = ld_acquire_gpu(&F.pt[p0 + lane]);
       if (e != PT_EMPTY && e != PT_CLAIMED && !(e & PT_INFLIGHT)) {
-        const uint32_t old = atomicAdd(&c.fstate[e], FR_REF);  // pin against eviction
-        if ((old & FR_VALID) && c.fkey[e] == page_key(fid, p0 + lane)) {
+        const uint32_t old = atomic_add_acquire_gpu(&c.fstate[e], FR_REF);  // pin against eviction
+        if ((old & FR_VALID) && __ldcg(&c.fkey[e]) == page_key(fid, p0 + lane)) {
           ok = true;
           f = e;
         } else {
@@ -1693,8 +1706,8 @@ __device__ int64_t gread(const DevCtx& c, Smem& s, int64_t fid, int64_t offset, 
           }
           continue;
         }
-        uint32_t old = atomicAdd(&c.fstate[e], FR_REF);
-        if ((old & FR_VALID) && c.fkey[e] == key) {
+        uint32_t old = atomic_add_acquire_gpu(&c.fstate[e], FR_REF);
+        if ((old & FR_VALID) && __ldcg(&c.fkey[e]) == key) {
           f = e;
           act = A_HIT;
           ST(pc_hits)++;
@@ -2519,6 +2532,27 @@ cudaError_t launch_gread(const DevCtx& c, int cta_threads, cudaStream_t st) {
 int64_t gread_tma_offset(const gfs_consumer& k, int cta_threads) {
   const int64_t off = tma_ring_offset(k, cta_threads);
   return off + TMA_NST * TMA_CH <= CONS_SMEM_MAX ? off : -1;
+}
+
+// Copy-queue probe (gfs_create): waits, bounded, until each of n flags was written by its
+// copy / doorbell stream while this kernel occupies the run stream.
+__global__ void queue_probe_kernel(const unsigned long long* flags, int n, uint64_t timeout_ns, int* ok) {
+  const uint64_t t0 = globaltimer();
+  for (int i = 0; i < n; i++)
+    while (ld_acquire_sys64(flags + i) != 1ull) {
+      if (globaltimer() - t0 > timeout_ns) {
+        *ok = 0;
+        return;
+      }
+      __nanosleep(1000);
+    }
+  *ok = 1;
+}
+
+cudaError_t launch_queue_probe(const unsigned long long* flags, int n, uint64_t timeout_ns, int* ok,
+                               cudaStream_t st) {
+  queue_probe_kernel<<<1, 1, 0, st>>>(flags, n, timeout_ns, ok);
+  return cudaGetLastError();
 }
 
 cudaError_t occupancy_gread(int cta_threads, int* blocks_per_sm) {

@@ -31,7 +31,7 @@ EXPORTS = ["gfs_create", "gfs_destroy", "gfs_gopen", "gfs_gclose", "gfs_file_siz
            "gfs_log_len", "gfs_log_copy", "gfs_checksum", "gfs_verify_dst", "gfs_gen_file",
            "gfs_last_error", "gfs_abi_version", "gfs_stat_count", "gfs_stat_name",
            "gfs_resident_ctas", "gfs_bench_storage", "gfs_bench_h2d", "gfs_bench_read_memcpy",
-           "gfs_replay", "gfs_gen_file_range"]
+           "gfs_replay", "gfs_gen_file_range", "gfs_transfer"]
 
 
 class GfsConfig(C.Structure):
@@ -102,6 +102,7 @@ def load(path: str = LIB_PATH):
     L.gfs_stat_name.restype = C.c_char_p
     L.gfs_stat_name.argtypes = [i32]
     L.gfs_resident_ctas.argtypes = [vp]
+    L.gfs_transfer.argtypes = [vp, C.POINTER(i32), C.POINTER(i32)]
     dp = C.POINTER(C.c_double)
     L.gfs_bench_storage.argtypes = [C.c_char_p, i64, i64, i32, i64, i32, dp]
     L.gfs_bench_h2d.argtypes = [i32, i64, i32, dp]
@@ -111,7 +112,7 @@ def load(path: str = LIB_PATH):
     for name in ("gfs_create", "gfs_gopen", "gfs_gclose", "gfs_file_size", "gfs_run",
                  "gfs_log_len", "gfs_log_copy", "gfs_checksum", "gfs_verify_dst", "gfs_gen_file",
                  "gfs_bench_storage", "gfs_bench_h2d", "gfs_bench_read_memcpy", "gfs_replay",
-                 "gfs_gen_file_range"):
+                 "gfs_gen_file_range", "gfs_transfer"):
         getattr(L, name).restype = i32
     if L.gfs_abi_version() != ABI_VERSION:
         raise GfsError(f"{path} has ABI {L.gfs_abi_version()}, this package needs {ABI_VERSION}: rebuild it")

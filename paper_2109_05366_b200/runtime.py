@@ -169,6 +169,14 @@ class GpuFS:
     def resident_ctas(self) -> int:
         return self._lib.gfs_resident_ctas(self._h)
 
+    @property
+    def transfer(self) -> str:
+        """The transfer in use (gfs_create may downgrade a copy-engine transfer to its SM-pull
+        sibling when copy streams cannot progress beside the persistent kernel)."""
+        t, was = C.c_int(), C.c_int()
+        native.check(self._lib.gfs_transfer(self._h, C.byref(t), C.byref(was)), "gfs_transfer")
+        return {v: k for k, v in native.TRANSFER.items()}[t.value]
+
     # -- files ----------------------------------------------------------------
 
     def gopen(self, path: str, flags: int = O_RDONLY, content_id: int = -1) -> int:
