@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define GFS_ABI_VERSION 2  /* 2: gfs_config grew timeline / k1_tma / numa_pin / lookahead / async_ra */
+#define GFS_ABI_VERSION 3  /* 3: io.readahead ondemand law, gfs_config.ra_clamp replaces async_ra */
 
 enum { GFS_OK = 0, GFS_EINVAL = -1, GFS_ECUDA = -2, GFS_EIO = -3, GFS_ENOMEM = -4,
        GFS_ETIMEDOUT = -5, GFS_EDEVICE = -6, GFS_ESTATE = -7 };
@@ -33,8 +33,14 @@ enum { GFS_OK = 0, GFS_EINVAL = -1, GFS_ECUDA = -2, GFS_EIO = -3, GFS_ENOMEM = -
 /* gpufs.policy (gpu_cache.py:27-29) */
 enum { GFS_POLICY_GLOBAL_LRU = 0, GFS_POLICY_PER_TB_LRA = 1 };
 /* io.readahead: static = the reference span page+prefetch (prefetcher.py:13-25);
- * adaptive = window doubling on sequential continuation up to ra_max_bytes */
-enum { GFS_RA_STATIC = 0, GFS_RA_ADAPTIVE = 1 };
+ * doubling = the span doubles on every sequential continuation up to ra_max_bytes;
+ * ondemand ("adaptive" in the Python config) = the reference's Linux-style ondemand law
+ *   (HostOs._decide, host_os.py:106-152) per TB stream: a cold sequential request of n pages
+ *   opens max(n, min(4n, ra_max)) pages, the tail asynchronous with a marker; a request
+ *   hitting the marker requests the next window (double, capped) asynchronously */
+enum { GFS_RA_STATIC = 0, GFS_RA_DOUBLING = 1, GFS_RA_ONDEMAND = 2 };
+/* ondemand windows end at the TB's segment end (its stride) or at EOF (the reference) */
+enum { GFS_RA_CLAMP_SEGMENT = 0, GFS_RA_CLAMP_EOF = 1 };
 /* io.transfer: zerocopy = SMs pull the span from per-CTA mapped pinned staging;
  * bounce = the daemon preads into a small (LLC-resident) per-worker pinned pool, the CTA
  *          pulls the whole span into its HBM landing slot at once and releases the buffer;
@@ -63,8 +69,8 @@ typedef struct gfs_config {
   int64_t cache_bytes;     /* gpufs.cache_bytes: frame pool in HBM */
   int64_t prefetch_bytes;  /* gpufs.prefetch_bytes */
   int64_t staging_bytes;   /* rpc.staging_bytes: PCIe batch size (accounting, rpc.py:31-55) */
-  int64_t ra_max_bytes;    /* io.ra_max_bytes: adaptive window cap */
-  int64_t ra_init_bytes;   /* io.ra_init_bytes: adaptive first window (0 = page + prefetch) */
+  int64_t ra_max_bytes;    /* io.ra_max_bytes: readahead window cap (doubling, ondemand) */
+  int64_t ra_init_bytes;   /* io.ra_init_bytes: doubling first window (0 = page + prefetch) */
   int64_t max_request_bytes; /* largest gread request (raw mode sizes staging to it) */
   int32_t policy;          /* GFS_POLICY_* */
   int32_t resident_limit;  /* reference residency (gpu_exec.py:44-50): sets the LRA quota */
@@ -85,8 +91,7 @@ typedef struct gfs_config {
   int32_t numa_pin;        /* io.numa_pin: daemon threads on the CPUs local to the GPU's PCIe root */
   int32_t lookahead;       /* gpu.lookahead: a page batch may run past a page-aligned request to
                               the TB's segment end (the next greads find their bytes delivered) */
-  int32_t async_ra;        /* io.async_readahead: copy-engine transfers submit the next window's
-                              request while the current window is consumed (not with logs) */
+  int32_t ra_clamp;        /* io.ra_clamp: GFS_RA_CLAMP_* (ondemand) */
 } gfs_config;
 
 /* One gread program set (workloads.py:24-31 programs, flattened).

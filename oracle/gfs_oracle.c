@@ -33,10 +33,17 @@
  * buffer -> user buffer, exactly like the device path, so user buffers and
  * checksums can be compared byte-for-byte.
  *
- * Extension beyond the reference (documented in DESIGN.md): readahead mode 1
- * ("adaptive") doubles the RPC span on every sequential continuation up to
- * ra_max_bytes (the ondemand doubling law of host_os.py:124-128), clamped to
- * EOF and to the end of the TB's current segment.
+ * Readahead modes:
+ *   0 static   — request_span, prefetcher.py:13-25 (the reference GPU prefetcher);
+ *   1 doubling — the RPC span doubles on every sequential continuation up to
+ *                ra_max_bytes, clamped to EOF and to the TB's segment end;
+ *   2 ondemand — io.readahead=adaptive: HostOs._decide's Linux ondemand law
+ *                (host_os.py:106-152, _resident_run :88-103) applied per TB stream to
+ *                the gread requests, with the device's two landing halves: the
+ *                synchronous span of a request's missing pages, asynchronous windows
+ *                pending in the other half, adopted as the private buffer when the walk
+ *                reaches them.  Pinned against the reference's own window_history
+ *                (tests/golden/window_*.json, made by tests/golden/make_windows.py).
  */
 #define _GNU_SOURCE
 #include <errno.h>
@@ -132,6 +139,7 @@ static int vec_push(vec_t* a, const int64_t* rec, int width) {
 
 /* frame states */
 enum { F_FREE = 0, F_INFLIGHT = 1, F_VALID = 2 };
+enum { OD_MARKS = 4 }; /* readahead markers remembered per TB stream (the device's bound) */
 
 typedef struct {
   int64_t fid, page;
@@ -148,7 +156,7 @@ struct orc_run_s {
   vec_t deliveries; /* (tb, fid, page) */
   vec_t rpcs;       /* (tb, fid, offset, size) */
   vec_t victims;    /* (tb, fid, page) */
-  vec_t windows;    /* (tb, span) per RPC in adaptive mode */
+  vec_t windows;    /* (tb, span) per RPC in doubling mode; (tb, window bytes) per ondemand decision */
   uint64_t checksum;
 
   /* page cache */
@@ -169,8 +177,26 @@ struct orc_run_s {
   int64_t pb_fid, pb_first, pb_count, pb_filled;
   int32_t* pb_nbytes; /* per entry, 0 = consumed/absent */
   int64_t pb_cap_bytes;
-  /* adaptive readahead state */
+  /* doubling readahead state */
   int64_t ra_win, ra_next_fid, ra_next_page;
+  /* ondemand readahead: the TB's stream (host_os.py ReadaheadState + markers) */
+  int64_t od_fid, od_ws, od_wsize, od_async, od_prev_end;
+  int64_t od_mark[OD_MARKS];
+  long long od_dec_key;
+  int64_t od_run_page, od_run_n;
+  /* the current gread and segment */
+  int64_t g_lo, g_hi, seg_lo, seg_hi;
+  long long seg_ord;
+  /* the two landing halves: a pending window (requested, not adopted) and its bytes */
+  struct {
+    int pending;
+    int64_t fid, page, span, n;
+    uint32_t age;
+  } hp[2];
+  uint32_t hp_age;
+  int span_half;
+  uint8_t* half_mem[2];
+  int64_t staging_pages; /* a landing half / span buffer, in pages (ondemand sync span cap) */
 
   /* data plane */
   uint8_t* frame_mem;
@@ -414,7 +440,7 @@ static void log_rpc(orc_run* r, int tb, int64_t fid, int64_t off, int64_t size) 
   S(rpc_requested_bytes) += size;
 }
 
-/* prefetcher.py:13-25 (+ adaptive extension) */
+/* prefetcher.py:13-25 (+ doubling extension) */
 static int64_t rpc_span(orc_run* r, int tb, int64_t fid, int64_t page, int64_t seg_end) {
   int64_t pg = r->cfg.page_size, fs = r->cfg.file_sizes[fid];
   int64_t off = page * pg;
@@ -422,7 +448,7 @@ static int64_t rpc_span(orc_run* r, int tb, int64_t fid, int64_t page, int64_t s
   int ro = r->cfg.read_only[fid];
   int64_t pf = r->cfg.prefetch_bytes;
   int64_t want = (ro && pf > 0) ? pg + pf : pg;
-  if (r->cfg.readahead == ORC_RA_ADAPTIVE && ro) {
+  if (r->cfg.readahead == ORC_RA_DOUBLING && ro) {
     int64_t base = pg + pf;
     int64_t init = r->cfg.ra_init_bytes < r->cfg.ra_max_bytes ? r->cfg.ra_init_bytes : r->cfg.ra_max_bytes;
     if (init > base) base = init; /* io.ra_init_bytes: a larger first window */
@@ -438,7 +464,7 @@ static int64_t rpc_span(orc_run* r, int tb, int64_t fid, int64_t page, int64_t s
     if (want < pg) want = pg;
   }
   int64_t span = want < fs - off ? want : fs - off;
-  if (r->cfg.readahead == ORC_RA_ADAPTIVE && ro) {
+  if (r->cfg.readahead == ORC_RA_DOUBLING && ro) {
     r->ra_next_fid = fid;
     r->ra_next_page = page + ceil_div(span, pg);
     int64_t rec[2] = {tb, span};
@@ -446,6 +472,217 @@ static int64_t rpc_span(orc_run* r, int tb, int64_t fid, int64_t page, int64_t s
   }
   (void)tb;
   return span;
+}
+
+/* ------------------------------------------------------- ondemand readahead */
+
+static int64_t od_pages(const orc_run* r, int64_t bytes) { return ceil_div(bytes, r->cfg.page_size); }
+
+static int od_pb_has(const orc_run* r, int64_t fid, int64_t page) {
+  int64_t i = page - r->pb_first;
+  return r->pb_count > 0 && fid == r->pb_fid && i >= 0 && i < r->pb_count && r->pb_nbytes[i] > 0;
+}
+
+static int od_in_pending(const orc_run* r, int64_t fid, int64_t p) {
+  for (int h = 0; h < 2; h++)
+    if (r->hp[h].pending && r->hp[h].fid == fid && p >= r->hp[h].page &&
+        p < r->hp[h].page + od_pages(r, r->hp[h].span))
+      return h;
+  return -1;
+}
+
+/* host_os.py:91-92 + in-flight pages: cached, in the private buffer or in a pending
+ * window; page `ex` (the miss being decided, just allocated) is not fetched yet. */
+static int od_resident(const orc_run* r, int64_t fid, int64_t p, int64_t ex) {
+  if (p < 0 || p >= od_pages(r, r->cfg.file_sizes[fid])) return 0;
+  /* segment clamp: the stream sees only its own segment */
+  if (r->cfg.ra_clamp == ORC_CLAMP_SEGMENT && (p < r->seg_lo / r->cfg.page_size || p >= od_pages(r, r->seg_hi)))
+    return 0;
+  if (od_pb_has(r, fid, p) || od_in_pending(r, fid, p) >= 0) return 1;
+  if (p == ex) return 0;
+  return r->pt[fid][p] >= 0;
+}
+
+static int64_t od_limit(const orc_run* r, int64_t fid) {
+  int64_t lim = od_pages(r, r->cfg.file_sizes[fid]);
+  if (r->cfg.ra_clamp == ORC_CLAMP_SEGMENT && od_pages(r, r->seg_hi) < lim) lim = od_pages(r, r->seg_hi);
+  return lim;
+}
+
+/* The current gread as pages [*gs, *ge) and its instance key (segment ordinal, index). */
+static long long od_request(const orc_run* r, int64_t fid, int64_t* gs, int64_t* ge) {
+  int64_t hi = r->g_hi < r->cfg.file_sizes[fid] ? r->g_hi : r->cfg.file_sizes[fid];
+  *gs = r->g_lo / r->cfg.page_size;
+  *ge = od_pages(r, hi);
+  return (r->seg_ord << 32) | (long long)((r->g_lo - r->seg_lo) / r->cfg.request_bytes);
+}
+
+static void od_add_mark(orc_run* r, int64_t page) {
+  for (int i = 0; i < OD_MARKS; i++)
+    if (r->od_mark[i] < 0) {
+      r->od_mark[i] = page;
+      return;
+    }
+  for (int i = 0; i + 1 < OD_MARKS; i++) r->od_mark[i] = r->od_mark[i + 1]; /* drop the oldest */
+  r->od_mark[OD_MARKS - 1] = page;
+}
+
+static void od_reset(orc_run* r, int64_t fid) {
+  r->od_fid = fid;
+  r->od_ws = r->od_wsize = r->od_async = 0;
+  r->od_prev_end = -1;
+  for (int i = 0; i < OD_MARKS; i++) r->od_mark[i] = -1;
+  r->od_dec_key = -1;
+  r->od_run_n = 0;
+}
+
+static int64_t i64max(int64_t a, int64_t b) { return a > b ? a : b; }
+static int64_t i64min(int64_t a, int64_t b) { return a < b ? a : b; }
+
+/* host_os.py:106-152 (HostOs._decide) for the request [gs, ge); _resident_run :88-103.
+ * Returns the window bytes window_history records (0 = none); the asynchronous run goes
+ * to od_run_page / od_run_n. */
+static int64_t od_decide(orc_run* r, int64_t fid, int64_t gs, int64_t ge, int64_t ex) {
+  const int64_t pg = r->cfg.page_size, ra_max = r->cfg.ra_max_bytes / pg;
+  const int64_t lim = od_limit(r, fid), npages = ge - gs, req_end = ge;
+  r->od_run_n = 0;
+  int64_t marker = -1;
+  for (int i = 0; i < OD_MARKS; i++) {
+    int64_t m = r->od_mark[i];
+    if (m >= gs && m < ge) {
+      r->od_mark[i] = -1; /* each marker triggers at most once */
+      if (marker < 0 || m < marker) marker = m;
+    }
+  }
+  if (marker >= 0) {
+    int64_t ns, nz;
+    if (r->od_wsize > 0 && marker == r->od_ws + r->od_wsize - r->od_async) {
+      ns = i64max(r->od_ws + r->od_wsize, req_end);
+      nz = i64min(2 * r->od_wsize, ra_max);
+    } else { /* context recovery: the resident run around the marker */
+      int64_t a = marker, e = marker + 1, np = od_pages(r, r->cfg.file_sizes[fid]);
+      while (marker - a < ra_max && a > 0 && od_resident(r, fid, a - 1, ex)) a--;
+      while (e - marker <= ra_max && e < np && od_resident(r, fid, e, ex)) e++;
+      ns = i64max(e, req_end);
+      nz = i64min(2 * i64max(e - a, 1), ra_max);
+    }
+    nz = i64min(nz, i64max(lim - ns, 0));
+    r->od_prev_end = req_end;
+    if (nz == 0) {
+      r->od_ws = gs;
+      r->od_wsize = r->od_async = 0;
+      return 0;
+    }
+    r->od_ws = ns;
+    r->od_wsize = r->od_async = nz;
+    r->od_run_page = ns;
+    r->od_run_n = nz;
+    od_add_mark(r, ns);
+    return nz * pg;
+  }
+  int seq = gs == 0 || gs == r->od_prev_end || (gs > 0 && od_resident(r, fid, gs - 1, ex));
+  r->od_prev_end = req_end;
+  if (!seq) {
+    r->od_ws = gs;
+    r->od_wsize = r->od_async = 0;
+    return 0;
+  }
+  int64_t w = i64max(npages, i64min(4 * npages, ra_max));
+  w = i64min(w, i64max(lim - gs, npages));
+  r->od_ws = gs;
+  r->od_wsize = w;
+  r->od_async = w - npages;
+  if (r->od_async <= 0) return w * pg;
+  r->od_run_page = req_end;
+  r->od_run_n = r->od_async;
+  od_add_mark(r, req_end);
+  return w * pg;
+}
+
+static void od_decide_once(orc_run* r, int tb, int64_t fid, int64_t ex, int64_t* ge_out) {
+  int64_t gs, ge;
+  long long key = od_request(r, fid, &gs, &ge);
+  *ge_out = ge;
+  if (key == r->od_dec_key) return;
+  r->od_dec_key = key;
+  int64_t w = od_decide(r, fid, gs, ge, ex);
+  if (w > 0) {
+    int64_t rec[2] = {tb, w};
+    vec_push(&r->windows, rec, 2);
+  }
+}
+
+/* A window the TB will not consume: dropped (its transfer was counted at request). */
+static void od_drain(orc_run* r, int h) { r->hp[h].pending = 0; }
+
+/* Landing half for a new span: one without a pending window, the half not holding the
+ * private buffer first (taking the private buffer's half discards its entries), else the
+ * older pending window is dropped.  `avoid`: the half of the span requested alongside. */
+static int od_pick_half(orc_run* r, int avoid) {
+  int a = r->span_half ^ 1, b = r->span_half, h = -1;
+  if (a != avoid && !r->hp[a].pending) h = a;
+  else if (b != avoid && !r->hp[b].pending) h = b;
+  if (h < 0) {
+    for (int k = 0; k < 2; k++)
+      if (k != avoid && (h < 0 || r->hp[k].age < r->hp[h].age)) h = k;
+    od_drain(r, h);
+  }
+  if (h == r->span_half && r->pb_count > 0) pb_discard_all(r);
+  return h;
+}
+
+/* Request `span` bytes at `page` (rpc.py:82-102): the RPC record, the read, the transfer. */
+static int64_t od_request_span(orc_run* r, int tb, int64_t fid, int64_t page, int64_t span, uint8_t* buf) {
+  log_rpc(r, tb, fid, page * r->cfg.page_size, span);
+  int64_t n = source_read(r, fid, page * r->cfg.page_size, span);
+  if (n < 0) return fail(r, "pread failed: %s", strerror(errno)), -1;
+  if (buf && materialized(r)) memcpy(buf, r->staging, (size_t)n);
+  account_transfer(r, n);
+  return n;
+}
+
+static int od_submit_run(orc_run* r, int tb, int64_t fid, int avoid) {
+  if (r->od_run_n <= 0) return 0;
+  const int64_t pg = r->cfg.page_size, fs = r->cfg.file_sizes[fid];
+  int64_t span = r->od_run_n * pg;
+  if (span > fs - r->od_run_page * pg) span = fs - r->od_run_page * pg;
+  r->od_run_n = 0;
+  if (span <= 0) return 0;
+  int h = od_pick_half(r, avoid);
+  int64_t n = od_request_span(r, tb, fid, r->od_run_page, span, r->half_mem[h]);
+  if (n < 0) return -1;
+  r->hp[h].pending = 1;
+  r->hp[h].fid = fid;
+  r->hp[h].page = r->od_run_page;
+  r->hp[h].span = span;
+  r->hp[h].n = n;
+  r->hp[h].age = ++r->hp_age;
+  return 0;
+}
+
+/* Walk position `page` (before its lookup): a marker there fires its request's decision; a
+ * pending window holding the page becomes the private buffer (all its pages). */
+static int od_top(orc_run* r, int tb, int64_t fid, int64_t page) {
+  for (int i = 0; i < OD_MARKS; i++)
+    if (r->od_mark[i] == page) {
+      int64_t ge;
+      od_decide_once(r, tb, fid, -1, &ge);
+      if (od_submit_run(r, tb, fid, -1) < 0) return -1;
+      break;
+    }
+  int h = od_in_pending(r, fid, page);
+  if (h >= 0) {
+    r->hp[h].pending = 0;
+    r->span_half = h;
+    int64_t n = r->hp[h].n;
+    if (n > 0) {
+      pb_fill(r, fid, r->hp[h].page, od_pages(r, n), n);
+      if (r->pb_mem) memcpy(r->pb_mem, r->half_mem[h], (size_t)(n < r->pb_cap_bytes ? n : r->pb_cap_bytes));
+    } else {
+      pb_discard_all(r);
+    }
+  }
+  return 0;
 }
 
 static void deliver(orc_run* r, int tb, int64_t fid, int64_t g_pos, int64_t want, int hit,
@@ -491,6 +728,12 @@ static int64_t gread(orc_run* r, int tb, int64_t fid, int64_t offset, int64_t si
     return n;
   }
   int64_t g_pos = offset, g_end = offset + size;
+  const int od = r->cfg.readahead == ORC_RA_ONDEMAND && r->cfg.read_only[fid];
+  if (r->cfg.readahead == ORC_RA_ONDEMAND) {
+    r->g_lo = offset;
+    r->g_hi = offset + size;
+    if (fid != r->od_fid) od_reset(r, fid); /* a new stream */
+  }
   for (;;) {
     if (g_pos >= g_end || g_pos >= fs) return g_pos - offset;
     int64_t page = g_pos / pg;
@@ -498,6 +741,7 @@ static int64_t gread(orc_run* r, int tb, int64_t fid, int64_t offset, int64_t si
     int64_t want = (g_end < page_end ? g_end : page_end) - g_pos;
     int64_t in_page = g_pos - page * pg;
     uint8_t* d = dst ? dst + (g_pos - offset) : NULL;
+    if (od && od_top(r, tb, fid, page) < 0) return -1;
 
     S(pc_lookups)++;
     int64_t fi = r->pt[fid][page];
@@ -510,6 +754,17 @@ static int64_t gread(orc_run* r, int tb, int64_t fid, int64_t offset, int64_t si
       continue;
     }
     S(pc_misses)++;
+    /* ondemand: the request's decision and its synchronous span are taken on the miss,
+     * before the page's frame is allocated (allocation may evict pages the scan sees) */
+    int64_t od_span = 0;
+    if (od && !od_pb_has(r, fid, page)) {
+      int64_t ge;
+      od_decide_once(r, tb, fid, -1, &ge);
+      int64_t lim = i64min(i64min(ge, page + r->staging_pages), od_pages(r, fs));
+      int64_t q = page + 1;
+      while (q < lim && !od_resident(r, fid, q, -1)) q++;
+      od_span = i64min((q - page) * pg, fs - page * pg);
+    }
     fi = cache_allocate(r, tb, fid, page);
     if (fi < 0) return -1;
     frame_t* f = &r->frames[fi];
@@ -523,9 +778,21 @@ static int64_t gread(orc_run* r, int tb, int64_t fid, int64_t offset, int64_t si
       g_pos += want;
       continue;
     }
-    int64_t span = rpc_span(r, tb, fid, page, seg_end);
-    log_rpc(r, tb, fid, page * pg, span);
-    int64_t n = source_read(r, fid, page * pg, span);
+    int64_t span, n;
+    if (od) { /* the synchronous span planned above, then the decided async run */
+      span = od_span;
+      int hs = od_pick_half(r, -1);
+      log_rpc(r, tb, fid, page * pg, span);
+      if (od_submit_run(r, tb, fid, hs) < 0) return -1;
+      r->span_half = hs;
+    } else {
+      int ph = 0;
+      if (r->cfg.readahead == ORC_RA_ONDEMAND) r->span_half = ph = od_pick_half(r, -1); /* non-RO file */
+      (void)ph;
+      span = rpc_span(r, tb, fid, page, seg_end);
+      log_rpc(r, tb, fid, page * pg, span);
+    }
+    n = source_read(r, fid, page * pg, span);
     if (n < 0) return fail(r, "pread failed: %s", strerror(errno)), -1;
     account_transfer(r, n);
     if (n == 0) { /* gpu_exec.py:207-211 */
@@ -584,10 +851,16 @@ static int setup(orc_run* r) {
     }
   }
   int64_t pb_cap = c->prefetch_bytes;
-  if (c->readahead == ORC_RA_ADAPTIVE && c->ra_max_bytes - c->page_size > pb_cap)
+  if (c->readahead == ORC_RA_DOUBLING && c->ra_max_bytes - c->page_size > pb_cap)
     pb_cap = c->ra_max_bytes - c->page_size;
+  if (c->readahead == ORC_RA_ONDEMAND) { /* a landing half holds a whole window */
+    if (c->ra_max_bytes < c->page_size || c->ra_max_bytes % c->page_size)
+      return fail(r, "ra_max_bytes must be a positive multiple of page_size");
+    pb_cap = i64max(c->ra_max_bytes, c->page_size + c->prefetch_bytes);
+  }
   r->pb_cap_bytes = pb_cap;
-  int64_t max_span = c->page_size + pb_cap;
+  int64_t max_span = c->readahead == ORC_RA_ONDEMAND ? pb_cap : c->page_size + pb_cap;
+  r->staging_pages = max_span / c->page_size;
   r->pb_nbytes = (int32_t*)calloc((size_t)(max_span / c->page_size + 2), sizeof(int32_t));
   if (!r->pb_nbytes) return fail(r, "out of host memory");
   if (materialized(r)) {
@@ -597,6 +870,9 @@ static int setup(orc_run* r) {
     if (posix_memalign((void**)&r->staging, 4096, (size_t)r->staging_cap + 4096))
       return fail(r, "out of host memory");
     if (!c->raw_mode) {
+      if (c->readahead == ORC_RA_ONDEMAND)
+        for (int h = 0; h < 2; h++)
+          if (!(r->half_mem[h] = (uint8_t*)malloc((size_t)max_span))) return fail(r, "out of host memory");
       r->frame_mem = (uint8_t*)malloc((size_t)(r->nframes * c->page_size));
       r->pb_mem = (uint8_t*)malloc((size_t)(pb_cap > 0 ? pb_cap : 1));
       if (!r->frame_mem || !r->pb_mem) return fail(r, "out of host memory for the frame pool");
@@ -623,10 +899,16 @@ static int execute(orc_run* r) {
     r->ra_win = 0;
     r->ra_next_fid = -1;
     r->ra_next_page = -1;
+    od_reset(r, -1);
+    r->hp[0].pending = r->hp[1].pending = 0;
+    r->span_half = 0;
     int64_t pos = c->dst_off ? c->dst_off[tb] : 0;
     for (int64_t s = c->prog_off[tb]; s < c->prog_off[tb + 1]; s++) { /* gpu_exec.py:95-105 */
       int64_t fid = c->segs[3 * s], base = c->segs[3 * s + 1], len = c->segs[3 * s + 2];
       if (fid < 0 || fid >= c->n_files) return fail(r, "segment names unknown file %lld", (long long)fid);
+      r->seg_lo = base; /* requests of this segment start at base + k * request_bytes */
+      r->seg_hi = base + len;
+      r->seg_ord = s - c->prog_off[tb];
       int64_t seg_off = 0;
       while (seg_off < len) {
         int64_t size = c->request_bytes < len - seg_off ? c->request_bytes : len - seg_off;
@@ -638,7 +920,9 @@ static int execute(orc_run* r) {
       }
       pos += len;
     }
-    /* on_tb_done: drain + retire (gpu_exec.py:281-286) */
+    /* on_tb_done: drain + retire (gpu_exec.py:281-286); windows never reached are dropped */
+    od_drain(r, 0);
+    od_drain(r, 1);
     pb_discard_all(r);
     if (!c->raw_mode && c->policy == ORC_POLICY_PER_TB) retire_tb(r);
   }
@@ -702,6 +986,8 @@ void orc_destroy(orc_run* r) {
   free(r->pb_nbytes);
   free(r->frame_mem);
   free(r->pb_mem);
+  free(r->half_mem[0]);
+  free(r->half_mem[1]);
   free(r->staging);
   if (r->fds) {
     for (int f = 0; f < r->cfg.n_files; f++)

@@ -24,15 +24,17 @@ enum {
 };
 
 enum { ORC_POLICY_GLOBAL = 0, ORC_POLICY_PER_TB = 1 };
-enum { ORC_RA_STATIC = 0, ORC_RA_ADAPTIVE = 1 };
+enum { ORC_RA_STATIC = 0, ORC_RA_DOUBLING = 1, ORC_RA_ONDEMAND = 2 };
+enum { ORC_CLAMP_SEGMENT = 0, ORC_CLAMP_EOF = 1 };
 enum { ORC_SRC_NONE = 0, ORC_SRC_SYNTH = 1, ORC_SRC_FILES = 2 };
 enum { ORC_LOG_DELIVERIES = 0, ORC_LOG_RPCS = 1, ORC_LOG_VICTIMS = 2, ORC_LOG_WINDOWS = 3 };
 
 typedef struct {
   int64_t page_size, cache_bytes, prefetch_bytes, request_bytes, staging_bytes, ra_max_bytes;
-  int64_t ra_init_bytes; /* adaptive first window (0 = page + prefetch) */
+  int64_t ra_init_bytes; /* doubling first window (0 = page + prefetch) */
   int32_t policy, resident_limit, raw_mode, readahead, pcie_disabled, log;
   int32_t n_files, n_tb;
+  int32_t ra_clamp, reserved; /* ondemand windows end at the TB's segment or at EOF */
   const int64_t* file_sizes;   /* n_files */
   const uint8_t* read_only;    /* n_files */
   const int64_t* prog_off;     /* n_tb + 1, index into segs (in segments) */

@@ -25,6 +25,7 @@ LIB_PATH = os.path.join(HERE, "_build", "libgfs_oracle.so")
 
 SRC_NONE, SRC_SYNTH, SRC_FILES = 0, 1, 2
 LOG_DELIVERIES, LOG_RPCS, LOG_VICTIMS, LOG_WINDOWS = 0, 1, 2, 3
+READAHEAD = {"static": 0, "doubling": 1, "adaptive": 2}  # adaptive = the ondemand law
 
 
 class OrcCfg(C.Structure):
@@ -35,6 +36,7 @@ class OrcCfg(C.Structure):
         ("policy", C.c_int32), ("resident_limit", C.c_int32), ("raw_mode", C.c_int32),
         ("readahead", C.c_int32), ("pcie_disabled", C.c_int32), ("log", C.c_int32),
         ("n_files", C.c_int32), ("n_tb", C.c_int32),
+        ("ra_clamp", C.c_int32), ("reserved", C.c_int32),
         ("file_sizes", C.POINTER(C.c_int64)), ("read_only", C.POINTER(C.c_uint8)),
         ("prog_off", C.POINTER(C.c_int64)), ("segs", C.POINTER(C.c_int64)),
         ("order", C.POINTER(C.c_int32)), ("dst_off", C.POINTER(C.c_int64)),
@@ -138,7 +140,8 @@ def run_oracle(cfg, workload, *, source: int = SRC_NONE, paths=None, io_direct: 
     c.policy = 1 if cfg["gpufs.policy"] == "per-tb-lra" else 0
     c.resident_limit = cfg.resident_limit()
     c.raw_mode = int(bool(cfg["mode.gpu_cache_disabled"]))
-    c.readahead = 1 if cfg["io.readahead"] == "adaptive" else 0
+    c.readahead = READAHEAD[cfg["io.readahead"]]
+    c.ra_clamp = 1 if cfg["io.ra_clamp"] == "eof" else 0
     c.pcie_disabled = int(bool(cfg["mode.pcie_disabled"]))
     c.log = int(log)
     c.n_files = n_files

@@ -404,7 +404,7 @@ static void worker_main(gfs_ctx* ctx, int wid) {
     } else if (from_map) {
       buf = nullptr;
     } else {
-      buf = ctx->h_staging + (int64_t)slot * ctx->slot_bytes;
+      buf = ctx->h_staging + ((int64_t)slot * ctx->landing_halves + half) * ctx->slot_bytes;
     }
     nreq++;
     const bool bad = slot < 0 || slot >= ctx->n_ctas || fid < 0 || fid >= (int)ctx->files.size() ||
@@ -448,7 +448,7 @@ static void worker_main(gfs_ctx* ctx, int wid) {
           const uint64_t pages = (uint64_t)((o + len + 4095) / 4096);
           CUresult cr = ctx->write_value64((CUstream)bs, (CUdeviceptr)(ctx->d_landed + li), (cuuint64_t)((pages << 32) | seq), 0);
           if (cr == CUDA_SUCCESS && o == 0)
-            cr = ctx->write_value64((CUstream)bs, (CUdeviceptr)(ctx->d_doorbell + slot),
+            cr = ctx->write_value64((CUstream)bs, (CUdeviceptr)(ctx->d_doorbell + li),
                                     (cuuint64_t)(((uint64_t)n << 32) | seq), 0);
           if (cr != CUDA_SUCCESS) ce = cudaErrorUnknown;
         }
@@ -467,7 +467,7 @@ static void worker_main(gfs_ctx* ctx, int wid) {
           cudaEventRecord(ctx->bell_ev[wid], st);
           cudaStreamWaitEvent(bs, ctx->bell_ev[wid], 0);
         }
-        CUresult cr = ctx->write_value64((CUstream)bs, (CUdeviceptr)(ctx->d_doorbell + slot), (cuuint64_t)v, 0);
+        CUresult cr = ctx->write_value64((CUstream)bs, (CUdeviceptr)(ctx->d_doorbell + li), (cuuint64_t)v, 0);
         if (cr != CUDA_SUCCESS) ctx->worker_error.store(EIO);
       }
       // The driver may hold freshly enqueued work in its push buffer until the next call on
@@ -477,7 +477,7 @@ static void worker_main(gfs_ctx* ctx, int wid) {
       cudaStreamQuery(bs);
       ctx->t_xfer.fetch_add((int64_t)(now_ns() - t1), std::memory_order_relaxed);
     } else {
-      RpcResp* r = &ctx->h_resp[slot];
+      RpcResp* r = &ctx->h_resp[(int64_t)slot * ctx->landing_halves + half];
       r->nbytes = n;
       r->buf = (mapped_zc || hybrid) ? -1 : b;
       if (bounce && n <= 0) ctx->bounce_last[b] = 0;  // nothing to pull: buffer stays free
@@ -508,10 +508,10 @@ static void reset_daemon(gfs_ctx* ctx) {
   cudaGetLastError();
   const uint64_t served = __atomic_load_n(ctx->h_served, __ATOMIC_ACQUIRE);
   memset(ctx->h_ring, 0, (size_t)ctx->ring_size * sizeof(RpcReq));
-  memset(ctx->h_resp, 0, (size_t)ctx->n_ctas * sizeof(RpcResp));
+  memset(ctx->h_resp, 0, (size_t)ctx->n_ctas * ctx->landing_halves * sizeof(RpcResp));
   if (ctx->h_release) memset(ctx->h_release, 0, ctx->bounce_last.size() * 4);
   std::fill(ctx->bounce_last.begin(), ctx->bounce_last.end(), 0u);
-  if (ctx->d_doorbell) cudaMemset(ctx->d_doorbell, 0, (size_t)ctx->n_ctas * 8);
+  if (ctx->d_doorbell) cudaMemset(ctx->d_doorbell, 0, (size_t)ctx->n_ctas * ctx->landing_halves * 8);
   if (ctx->d_landed) cudaMemset(ctx->d_landed, 0, (size_t)ctx->n_ctas * ctx->landing_halves * 8);
   ctx->req_head.store(served);
   ctx->stop.store(false);
@@ -572,7 +572,9 @@ extern "C" int gfs_create(const gfs_config* cfg_in, gfs_ctx** out) {
   if (cfg.staging_bytes < 1) return fail(GFS_EINVAL, "staging_bytes must be >= 1");
   if (cfg.policy != GFS_POLICY_GLOBAL_LRU && cfg.policy != GFS_POLICY_PER_TB_LRA)
     return fail(GFS_EINVAL, "unknown policy %d", cfg.policy);
-  if (cfg.readahead == GFS_RA_ADAPTIVE && (cfg.ra_max_bytes < cfg.page_size || cfg.ra_max_bytes % cfg.page_size))
+  if (cfg.readahead < GFS_RA_STATIC || cfg.readahead > GFS_RA_ONDEMAND)
+    return fail(GFS_EINVAL, "unknown readahead mode %d", cfg.readahead);
+  if (cfg.readahead != GFS_RA_STATIC && (cfg.ra_max_bytes < cfg.page_size || cfg.ra_max_bytes % cfg.page_size))
     return fail(GFS_EINVAL, "ra_max_bytes must be a positive multiple of page_size");
   if (cfg.ra_init_bytes < 0 || cfg.ra_init_bytes % cfg.page_size)
     return fail(GFS_EINVAL, "ra_init_bytes must be 0 or a multiple of page_size");
@@ -587,8 +589,12 @@ extern "C" int gfs_create(const gfs_config* cfg_in, gfs_ctx** out) {
                 "per-tb-lra needs cache_bytes/page_size >= resident TBs (%lld frames for %d TBs)",
                 (long long)nframes, cfg.resident_limit);
   int64_t pb_cap = cfg.prefetch_bytes;
-  if (cfg.readahead == GFS_RA_ADAPTIVE && cfg.ra_max_bytes - cfg.page_size > pb_cap)
+  if (cfg.readahead == GFS_RA_DOUBLING && cfg.ra_max_bytes - cfg.page_size > pb_cap)
     pb_cap = cfg.ra_max_bytes - cfg.page_size;
+  // ondemand: a landing half holds a whole window or synchronous span, and an adopted window
+  // is the private buffer in full (its first page included)
+  if (cfg.readahead == GFS_RA_ONDEMAND)
+    pb_cap = round_up(std::max(cfg.ra_max_bytes, cfg.page_size + cfg.prefetch_bytes), cfg.page_size);
   if (pb_cap / cfg.page_size >= MAX_PB_ENTRIES)
     return fail(GFS_EINVAL, "private buffer of %lld pages exceeds %d", (long long)(pb_cap / cfg.page_size),
                 MAX_PB_ENTRIES - 1);
@@ -598,9 +604,11 @@ extern "C" int gfs_create(const gfs_config* cfg_in, gfs_ctx** out) {
   ctx->nframes = nframes;
   ctx->quota = quota;
   ctx->pb_cap = pb_cap;
-  int64_t span_max = cfg.page_size + pb_cap;
+  int64_t span_max = cfg.readahead == GFS_RA_ONDEMAND ? pb_cap : cfg.page_size + pb_cap;
   if (cfg.raw_mode) span_max = std::max<int64_t>(cfg.max_request_bytes, 4096);
   ctx->slot_bytes = round_up(span_max, 4096);
+  // ondemand readahead: the next window lands in the other half while the CTA reads one
+  ctx->landing_halves = (cfg.readahead == GFS_RA_ONDEMAND && !cfg.raw_mode) ? 2 : 1;
   auto bail = [&](int rc) {
     free_all(ctx);
     delete ctx;
@@ -706,13 +714,13 @@ extern "C" int gfs_create(const gfs_config* cfg_in, gfs_ctx** out) {
   TRY(cudaMalloc(&ctx->d_scratch, 64));
   TRY(cudaHostAlloc(&ctx->h_ring, (size_t)ctx->ring_size * sizeof(RpcReq),
                     cudaHostAllocMapped | cudaHostAllocPortable));
-  TRY(cudaHostAlloc(&ctx->h_resp, (size_t)ctx->n_ctas * sizeof(RpcResp),
+  TRY(cudaHostAlloc(&ctx->h_resp, (size_t)ctx->n_ctas * ctx->landing_halves * sizeof(RpcResp),
                     cudaHostAllocMapped | cudaHostAllocPortable));
   if (cfg.transfer == GFS_XFER_ZEROCOPY)
-    TRY(cudaHostAlloc(&ctx->h_staging, (size_t)(ctx->n_ctas * ctx->slot_bytes),
+    TRY(cudaHostAlloc(&ctx->h_staging, (size_t)(ctx->n_ctas * ctx->landing_halves * ctx->slot_bytes),
                       cudaHostAllocMapped | cudaHostAllocPortable));
   if (cfg.transfer == GFS_XFER_MAPPED_ZC)
-    TRY(cudaMalloc(&ctx->d_landing, (size_t)(ctx->n_ctas * ctx->slot_bytes)));
+    TRY(cudaMalloc(&ctx->d_landing, (size_t)(ctx->n_ctas * ctx->landing_halves * ctx->slot_bytes)));
   if (cfg.transfer == GFS_XFER_BOUNCE) {
     // ~24 MiB pool in total so it stays resident in the host LLC, 2..8 buffers per worker
     ctx->nbounce = (int)std::max<int64_t>(2, (24ll << 20) / (ctx->slot_bytes * cfg.io_workers));
@@ -723,15 +731,14 @@ extern "C" int gfs_create(const gfs_config* cfg_in, gfs_ctx** out) {
     TRY(cudaHostAlloc(&ctx->h_release, (size_t)nb * 4, cudaHostAllocMapped | cudaHostAllocPortable));
     memset(ctx->h_release, 0, (size_t)nb * 4);
     ctx->bounce_last.assign((size_t)nb, 0);
-    TRY(cudaMalloc(&ctx->d_landing, (size_t)(ctx->n_ctas * ctx->slot_bytes)));
+    TRY(cudaMalloc(&ctx->d_landing, (size_t)(ctx->n_ctas * ctx->landing_halves * ctx->slot_bytes)));
   }
   memset(ctx->h_ring, 0, (size_t)ctx->ring_size * sizeof(RpcReq));
-  memset(ctx->h_resp, 0, (size_t)ctx->n_ctas * sizeof(RpcResp));
+  memset(ctx->h_resp, 0, (size_t)ctx->n_ctas * ctx->landing_halves * sizeof(RpcResp));
   TRY(cudaHostAlloc(&ctx->h_served, 64, cudaHostAllocMapped | cudaHostAllocPortable));
   memset(ctx->h_served, 0, 64);
   if (cfg.transfer == GFS_XFER_DMA || cfg.transfer == GFS_XFER_MAPPED ||
       cfg.transfer == GFS_XFER_MAPPED_HYBRID) {
-    ctx->landing_halves = (cfg.async_ra && !cfg.raw_mode && cfg.transfer != GFS_XFER_MAPPED_HYBRID) ? 2 : 1;
     TRY(cudaMalloc(&ctx->d_landing, (size_t)(ctx->n_ctas * ctx->landing_halves * ctx->slot_bytes)));
     // experiments: GFS_STREAM_PIECE_MIB (0 = off, the default: whole-window copies measured
     // faster on the headline, 54.0 vs 51.9 GB/s with 4 MiB pieces)
@@ -741,8 +748,8 @@ extern "C" int gfs_create(const gfs_config* cfg_in, gfs_ctx** out) {
                          ctx->slot_bytes >= 2 * ctx->stream_piece;
     TRY(cudaMalloc(&ctx->d_landed, (size_t)ctx->n_ctas * ctx->landing_halves * 8));
     TRY(cudaMemset(ctx->d_landed, 0, (size_t)ctx->n_ctas * ctx->landing_halves * 8));
-    TRY(cudaMalloc(&ctx->d_doorbell, (size_t)ctx->n_ctas * 8));
-    TRY(cudaMemset(ctx->d_doorbell, 0, (size_t)ctx->n_ctas * 8));
+    TRY(cudaMalloc(&ctx->d_doorbell, (size_t)ctx->n_ctas * ctx->landing_halves * 8));
+    TRY(cudaMemset(ctx->d_doorbell, 0, (size_t)ctx->n_ctas * ctx->landing_halves * 8));
     ctx->bell_ev.resize((size_t)cfg.io_workers, nullptr);
     for (auto& ev : ctx->bell_ev) TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   }
@@ -1037,7 +1044,7 @@ extern "C" int gfs_run_consume(gfs_ctx* ctx, const gfs_program* prog, void* dst,
   c.stream_pieces = ctx->stream_pieces ? 1 : 0;
   c.stream_piece = ctx->stream_piece;
   c.landed = ctx->d_landed;
-  c.async_ra = ctx->landing_halves > 1 && !cfg.log;
+  c.ra_clamp = cfg.ra_clamp;
   c.verify = cfg.verify;
   c.pcie_disabled = cfg.pcie_disabled;
   c.n_files = (int32_t)ctx->files.size();
@@ -1146,16 +1153,18 @@ extern "C" int gfs_run_consume(gfs_ctx* ctx, const gfs_program* prog, void* dst,
     std::string diag;
     if (g.error == ERR_TIMEOUT && g.error_info >= 21 && g.error_info <= 23) {
       // a request never completed: say where it is (ring entry, mailbox/doorbell, workers)
-      const int slot = (int)(g.error_arg >> 32);
+      const int mb = (int)(g.error_arg >> 32);  // mailbox / doorbell: slot * halves + half
+      const int slot = mb / ctx->landing_halves;
       const uint32_t seq = (uint32_t)g.error_arg;
       char b[256];
       const RpcReq* e = &ctx->h_ring[(seq - 1) & (ctx->ring_size - 1)];
-      snprintf(b, sizeof b, "; slot %d seq %u: ring entry seq %u slot %d, mailbox seq %u", slot, seq,
-               e->seq, e->slot, slot < ctx->n_ctas ? ctx->h_resp[slot].seq : 0);
+      snprintf(b, sizeof b, "; slot %d half %d seq %u: ring entry seq %u slot %d, mailbox seq %u", slot,
+               mb % ctx->landing_halves, seq, e->seq, e->slot,
+               slot < ctx->n_ctas ? ctx->h_resp[mb].seq : 0);
       diag += b;
       if (ctx->d_doorbell && slot < ctx->n_ctas) {
         unsigned long long bell = 0;
-        cudaMemcpy(&bell, ctx->d_doorbell + slot, 8, cudaMemcpyDeviceToHost);
+        cudaMemcpy(&bell, ctx->d_doorbell + mb, 8, cudaMemcpyDeviceToHost);
         snprintf(b, sizeof b, ", doorbell seq %u n %u", (uint32_t)bell, (uint32_t)(bell >> 32));
         diag += b;
       }

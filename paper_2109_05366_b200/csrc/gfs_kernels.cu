@@ -132,6 +132,7 @@ __device__ __forceinline__ uint8_t ld1(const uint8_t* p) {
 // ----------------------------------------------------------------- CTA state
 
 constexpr int TMA_NST = 4;        // K1 stage ring: stages
+constexpr int OD_MARKS = 4;       // readahead markers remembered per TB stream
 constexpr int64_t TMA_CH = 8192;  // bytes per stage (one bulk load, 1-2 bulk stores per page)
 
 struct Smem {
@@ -169,6 +170,7 @@ struct Smem {
     unsigned tail_mask, part_mask;  // pages with a sub-16 B EOF tail / a partial delivery
     int64_t total;                  // bytes this batch delivers
     int64_t rpc_n;
+    int64_t sync_m;                 // ondemand: pages of the synchronous span (od_plan_sync)
     unsigned long long ret_pos;
     int64_t own_head0, own_tail0;
     uint32_t frame[32];
@@ -180,16 +182,33 @@ struct Smem {
   int fresh_done;            // this CTA saw the never-used frames run out (they never return)
   // lookahead: file bytes [la_lo, la_hi) of la_fid were delivered ahead of their gread
   int64_t la_fid, la_lo, la_hi;
-  // asynchronous readahead: the landing half holding the current span, and the next
-  // window's request in flight into the other half
-  int span_half, ar_pending, ar_half;
+  // the landing half holding the current span (the private buffer's bytes)
+  int span_half;
   // streamed windows, per landing half: the last request into it and how much has landed
   uint32_t st_seq[2];
   int64_t st_n[2], st_landed[2];
-  int64_t ar_fid, ar_page, ar_span;
-  uint32_t ar_seq;
-  unsigned long long ar_pos;
   int64_t page_size_cached;  // c.page_size, for the smem-only pb_take
+  int64_t pb_off_adj;        // span offset of entry i = i * page - pb_off_adj (pg for adopted windows)
+  // ondemand readahead (io.readahead=adaptive, host_os.py:106-152), one stream per TB
+  struct {
+    int64_t fid, ws, wsize, async, prev_end;          // ReadaheadState, in pages
+    int64_t mark[OD_MARKS];                            // marker pages (-1 = none)
+    long long dec_key;                                 // gread instance decided last
+    int64_t run_page, run_n;                           // async run decided, not yet submitted
+    int64_t cap;                                       // next marker past the walk position
+  } od;
+  // the current gread and segment (ondemand: which request a page belongs to)
+  int64_t g_lo, g_hi, seg_lo, seg_hi;
+  long long seg_ord;
+  int g_la;
+  // landing halves holding a pending (requested, not adopted) readahead window
+  struct {
+    int pending, deferred;
+    int64_t fid, page, span;
+    uint32_t seq, age;
+    unsigned long long pos;
+  } hp[2];
+  uint32_t hp_age;
   uint32_t pb_absent[MAX_PB_ENTRIES / 32];  // private-buffer entries consumed / dropped
 };
 
@@ -522,6 +541,7 @@ __device__ void pb_fill(const DevCtx& c, Smem& s, int64_t fid, int64_t base, int
   ST(pb_discarded_bytes) += s.pb_filled;  // every unconsumed entry is stale
   s.pb_fid = fid;
   s.pb_base = base;
+  s.pb_off_adj = 0;
   const int64_t pg = c.page_size;
   int64_t cnt = m - 1;
   if (cnt >= MAX_PB_ENTRIES) {
@@ -550,6 +570,11 @@ __device__ void pb_fill(const DevCtx& c, Smem& s, int64_t fid, int64_t base, int
 
 __device__ __forceinline__ bool pb_present(const Smem& s, int64_t i) {
   return !((s.pb_absent[i >> 5] >> (i & 31)) & 1u);
+}
+
+__device__ __forceinline__ bool pb_has(const Smem& s, int64_t fid, int64_t page) {
+  const int64_t i = page - s.pb_base;
+  return s.pb_count > 0 && fid == s.pb_fid && i >= 1 && i <= s.pb_count && pb_present(s, i);
 }
 
 // prefetcher.py:52-61
@@ -605,8 +630,8 @@ __device__ int64_t pb_take_run(Smem& s, int64_t page, int n) {
   return bytes;
 }
 
-// request_span (prefetcher.py:13-25) + the adaptive window (io.readahead=adaptive)
-// Pure part of request_span: the span an RPC at `page` would have, and the adaptive
+// request_span (prefetcher.py:13-25) + the doubling window (io.readahead=doubling)
+// Pure part of request_span: the span an RPC at `page` would have, and the doubling
 // window it implies (no state change).
 __device__ int64_t span_peek(const DevCtx& c, const Smem& s, int64_t fid, int64_t page,
                              int64_t seg_end, int64_t* new_win) {
@@ -617,7 +642,7 @@ __device__ int64_t span_peek(const DevCtx& c, const Smem& s, int64_t fid, int64_
   if (off >= F.size) return 0;
   const bool ro = F.read_only != 0;
   int64_t want = (ro && c.prefetch_bytes > 0) ? pg + c.prefetch_bytes : pg;
-  if (c.readahead == GFS_RA_ADAPTIVE && ro) {
+  if (c.readahead == GFS_RA_DOUBLING && ro) {
     const int64_t base = c.ra_init_bytes > pg + c.prefetch_bytes ? c.ra_init_bytes : pg + c.prefetch_bytes;
     int64_t win = base;
     if (s.ra_win > 0 && fid == s.ra_next_fid && page == s.ra_next_page)
@@ -634,7 +659,7 @@ __device__ int64_t span_peek(const DevCtx& c, const Smem& s, int64_t fid, int64_
 __device__ int64_t rpc_span(const DevCtx& c, Smem& s, int64_t fid, int64_t page, int64_t seg_end) {
   int64_t win;
   const int64_t span = span_peek(c, s, fid, page, seg_end, &win);
-  if (span > 0 && c.readahead == GFS_RA_ADAPTIVE && c.files[fid].read_only) {
+  if (span > 0 && c.readahead == GFS_RA_DOUBLING && c.files[fid].read_only) {
     s.ra_win = win;
     s.ra_next_fid = fid;
     s.ra_next_page = page + (span + c.page_size - 1) / c.page_size;
@@ -696,7 +721,7 @@ __device__ int64_t rpc_wait(const DevCtx& c, Smem& s, int64_t fid, int64_t off, 
   const uint64_t tw = globaltimer();
   int64_t n;
   if (c.transfer == GFS_XFER_DMA || c.transfer == GFS_XFER_MAPPED) {
-    const unsigned long long* bell = &c.doorbell[slot];
+    const unsigned long long* bell = &c.doorbell[(int64_t)slot * c.landing_halves + half];
     for (;;) {
       uint64_t v = ld_acquire_sys64(bell);
       if ((uint32_t)v == seq) {
@@ -705,7 +730,7 @@ __device__ int64_t rpc_wait(const DevCtx& c, Smem& s, int64_t fid, int64_t off, 
         break;
       }
       if (!keep_waiting(c, t0, 21)) {
-        c.g->error_arg = ((unsigned long long)slot << 32) | seq;
+        c.g->error_arg = ((unsigned long long)(slot * c.landing_halves + half) << 32) | seq;
         return -1;
       }
       __nanosleep(256);
@@ -715,7 +740,7 @@ __device__ int64_t rpc_wait(const DevCtx& c, Smem& s, int64_t fid, int64_t off, 
     // slot) or by mailbox (the CTA pulls the span from the pinned page-cache mapping)
     // (both answers arrive through the HBM doorbell, so nothing polls host memory: bit 63
     // set = "not copied, pull it yourself")
-    const unsigned long long* bell = &c.doorbell[slot];
+    const unsigned long long* bell = &c.doorbell[(int64_t)slot * c.landing_halves + half];
     for (;;) {
       const uint64_t v = ld_acquire_sys64(bell);
       if ((uint32_t)v == seq) {
@@ -729,13 +754,13 @@ __device__ int64_t rpc_wait(const DevCtx& c, Smem& s, int64_t fid, int64_t off, 
         break;
       }
       if (!keep_waiting(c, t0, 23)) {
-        c.g->error_arg = ((unsigned long long)slot << 32) | seq;
+        c.g->error_arg = ((unsigned long long)(slot * c.landing_halves + half) << 32) | seq;
         return -1;
       }
       __nanosleep(256);
     }
   } else {
-    const RpcResp* r = &c.resp[slot];
+    const RpcResp* r = &c.resp[(int64_t)slot * c.landing_halves + half];
     __nanosleep(2000);
     for (;;) {
       if (ld_acquire_sys(&r->seq) == seq) {
@@ -753,7 +778,7 @@ __device__ int64_t rpc_wait(const DevCtx& c, Smem& s, int64_t fid, int64_t off, 
         break;
       }
       if (!keep_waiting(c, t0, 22)) {
-        c.g->error_arg = ((unsigned long long)slot << 32) | seq;
+        c.g->error_arg = ((unsigned long long)(slot * c.landing_halves + half) << 32) | seq;
         return -1;
       }
       __nanosleep(4000);
@@ -797,7 +822,8 @@ __device__ bool wait_landed(const DevCtx& c, Smem& s, int h, int64_t need) {
 
 // Where the current span (page 0 + private-buffer pages) lives.
 __device__ __forceinline__ const uint8_t* span_base(const DevCtx& c, const Smem& s) {
-  if (c.transfer == GFS_XFER_ZEROCOPY) return c.staging + (int64_t)blockIdx.x * c.slot_bytes;
+  if (c.transfer == GFS_XFER_ZEROCOPY)
+    return c.staging + ((int64_t)blockIdx.x * c.landing_halves + s.span_half) * c.slot_bytes;
   return c.landing + ((int64_t)blockIdx.x * c.landing_halves + s.span_half) * c.slot_bytes;
 }
 
@@ -810,69 +836,370 @@ __device__ int64_t rpc_call(const DevCtx& c, Smem& s, int64_t fid, int64_t off, 
   return rpc_wait(c, s, fid, off, seq, pos, half);
 }
 
-// A readahead the TB did not consume (it left the stream): wait for it, count its bytes
-// as moved (they show up as prefetch waste).
-__device__ int drain_readahead(const DevCtx& c, Smem& s) {
-  if (!s.ar_pending) return 0;
-  const int64_t n = rpc_wait(c, s, s.ar_fid, s.ar_page * c.page_size, s.ar_seq, s.ar_pos, s.ar_half);
-  s.ar_pending = 0;
-  if (n < 0 || !wait_landed(c, s, s.ar_half, n)) return -1;
-  account_transfer(c, s, n);
+// ------------------------------------------------------------- ondemand readahead
+//
+// io.readahead=adaptive is the reference's Linux-style ondemand law (HostOs._decide,
+// host_os.py:106-152) run per TB stream on the device.  A "read" is one gread request
+// (the reference's pread).  Its decision is taken the first time the walk meets one of its
+// pages that is missing (not cached, not in the private buffer, not in a pending window) or
+// a readahead marker — the reference decides at pread entry on "any page missing or any
+// marker" (host_os.py:255-265); the inputs are the same, the walk only takes it lazily.
+//   cold sequential read of n pages: window max(n, min(4n, ra_max)); the requested pages
+//     are fetched synchronously, the rest asynchronously, marker on the first async page;
+//   a read hitting the marker: the next window (double, capped at ra_max) asynchronously,
+//     marker on its first page (a marker that does not match the window state rebuilds it
+//     from the resident run around it, the reference's context recovery);
+//   a non-sequential read: exactly its missing pages, window state reset.
+// Asynchronous windows land in the CTA's other landing half while it consumes the current
+// one and are adopted as the private buffer when the walk reaches them.  Windows are clamped
+// at EOF (io.ra_clamp=eof, the reference) or at the TB's segment end (segment, the default:
+// a TB's stream is its stride, and the law sees only that segment's pages).
+
+__device__ __forceinline__ int64_t od_pages(const DevCtx& c, int64_t bytes) {
+  return (bytes + c.page_size - 1) / c.page_size;
+}
+
+__device__ bool od_in_pending(const DevCtx& c, const Smem& s, int64_t fid, int64_t p, int* h_out) {
+  for (int h = 0; h < 2; h++)
+    if (s.hp[h].pending && s.hp[h].fid == fid && p >= s.hp[h].page &&
+        p < s.hp[h].page + od_pages(c, s.hp[h].span)) {
+      if (h_out) *h_out = h;
+      return true;
+    }
+  return false;
+}
+
+// Resident for the law (the sequentiality test and the resident run): cached or being
+// fetched by anyone, in the private buffer, or in a pending window — except this TB's own
+// claims [ex_lo, ex_hi) for the request being decided, which nothing has fetched yet.  With
+// the segment clamp the stream sees only its own segment (what other TBs cached next to it
+// would make the decision depend on their progress).
+__device__ bool od_resident(const DevCtx& c, const Smem& s, int64_t fid, int64_t p, int64_t ex_lo,
+                            int64_t ex_hi) {
+  const DevFile& F = c.files[fid];
+  if (p < 0 || p >= od_pages(c, F.size)) return false;
+  if (c.ra_clamp == GFS_RA_CLAMP_SEGMENT && (p < s.seg_lo / c.page_size || p >= od_pages(c, s.seg_hi)))
+    return false;
+  if (pb_has(s, fid, p) || od_in_pending(c, s, fid, p, nullptr)) return true;
+  if (p >= ex_lo && p < ex_hi) return false;
+  return ld_acquire_gpu(&F.pt[p]) != PT_EMPTY;
+}
+
+// Page limit of the stream: EOF, or the end of the TB's segment.
+__device__ int64_t od_limit(const DevCtx& c, const Smem& s, int64_t fid) {
+  int64_t lim = od_pages(c, c.files[fid].size);
+  if (c.ra_clamp == GFS_RA_CLAMP_SEGMENT) {
+    const int64_t se = od_pages(c, s.seg_hi);
+    if (se < lim) lim = se;
+  }
+  return lim;
+}
+
+// The request page p belongs to, as pages [*gs, *ge), and its instance key.  With lookahead
+// a batch walks the TB's next requests too; they start at seg_lo + k * request_bytes.
+__device__ long long od_request_of(const DevCtx& c, const Smem& s, int64_t fid, int64_t p, int64_t* gs,
+                                   int64_t* ge) {
+  const int64_t pg = c.page_size, fs = c.files[fid].size;
+  int64_t lo = s.g_lo, hi = s.g_hi;
+  if (s.g_la) {
+    lo = s.seg_lo + (p * pg - s.seg_lo) / c.request_bytes * c.request_bytes;
+    hi = lo + c.request_bytes < s.seg_hi ? lo + c.request_bytes : s.seg_hi;
+  }
+  if (hi > fs) hi = fs;
+  *gs = lo / pg;
+  *ge = od_pages(c, hi);
+  return (s.seg_ord << 32) | (long long)((lo - s.seg_lo) / c.request_bytes);
+}
+
+// HostOs._resident_run (host_os.py:88-103): the resident run [*rs, *re) around page m,
+// each scan capped at ra_max pages.
+__device__ void od_resident_run(const DevCtx& c, const Smem& s, int64_t fid, int64_t m, int64_t ex_lo,
+                                int64_t ex_hi, int64_t* rs, int64_t* re) {
+  const int64_t ra_max = c.ra_max_bytes / c.page_size, np = od_pages(c, c.files[fid].size);
+  int64_t a = m;
+  while (m - a < ra_max && a > 0 && od_resident(c, s, fid, a - 1, ex_lo, ex_hi)) a--;
+  int64_t e = m + 1;
+  while (e - m <= ra_max && e < np && od_resident(c, s, fid, e, ex_lo, ex_hi)) e++;
+  *rs = a;
+  *re = e;
+}
+
+__device__ void od_add_mark(Smem& s, int64_t page) {
+  for (int i = 0; i < OD_MARKS; i++)
+    if (s.od.mark[i] < 0) {
+      s.od.mark[i] = page;
+      return;
+    }
+  for (int i = 0; i + 1 < OD_MARKS; i++) s.od.mark[i] = s.od.mark[i + 1];  // drop the oldest
+  s.od.mark[OD_MARKS - 1] = page;
+}
+
+__device__ void od_reset(Smem& s, int64_t fid) {
+  s.od.fid = fid;
+  s.od.ws = s.od.wsize = s.od.async = 0;
+  s.od.prev_end = -1;
+  for (int i = 0; i < OD_MARKS; i++) s.od.mark[i] = -1;
+  s.od.dec_key = -1;
+  s.od.run_n = 0;
+}
+
+// HostOs._decide (host_os.py:106-152) for the request [gs, ge) (thread 0).  Updates the
+// window state and markers; the asynchronous run to request goes to s.od.run_page/run_n
+// (run_n = 0: none).  Returns the window bytes window_history records (0 = none).
+__device__ int64_t od_decide(const DevCtx& c, Smem& s, int64_t fid, int64_t gs, int64_t ge, int64_t ex_lo,
+                             int64_t ex_hi) {
+  const int64_t pg = c.page_size, ra_max = c.ra_max_bytes / pg;
+  const int64_t lim = od_limit(c, s, fid);
+  const int64_t npages = ge - gs, req_end = ge;
+  s.od.run_n = 0;
+  int64_t marker = -1;
+  for (int i = 0; i < OD_MARKS; i++) {  // each marker triggers at most once
+    const int64_t m = s.od.mark[i];
+    if (m >= gs && m < ge) {
+      s.od.mark[i] = -1;
+      if (marker < 0 || m < marker) marker = m;
+    }
+  }
+  if (marker >= 0) {
+    int64_t ns, nz;
+    if (s.od.wsize > 0 && marker == s.od.ws + s.od.wsize - s.od.async) {
+      ns = max(s.od.ws + s.od.wsize, req_end);
+      nz = min(2 * s.od.wsize, ra_max);
+    } else {  // context recovery
+      int64_t rs, re;
+      od_resident_run(c, s, fid, marker, ex_lo, ex_hi, &rs, &re);
+      ns = max(re, req_end);
+      nz = min(2 * max(re - rs, (int64_t)1), ra_max);
+    }
+    nz = min(nz, max(lim - ns, (int64_t)0));
+    s.od.prev_end = req_end;
+    if (nz == 0) {
+      s.od.ws = gs;
+      s.od.wsize = s.od.async = 0;
+      return 0;
+    }
+    s.od.ws = ns;
+    s.od.wsize = s.od.async = nz;
+    s.od.run_page = ns;
+    s.od.run_n = nz;
+    od_add_mark(s, ns);
+    return nz * pg;
+  }
+  const bool seq = gs == 0 || gs == s.od.prev_end ||
+                   (gs > 0 && od_resident(c, s, fid, gs - 1, ex_lo, ex_hi));
+  s.od.prev_end = req_end;
+  if (!seq) {
+    s.od.ws = gs;
+    s.od.wsize = s.od.async = 0;
+    return 0;
+  }
+  int64_t w = max(npages, min(4 * npages, ra_max));
+  w = min(w, max(lim - gs, npages));
+  s.od.ws = gs;
+  s.od.wsize = w;
+  s.od.async = w - npages;
+  if (s.od.async <= 0) return w * pg;
+  s.od.run_page = req_end;
+  s.od.run_n = s.od.async;
+  od_add_mark(s, req_end);
+  return w * pg;
+}
+
+// Request `span` bytes at `page` into landing half h (thread 0), with its RPC record and
+// counters.  A pending window under bounce transfers is requested only when adopted: a CTA
+// must not hold a host pool buffer while it waits for another request.
+__device__ bool od_submit(const DevCtx& c, Smem& s, int64_t fid, int64_t page, int64_t span, int h,
+                          bool pending) {
+  log_rec(c, GFS_LOG_RPCS, s.tb, fid, page * c.page_size, span);
+  ST(rpc_count)++;
+  ST(rpc_requested_bytes) += span;
+  s.hp[h].fid = fid;
+  s.hp[h].page = page;
+  s.hp[h].span = span;
+  s.hp[h].age = ++s.hp_age;
+  s.hp[h].pending = pending;
+  s.hp[h].deferred = pending && c.transfer == GFS_XFER_BOUNCE;
+  if (s.hp[h].deferred) return true;
+  if (!wait_landed(c, s, h, s.st_n[h])) return false;
+  return rpc_submit(c, s, fid, page * c.page_size, span, h, &s.hp[h].seq, &s.hp[h].pos);
+}
+
+// Wait for half h's request (submitting a deferred one first); counts its transfer.
+__device__ int64_t od_wait(const DevCtx& c, Smem& s, int h) {
+  const int64_t off = s.hp[h].page * c.page_size;
+  if (s.hp[h].deferred) {
+    s.hp[h].deferred = 0;
+    if (!wait_landed(c, s, h, s.st_n[h])) return -1;
+    if (!rpc_submit(c, s, s.hp[h].fid, off, s.hp[h].span, h, &s.hp[h].seq, &s.hp[h].pos)) return -1;
+  }
+  s.hp[h].pending = 0;
+  const int64_t n = rpc_wait(c, s, s.hp[h].fid, off, s.hp[h].seq, s.hp[h].pos, h);
+  if (n >= 0) account_transfer(c, s, n);
+  return n;
+}
+
+// A pending window the TB will not consume: wait for it and drop it (its bytes moved:
+// they show up as prefetch waste).
+__device__ int od_drain(const DevCtx& c, Smem& s, int h) {
+  const int64_t n = od_wait(c, s, h);
+  if (n < 0 || !wait_landed(c, s, h, n)) return -1;
+  if (s.pull_n > 0) {  // never pulled: hand a bounce buffer straight back
+    if (s.pull_buf >= 0) {
+      __threadfence_system();
+      st_release_sys(&c.bounce_release[s.pull_buf], s.pull_seq);
+    }
+    s.pull_n = 0;
+  }
+  return 0;
+}
+
+// Landing half for a new span (thread 0): one without a pending window — the half not
+// holding the private buffer first; taking the private buffer's half discards its
+// unconsumed entries — else the older pending window is drained.  `avoid`: a half taken
+// by the span requested alongside.  -1 on abort.
+__device__ int od_pick_half(const DevCtx& c, Smem& s, int avoid) {
+  const int a = s.span_half ^ 1, b = s.span_half;
+  int h = -1;
+  if (a != avoid && !s.hp[a].pending) h = a;
+  else if (b != avoid && !s.hp[b].pending) h = b;
+  if (h < 0) {
+    for (int k = 0; k < 2; k++)
+      if (k != avoid && (h < 0 || s.hp[k].age < s.hp[h].age)) h = k;
+    if (od_drain(c, s, h) < 0) return -1;
+  }
+  if (h == s.span_half && s.pb_count > 0) {
+    ST(pb_discarded_bytes) += s.pb_filled;
+    s.pb_filled = 0;
+    s.pb_count = 0;
+  }
+  return h;
+}
+
+__device__ bool od_submit_run(const DevCtx& c, Smem& s, int64_t fid, int avoid) {
+  if (s.od.run_n <= 0) return true;
+  const int64_t pg = c.page_size, fs = c.files[fid].size;
+  int64_t span = s.od.run_n * pg;
+  if (span > fs - s.od.run_page * pg) span = fs - s.od.run_page * pg;
+  s.od.run_n = 0;
+  if (span <= 0) return true;
+  const int h = od_pick_half(c, s, avoid);
+  return h >= 0 && od_submit(c, s, fid, s.od.run_page, span, h, true);
+}
+
+// Take the request decision for page p's request if it has not been taken (thread 0).
+__device__ void od_decide_once(const DevCtx& c, Smem& s, int64_t fid, int64_t p, int64_t ex_lo, int64_t ex_hi,
+                               int64_t* ge_out) {
+  int64_t gs, ge;
+  const long long key = od_request_of(c, s, fid, p, &gs, &ge);
+  *ge_out = ge;
+  if (key == s.od.dec_key) return;
+  s.od.dec_key = key;
+  const int64_t w = od_decide(c, s, fid, gs, ge, ex_lo, ex_hi);
+  if (w > 0) log_rec(c, GFS_LOG_WINDOWS, s.tb, w, 0, 0);
+}
+
+// Walk position p0, before a batch (thread 0): a marker there fires its request's
+// decision (the next window is requested); a pending window holding p0 is adopted as the
+// private buffer (all its pages are entries: pb_off_adj).  Sets od.cap, the next marker or
+// pending window past p0: batches and hit runs stop before it.  False on abort.
+__device__ bool od_top(const DevCtx& c, Smem& s, int64_t fid, int64_t p0) {
+  s.od.cap = INT64_MAX;
+  if (!c.files[fid].read_only) return true;
+  for (int i = 0; i < OD_MARKS; i++)
+    if (s.od.mark[i] == p0) {
+      int64_t ge;
+      od_decide_once(c, s, fid, p0, 0, 0, &ge);
+      if (!od_submit_run(c, s, fid, -1)) return false;
+      break;
+    }
+  int h;
+  if (od_in_pending(c, s, fid, p0, &h)) {
+    const int64_t head = s.hp[h].page;
+    const int64_t n = od_wait(c, s, h);
+    if (n < 0) return false;
+    s.span_half = h;
+    if (n > 0) {
+      pb_fill(c, s, fid, head - 1, od_pages(c, n) + 1, n);
+      s.pb_off_adj = c.page_size;
+    } else {
+      ST(pb_discarded_bytes) += s.pb_filled;
+      s.pb_filled = 0;
+      s.pb_count = 0;
+    }
+  }
+  for (int i = 0; i < OD_MARKS; i++)
+    if (s.od.mark[i] > p0 && s.od.mark[i] < s.od.cap) s.od.cap = s.od.mark[i];
+  for (int k = 0; k < 2; k++)  // a pending window is adopted at its first page the walk reaches
+    if (s.hp[k].pending && s.hp[k].fid == fid && s.hp[k].page > p0 && s.hp[k].page < s.od.cap)
+      s.od.cap = s.hp[k].page;
+  return true;
+}
+
+// A synchronous miss at p0 with this TB's claims [ex_lo, ex_hi) (thread 0): the request's
+// decision, then the synchronous span — the missing pages from p0 to the request's end or
+// the first resident page, at most one landing half.  Returns its pages.
+__device__ int64_t od_plan_sync(const DevCtx& c, Smem& s, int64_t fid, int64_t p0, int64_t ex_lo, int64_t ex_hi) {
+  int64_t ge;
+  od_decide_once(c, s, fid, p0, ex_lo, ex_hi, &ge);
+  int64_t lim = p0 + c.slot_bytes / c.page_size;
+  if (ge < lim) lim = ge;
+  const int64_t np = od_pages(c, c.files[fid].size);
+  if (np < lim) lim = np;
+  int64_t q = p0 + 1;
+  while (q < lim && !od_resident(c, s, fid, q, ex_lo, ex_hi)) q++;
+  return q - p0;
+}
+
+// The synchronous span (thread 0): requested, then the decided asynchronous run, then
+// waited for; it becomes the private buffer's span.  Returns bytes, -1 on abort.
+__device__ int64_t fetch_span_od(const DevCtx& c, Smem& s, int64_t fid, int64_t page, int64_t sync_pages,
+                                 int64_t* span_out) {
+  const int64_t pg = c.page_size, fs = c.files[fid].size;
+  int64_t span = sync_pages * pg;
+  if (span > fs - page * pg) span = fs - page * pg;
+  *span_out = span;
+  if (span <= 0) {
+    s.od.run_n = 0;
+    return 0;
+  }
+  const int hs = od_pick_half(c, s, -1);
+  if (hs < 0 || !od_submit(c, s, fid, page, span, hs, false)) return -1;
+  if (!od_submit_run(c, s, fid, hs)) return -1;
+  const int64_t n = od_wait(c, s, hs);
+  s.span_half = hs;
+  return n;
+}
+
+// TB done: drop windows it did not reach.
+__device__ int od_drain_all(const DevCtx& c, Smem& s) {
+  for (int h = 0; h < 2; h++)
+    if (s.hp[h].pending && od_drain(c, s, h) < 0) return -1;
   return 0;
 }
 
 // The span starting at `page` (thread 0): request_span + RPC (prefetcher.py:13-25,
-// rpc.py:82-229).  With asynchronous readahead (copy-engine transfers, adaptive windows)
-// the request for the window after it is submitted as soon as this one lands, into the
-// other landing half, and adopted when the TB reaches its first page — the same requests,
-// the same windows and counters, issued one window earlier.  Returns bytes, -1 on abort.
+// rpc.py:82-229); under ondemand readahead the synchronous span of the request's missing
+// pages (sync_pages from od_plan_sync; < 0 = plan it here, claims [page, page + 1)).
+// Returns bytes, -1 on abort.
 __device__ int64_t fetch_span(const DevCtx& c, Smem& s, int64_t fid, int64_t page, int64_t seg_end,
-                              int64_t* span_out) {
+                              int64_t* span_out, int64_t sync_pages = -1) {
+  if (c.readahead == GFS_RA_ONDEMAND && c.files[fid].read_only) {
+    if (sync_pages < 0) sync_pages = od_plan_sync(c, s, fid, page, page, page + 1);
+    return fetch_span_od(c, s, fid, page, sync_pages, span_out);
+  }
   const int64_t pg = c.page_size;
-  int64_t span, n;
-  if (s.ar_pending && s.ar_fid == fid && s.ar_page == page) {  // adopt the readahead
-    span = s.ar_span;
-    n = rpc_wait(c, s, fid, page * pg, s.ar_seq, s.ar_pos, s.ar_half);
-    s.ar_pending = 0;
-    s.span_half = s.ar_half;
-  } else {
-    if (drain_readahead(c, s) < 0) return -1;
-    span = rpc_span(c, s, fid, page, seg_end);
-    const int h = c.landing_halves > 1 ? (s.span_half ^ 1) : 0;
-    n = span > 0 ? rpc_call(c, s, fid, page * pg, span, h) : 0;
-    if (n >= 0) {
-      log_rec(c, GFS_LOG_RPCS, s.tb, fid, page * pg, span);
-      ST(rpc_count)++;
-      ST(rpc_requested_bytes) += span;
-    }
-    s.span_half = h;
+  int h = 0;
+  if (c.readahead == GFS_RA_ONDEMAND && (h = od_pick_half(c, s, -1)) < 0) return -1;  // non-RO file
+  const int64_t span = rpc_span(c, s, fid, page, seg_end);
+  const int64_t n = span > 0 ? rpc_call(c, s, fid, page * pg, span, h) : 0;
+  if (n >= 0) {
+    log_rec(c, GFS_LOG_RPCS, s.tb, fid, page * pg, span);
+    ST(rpc_count)++;
+    ST(rpc_requested_bytes) += span;
+    account_transfer(c, s, n);
   }
+  s.span_half = h;
   *span_out = span;
-  if (n < 0) return -1;
-  account_transfer(c, s, n);
-  if (c.async_ra && n > 0 && n == span) {
-    const int64_t next = page + (n + pg - 1) / pg;
-    if (next * pg < seg_end && next * pg < c.files[fid].size) {
-      const int64_t span2 = rpc_span(c, s, fid, next, seg_end);
-      if (span2 > 0) {
-        const int h2 = s.span_half ^ 1;
-        uint32_t seq;
-        unsigned long long pos;
-        if (!wait_landed(c, s, h2, s.st_n[h2])) return -1;
-        if (!rpc_submit(c, s, fid, next * pg, span2, h2, &seq, &pos)) return -1;
-        log_rec(c, GFS_LOG_RPCS, s.tb, fid, next * pg, span2);
-        ST(rpc_count)++;
-        ST(rpc_requested_bytes) += span2;
-        s.ar_pending = 1;
-        s.ar_fid = fid;
-        s.ar_page = next;
-        s.ar_span = span2;
-        s.ar_half = h2;
-        s.ar_seq = seq;
-        s.ar_pos = pos;
-      }
-    }
-  }
   return n;
 }
 
@@ -992,10 +1319,6 @@ __device__ int copy_page_in(uint8_t* frame, uint8_t* dst_whole, const uint8_t* s
 // per-page walk would produce for the same TB; only pages that are hits, in flight or
 // raced by another TB take the per-page path.
 
-__device__ __forceinline__ bool pb_has(const Smem& s, int64_t fid, int64_t page) {
-  const int64_t i = page - s.pb_base;
-  return s.pb_count > 0 && fid == s.pb_fid && i >= 1 && i <= s.pb_count && pb_present(s, i);
-}
 
 // Reserve n consecutive log records (one atomic); ~0 when logging is off / full.
 __device__ unsigned long long log_reserve(const DevCtx& c, int kind, int n) {
@@ -1151,6 +1474,17 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
   uint32_t* pt = F.pt;
   uint64_t t_start = 0;
   if (tid == 0) t_start = globaltimer();
+  if (c.readahead == GFS_RA_ONDEMAND) {  // markers and pending windows at the walk position
+    if (tid == 0) {
+      if (!od_top(c, s, fid, p0)) set_error(c, ERR_IO, (int)fid, (unsigned long long)p0);
+      s.abort = has_error(c);
+    }
+    __syncthreads();
+    if (s.abort) return -1;  // block-uniform
+    pull_span<BS>(c, s);     // an adopted window pulled by the CTA (bounce / mapped)
+    span_buf = span_base(c, s);
+    if (s.od.cap - p0 < nmax) nmax = (int)(s.od.cap - p0);
+  }
 
   // (A) warp 0: look up and claim the leading run of uncached pages
   if (w0) {
@@ -1168,8 +1502,12 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
   // (B) thread 0: how many of them this batch can serve, and their frames
   if (tid == 0) {
     int kp = 1;
+    s.b.sync_m = -1;
     if (pb_has(s, fid, p0)) {
       kp = max(1, pb_run(s, fid, p0, kc));
+    } else if (c.readahead == GFS_RA_ONDEMAND && F.read_only) {
+      s.b.sync_m = od_plan_sync(c, s, fid, p0, p0, p0 + kc);  // the request's decision first
+      kp = (int)min((int64_t)kc, max((int64_t)1, s.b.sync_m));
     } else {
       int64_t win;
       const int64_t span = span_peek(c, s, fid, p0, seg_end, &win);
@@ -1245,7 +1583,7 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
       ST(pb_misses)++;
       j0 = 1;
       int64_t span;
-      const int64_t n = fetch_span(c, s, fid, page, seg_end, &span);
+      const int64_t n = fetch_span(c, s, fid, page, seg_end, &span, s.b.sync_m);
       if (n < 0) {
         status = 2;
       } else if (n == 0) {
@@ -1278,7 +1616,7 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
     if (lane >= s.b.j0 && lane < kk) {
       const int64_t i = p0 + lane - s.pb_base;
       s.b.nb[lane] = (int32_t)(i == s.pb_count ? s.pb_last_nb : pg);
-      s.b.src_off[lane] = i * pg;
+      s.b.src_off[lane] = i * pg - s.pb_off_adj;
     }
     if (lane < kk) c.fkey[s.b.frame[lane]] = page_key(fid, p0 + lane);
     __syncwarp();
@@ -1509,7 +1847,8 @@ __device__ int64_t gread_hits(const DevCtx& c, Smem& s, int64_t fid, int64_t g_p
   const int64_t pg = c.page_size, fs = F.size;
   const int64_t p0 = g_pos / pg;
   const int64_t lim = g_end < fs ? g_end : fs;
-  const int nmax = (int)min((int64_t)32, (lim + pg - 1) / pg - p0);
+  int nmax = (int)min((int64_t)32, (lim + pg - 1) / pg - p0);
+  if (c.readahead == GFS_RA_ONDEMAND && s.od.cap - p0 < nmax) nmax = (int)(s.od.cap - p0);  // markers
   if (w0) {
     bool ok = false;
     uint32_t f = 0;
@@ -1606,7 +1945,13 @@ __device__ int64_t gread(const DevCtx& c, Smem& s, int64_t fid, int64_t offset, 
   const DevFile& F = c.files[fid];
   const int64_t fs = F.size;
   const uint8_t* span_buf = span_base(c, s);
-  if (tid == 0) ST(greads)++;
+  if (tid == 0) {
+    ST(greads)++;
+    s.g_lo = offset;
+    s.g_hi = offset + size;
+    s.g_la = c.lookahead && (offset % pg) == 0 && (c.request_bytes % pg) == 0;
+    if (c.readahead == GFS_RA_ONDEMAND && fid != s.od.fid) od_reset(s, fid);  // a new stream
+  }
 
   if (c.raw_mode) {  // gpu_exec.py:114-119, 131-138: whole request, no page cache
     if (tid == 0) {
@@ -1717,6 +2062,10 @@ __device__ int64_t gread(const DevCtx& c, Smem& s, int64_t fid, int64_t offset, 
       }
       if (miss) {
         ST(pc_misses)++;
+        // ondemand: decision + synchronous span before the frame allocation may evict pages
+        int64_t sync_m = -1;
+        if (c.readahead == GFS_RA_ONDEMAND && F.read_only && !pb_has(s, fid, page))
+          sync_m = od_plan_sync(c, s, fid, page, page, page + 1);
         const uint64_t ta = globaltimer();
         ST(lookup_ns) += (long long)(ta - t0);
         f = c.policy == GFS_POLICY_GLOBAL_LRU ? alloc_global(c, s) : alloc_per_tb(c, s);
@@ -1728,10 +2077,10 @@ __device__ int64_t gread(const DevCtx& c, Smem& s, int64_t fid, int64_t offset, 
           if (nb > 0) {
             act = A_PBHIT;
             s.nb = nb;
-            s.src_off = (page - s.pb_base) * pg;
+            s.src_off = (page - s.pb_base) * pg - s.pb_off_adj;
           } else {
             int64_t span;
-            int64_t n = fetch_span(c, s, fid, page, seg_end, &span);
+            int64_t n = fetch_span(c, s, fid, page, seg_end, &span, sync_m);
             if (n >= 0) {
               act = A_RPC;
               s.n = n;
@@ -2310,6 +2659,8 @@ __device__ bool run_tb(const DevCtx& c, Smem& s, float* cons_smem, int tb, int& 
     s.ra_win = 0;
     s.ra_next_fid = -1;
     s.ra_next_page = -1;
+    s.pb_off_adj = 0;
+    od_reset(s, -1);
     s.last_gfifo_pos = -1;
     s.la_fid = -1;
     s.la_lo = s.la_hi = 0;
@@ -2329,6 +2680,11 @@ __device__ bool run_tb(const DevCtx& c, Smem& s, float* cons_smem, int tb, int& 
       __syncthreads();
       if (tid == 0) s.la_fid = -1;
       __syncthreads();
+    }
+    if (tid == 0) {  // the requests of this segment start at base + k * request_bytes
+      s.seg_lo = base;
+      s.seg_hi = base + len;
+      s.seg_ord = sg - s0;
     }
     int64_t seg_off = 0;
     while (seg_off < len) {
@@ -2354,7 +2710,7 @@ __device__ bool run_tb(const DevCtx& c, Smem& s, float* cons_smem, int tb, int& 
   // TB done: drain the private buffer, retire own frames (pages stay hittable)
   __shared__ unsigned long long ret_pos;
   if (tid == 0) {
-    if (drain_readahead(c, s) < 0) set_error(c, ERR_IO, -1, 0);
+    if (od_drain_all(c, s) < 0) set_error(c, ERR_IO, -1, 0);
     ST(pb_discarded_bytes) += s.pb_filled;
     s.pb_filled = 0;
     s.pb_count = 0;
@@ -2381,7 +2737,8 @@ __global__ void __launch_bounds__(BS, 4) gread_driver(DevCtx c) {
     for (int i = 0; i < GFS_NSTATS; i++) s.st[i] = 0;
     s.pull_n = 0;
     s.span_half = 0;
-    s.ar_pending = 0;
+    s.hp[0].pending = s.hp[1].pending = 0;
+    s.hp_age = 0;
     s.st_seq[0] = s.st_seq[1] = 0;
     s.st_n[0] = s.st_n[1] = 0;
     s.st_landed[0] = s.st_landed[1] = 0;

@@ -75,7 +75,7 @@ struct DevCtx {
   int64_t page_size;
   int64_t prefetch_bytes;
   int64_t ra_max_bytes;
-  int64_t ra_init_bytes;     // adaptive first window (>= page + prefetch, <= ra_max)
+  int64_t ra_init_bytes;     // doubling first window (>= page + prefetch, <= ra_max)
   int64_t pb_cap_bytes;      // private-buffer capacity (bytes)
   int64_t slot_bytes;        // span buffer bytes per CTA slot
   int64_t staging_bytes;     // PCIe batch accounting unit
@@ -86,8 +86,8 @@ struct DevCtx {
   int32_t policy, readahead, transfer, raw_mode, log, verify, pcie_disabled, timeline;
   int32_t tma;               // K1 by TMA bulk copies through the shared-memory stage ring
   int32_t lookahead;         // batches may run past a page-aligned request (gpu.lookahead)
-  int32_t async_ra;          // submit the next window while the current one is consumed
-  int32_t landing_halves;    // landing slots per CTA (2 with async readahead)
+  int32_t ra_clamp;          // ondemand windows end at EOF or at the TB's segment end
+  int32_t landing_halves;    // landing slots per CTA (2 with ondemand readahead)
   int32_t stream_pieces;     // copy-engine windows land piece by piece (landed markers)
   int64_t stream_piece;      // piece bytes (windows of >= 2 pieces are streamed)
   unsigned long long* landed;  // [n_ctas * landing_halves]: (4 KiB pages landed << 32) | seq
@@ -123,7 +123,7 @@ struct DevCtx {
   // which restores device memory but not the daemon's progress.
   const unsigned long long* host_served;
   RpcResp* resp;
-  uint8_t* staging;          // [n_ctas][slot_bytes] (zerocopy span buffers)
+  uint8_t* staging;          // [n_ctas][landing_halves][slot_bytes] (zerocopy span buffers)
   // DMA mode (device)
   uint8_t* landing;          // [n_ctas][slot_bytes]
   unsigned long long* doorbell; // [n_ctas] (nbytes << 32 | seq), written by cuStreamWriteValue64

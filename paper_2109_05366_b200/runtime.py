@@ -63,7 +63,7 @@ def native_config(cfg: ExperimentConfig, max_request_bytes: int = 0) -> native.G
     c.k1_tma = int(cfg["gpu.k1_copy"] == "tma")
     c.numa_pin = int(bool(cfg["io.numa_pin"]))
     c.lookahead = int(bool(cfg["gpu.lookahead"]))
-    c.async_ra = int(bool(cfg["io.async_readahead"]))
+    c.ra_clamp = native.RA_CLAMP[cfg["io.ra_clamp"]]
     return c
 
 

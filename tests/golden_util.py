@@ -110,3 +110,38 @@ def compare(g: dict, stats: dict, deliveries, rpcs, victims, *, exact_victims=Tr
         if got_v.shape != want_v.shape or not np.array_equal(got_v, want_v):
             errs.append(f"victim log differs ({len(got_v)} vs {len(want_v)})")
     return errs
+
+
+# ---- readahead-law fixtures (tests/golden/windows, made by make_windows.py) ----
+
+WINDOW_DIR = os.path.join(GOLDEN_DIR, "windows")
+
+
+def window_case_names() -> list[str]:
+    return sorted(os.path.splitext(os.path.basename(p))[0]
+                  for p in glob.glob(os.path.join(WINDOW_DIR, "*.json")))
+
+
+def window_case(name: str, **extra):
+    """(fixture, config, workload) replaying a reference HostOs read stream as one TB whose
+    program is the read list (one segment = one gread each), ondemand readahead with the
+    reference's EOF clamp, a cache larger than the file (the reference host cache never
+    evicts here)."""
+    from paper_2109_05366_b200.workloads import WorkloadSpec, union_bytes
+    with open(os.path.join(WINDOW_DIR, f"{name}.json")) as fh:
+        g = json.load(fh)
+    reads = [tuple(r) for r in g["reads"]]
+    req = max(sz for _, sz in reads)
+    fb = g["file_bytes"]
+    cache = max(4 << 20, (fb + 2 * g["ra_max"] + (1 << 20)) // (1 << 20) * (1 << 20))
+    over = {"gpufs.page_size": g["page"], "gpufs.prefetch_bytes": 0, "gpufs.cache_bytes": cache,
+            "gpufs.policy": "per-tb-lra", "io.readahead": "adaptive", "io.ra_clamp": "eof",
+            "io.ra_max_bytes": g["ra_max"], "gpu.sm_count": 1, "gpu.threads_per_tb": 2048,
+            "mode.deterministic": True, "workload.request_bytes": req}
+    over.update(extra)
+    cfg = ExperimentConfig(over)
+    prog = [(0, off, min(sz, fb - off)) for off, sz in reads if off < fb]
+    wl = WorkloadSpec(name=f"window_{name}", files={0: fb}, read_only={0: True}, programs=[prog],
+                      request_bytes=req, total_bytes=sum(ln for _, _, ln in prog),
+                      unique_bytes=union_bytes([prog]))
+    return g, cfg, wl

@@ -41,7 +41,7 @@ def random_case(k: int) -> dict:
         "gpufs.page_size": page, "gpufs.prefetch_bytes": page * r.below(8),
         "gpufs.cache_bytes": frames * page,
         "gpufs.policy": ["global-lru-dealloc", "per-tb-lra"][r.below(2)],
-        "io.readahead": ["static", "adaptive"][r.below(2)],
+        "io.readahead": ["static", "adaptive", "doubling"][r.below(3)],
         "io.ra_max_bytes": page * (1 << (2 + r.below(4))),
         "gpu.dispatch_order": ["round-robin", "shuffled", "reverse"][r.below(3)],
         "gpu.sm_count": 1, "gpu.max_threads_per_sm": 2048, "gpu.threads_per_tb": 2048,

@@ -59,7 +59,7 @@ def test_golden_case_on_device(name, transfer, synth_dir):
 
 
 @pytest.mark.parametrize("policy", ["per-tb-lra", "global-lru-dealloc"])
-@pytest.mark.parametrize("readahead", ["static", "adaptive"])
+@pytest.mark.parametrize("readahead", ["static", "adaptive", "doubling"])
 def test_pressure_many_waves_vs_oracle(policy, readahead, synth_dir):
     """File 4x the cache, n_tb > resident CTAs (retired-frame reclaim is exercised);
     counts, per-TB deliveries and RPC traces must equal the oracle's."""
@@ -80,16 +80,16 @@ def test_pressure_many_waves_vs_oracle(policy, readahead, synth_dir):
         assert st[k] == ref_log.stats[k], k
     assert np.array_equal(gu.by_tb(sim.result.deliveries), gu.by_tb(ref_log.deliveries))
     assert np.array_equal(gu.by_tb(sim.result.rpcs), gu.by_tb(ref_log.rpcs))
-    if readahead == "adaptive":
+    if readahead != "static":
         assert np.array_equal(gu.by_tb(sim.result.windows), gu.by_tb(ref_log.windows))
         assert st["rpc_count"] < 96 * (1 * MiB // (64 * KiB))
     assert sim.checksum == want_sum
     assert st["word_mismatches"] == 0
 
 
-def test_adaptive_window_law_single_stream(synth_dir):
+def test_doubling_window_law_single_stream(synth_dir):
     over = {"workload.n_tb": 1, "workload.file_bytes": 8 * MiB, "gpufs.prefetch_bytes": 60 * KiB,
-            "io.readahead": "adaptive", "io.ra_max_bytes": 1 * MiB, "gpufs.cache_bytes": 16 * MiB,
+            "io.readahead": "doubling", "io.ra_max_bytes": 1 * MiB, "gpufs.cache_bytes": 16 * MiB,
             "io.ra_init_bytes": 64 * KiB}  # explicit: auto depends on the transfer mode
     sim, rep = run_sim(over, 1, synth_dir)
     w = [int(x) for x in sim.result.windows[:, 1]]
@@ -234,7 +234,9 @@ def test_timeline_log(synth_dir):
 
 
 @pytest.mark.parametrize("request_bytes,readahead", [(4 * KiB, "static"), (16 * KiB, "adaptive"),
-                                                      (64 * KiB, "static"), (10_000, "static")])
+                                                      (4 * KiB, "adaptive"), (64 * KiB, "adaptive"),
+                                                      (16 * KiB, "doubling"), (64 * KiB, "static"),
+                                                      (10_000, "static"), (10_000, "adaptive")])
 def test_lookahead_is_invisible(request_bytes, readahead, synth_dir):
     """gpu.lookahead (batches running past page-aligned requests) changes nothing the
     reference can observe: counters, per-TB deliveries, RPC traces, victims and the user
@@ -255,34 +257,36 @@ def test_lookahead_is_invisible(request_bytes, readahead, synth_dir):
               "rpc_count", "rpc_requested_bytes", "pc_allocs", "pc_remaps", "victims",
               "pb_filled_bytes", "pb_discarded_bytes", "pb_consumed_bytes", "cache_hit_user_bytes"):
         assert a.result.stats[k] == b.result.stats[k], k
-    for log in ("deliveries", "rpcs", "victims"):
+    for log in ("deliveries", "rpcs", "victims", "windows"):
         assert np.array_equal(getattr(a.result, log), getattr(b.result, log)), log
     assert a.checksum == b.checksum and a.mismatched_words == b.mismatched_words == 0
 
 
-@pytest.mark.parametrize("transfer", ["mapped_dma", "dma"])
-@pytest.mark.parametrize("n_tb,ra_max", [(8, 256 * KiB), (48, 1 * MiB), (192, 512 * KiB)])
-def test_async_readahead_is_invisible(transfer, n_tb, ra_max, synth_dir):
-    """io.async_readahead submits each next window while the current one is consumed; the
-    requests, windows, private-buffer accounting and bytes are those of the synchronous
-    walk (sequential strides: every readahead is adopted), and the user buffer verifies."""
-    from paper_2109_05366_b200.runtime import Simulation
-    over = {"workload.n_tb": n_tb, "workload.file_bytes": 48 * MiB, "workload.request_bytes": 64 * KiB,
+@pytest.mark.parametrize("transfer", ["mapped_dma", "dma", "mapped", "bounce", "zerocopy", "mapped_hybrid"])
+@pytest.mark.parametrize("n_tb,ra_max,req", [(8, 256 * KiB, 64 * KiB), (48, 1 * MiB, 64 * KiB),
+                                             (192, 512 * KiB, 16 * KiB)])
+def test_ondemand_readahead_vs_oracle(transfer, n_tb, ra_max, req, synth_dir):
+    """The ondemand law (io.readahead=adaptive) under every transfer, many TBs at once:
+    window log, RPC trace and deliveries per TB, every counter, and the user buffer equal the
+    oracle's (asynchronous windows land in the other landing half while the TB reads one;
+    under bounce they are requested when adopted — same requests, same bytes)."""
+    over = {"workload.n_tb": n_tb, "workload.file_bytes": 48 * MiB, "workload.request_bytes": req,
             "gpufs.prefetch_bytes": 60 * KiB, "gpufs.cache_bytes": 16 * MiB, "gpufs.policy": "per-tb-lra",
             "gpu.sm_count": 16, "io.readahead": "adaptive", "io.ra_max_bytes": ra_max,
-            "io.ra_init_bytes": 64 * KiB, "io.transfer": transfer, "io.dir": synth_dir, "io.workers": 8}
-    res = []
-    for ar in (True, False):
-        sim = Simulation(ExperimentConfig({**over, "io.async_readahead": ar}), 42)
-        rep = sim.run()
-        res.append((sim, rep))
-    (a, ra), (b, rb) = res
-    for k in ("user_bytes", "greads", "pc_misses", "pb_hits", "pb_misses", "rpc_count",
-              "rpc_requested_bytes", "pc_allocs", "pc_remaps", "victims", "pb_filled_bytes",
-              "pb_discarded_bytes", "pcie_bytes"):
-        assert a.result.stats[k] == b.result.stats[k], k
-    assert a.checksum == b.checksum and a.mismatched_words == b.mismatched_words == 0
-    assert ra["user_bytes"] == 48 * MiB
+            "io.transfer": transfer}
+    sim, rep = run_sim(over, 42, synth_dir)
+    cfg = ExperimentConfig({**over, "io.dir": synth_dir})
+    want_sum, _ = oracle_checksum(cfg, 42)
+    ref = orc.run_oracle(cfg, build_workload(cfg))
+    st = sim.result.stats
+    for k in ("user_bytes", "greads", "pc_lookups", "pc_misses", "pc_hits", "pb_hits", "pb_misses",
+              "rpc_count", "rpc_requested_bytes", "pc_allocs", "pc_remaps", "victims", "pb_filled_bytes",
+              "pb_consumed_bytes", "pb_discarded_bytes", "pcie_bytes", "pcie_transfers"):
+        assert st[k] == ref.stats[k], (k, st[k], ref.stats[k])
+    for log in ("deliveries", "rpcs", "windows"):
+        assert np.array_equal(gu.by_tb(getattr(sim.result, log)), gu.by_tb(getattr(ref, log))), log
+    assert sim.checksum == want_sum and sim.mismatched_words == 0 and st["word_mismatches"] == 0
+    assert rep["user_bytes"] == 48 * MiB and st["pcie_bytes"] == 48 * MiB  # nothing fetched twice
 
 
 def test_reference_acceptance_criteria_on_hardware(synth_dir):
@@ -311,7 +315,7 @@ def test_reference_acceptance_criteria_on_hardware(synth_dir):
 @pytest.mark.timeout(900)
 def test_headline_config_full_size_against_oracle():
     """BASELINE configs[1] at full size (16 GiB file, 4 GiB cache, 1024 TBs, per-tb-lra,
-    adaptive windows, the bench's transfer): every counter equals the oracle's run of the
+    ondemand readahead, the bench's transfer): every counter equals the oracle's run of the
     same 16 GiB workload, every delivered word verifies against the content law, and the
     closed forms hold (each page missed once, frames allocated once, the rest remapped)."""
     import shutil
@@ -383,7 +387,7 @@ def test_lookahead_segment_boundary_many_tbs(transfer, k1, synth_dir):
     table = ProgramTable.from_programs([[(0, t * stride, stride)] * 2 for t in range(n_tb)])
     cfg = ExperimentConfig({"gpufs.cache_bytes": 2 * size, "gpufs.prefetch_bytes": 60 * KiB,
                             "gpufs.policy": "per-tb-lra", "io.dir": synth_dir, "io.transfer": transfer,
-                            "io.readahead": "adaptive", "io.ra_init_bytes": 512 * KiB,
+                            "io.readahead": "adaptive", "io.ra_max_bytes": 512 * KiB,
                             "gpu.k1_copy": k1, "gpu.lookahead": True, "mode.verify": True,
                             "workload.request_bytes": req})
     with GpuFS(cfg, max_request_bytes=req) as fs:

@@ -48,7 +48,7 @@ def random_case(k: int):
         "gpufs.prefetch_bytes": page * r.below(16),
         "gpufs.cache_bytes": [256 * MiB, 1024 * MiB, 4096 * MiB][r.below(3)],
         "gpufs.policy": "global-lru-dealloc" if r.below(6) == 0 else "per-tb-lra",
-        "io.readahead": ["static", "adaptive"][r.below(2)],
+        "io.readahead": ["static", "adaptive", "doubling"][r.below(3)],
         "io.ra_max_bytes": page << (4 + r.below(9)),
         "io.transfer": TRANSFERS[k % len(TRANSFERS)],
         "gpu.k1_copy": ("tma", "ldg")[(k // len(TRANSFERS)) % 2],
