@@ -49,8 +49,9 @@ enum { GFS_RA_CLAMP_SEGMENT = 0, GFS_RA_CLAMP_EOF = 1 };
  *          pinned page-cache mapping into the HBM landing slot (no CPU copy);
  * mapped = memory-resident files: the daemon only answers the RPC, the CTA pulls the span
  *          from the pinned page-cache mapping into its HBM landing slot itself;
- * mapped_hybrid = mapped, but spans of >= 1 MiB go by copy engine (mapped_dma): SM pulls
- *          cap at ~51.5 GB/s on PCIe Gen5 x16, large copy-engine copies reach ~55 */
+ * mapped_hybrid = mapped, but spans of >= 4 MiB go by copy engine (mapped_dma): SM pulls
+ *          cap at ~51.5 GB/s on PCIe Gen5 x16, large copy-engine copies reach ~55, small
+ *          copy-engine copies pay a fixed cost each */
 enum { GFS_XFER_ZEROCOPY = 0, GFS_XFER_DMA = 1, GFS_XFER_BOUNCE = 2, GFS_XFER_MAPPED = 3,
        GFS_XFER_MAPPED_ZC = 4, GFS_XFER_MAPPED_HYBRID = 5 };
 /* gopen flags: read-only files are the only ones prefetched (prefetcher.py:22-24) */

@@ -262,6 +262,7 @@ struct gfs_ctx {
   // calls fail fast instead of timing out against workers parked on stale positions
   bool poisoned = false;
   int downgraded_from = -1;  // copy-engine transfer replaced by its SM-pull sibling (queue probe)
+  int64_t ce_min = 4 << 20;  // mapped_hybrid: spans of at least this many bytes go by copy engine
   // driver entry point resolved through cudart (libgfs does not link libcuda, so it
   // loads on machines without a driver; CUDA calls then fail loudly)
   CUresult (*write_value64)(CUstream, CUdeviceptr, cuuint64_t, unsigned int) = nullptr;
@@ -351,7 +352,7 @@ static void worker_main(gfs_ctx* ctx, int wid) {
   const bool mapped_ce = ctx->cfg.transfer == GFS_XFER_MAPPED;     // copy engine from the mapping
   const bool mapped_zc = ctx->cfg.transfer == GFS_XFER_MAPPED_ZC;  // the CTA pulls it itself
   const bool from_map = mapped_ce || mapped_zc || hybrid;
-  const int64_t ce_min = 1 << 20;  // hybrid: spans this large go by copy engine
+  const int64_t ce_min = ctx->ce_min;  // hybrid: spans this large go by copy engine
   cudaStream_t st = (dma || mapped_ce || hybrid)
                         ? ctx->worker_streams[(size_t)wid % ctx->worker_streams.size()]
                         : nullptr;
@@ -647,6 +648,7 @@ extern "C" int gfs_create(const gfs_config* cfg_in, gfs_ctx** out) {
     // stream risks sharing a hardware queue with the persistent kernel's stream
     int nstreams = 2;
     if (const char* e = getenv("GFS_COPY_STREAMS")) nstreams = std::max(1, std::min(16, atoi(e)));  // experiments
+    if (const char* e = getenv("GFS_CE_MIN_KIB")) ctx->ce_min = std::max(4, atoi(e)) * 1024ll;  // experiments
     ctx->worker_streams.resize((size_t)std::min(cfg.io_workers, nstreams), nullptr);
     for (auto& s : ctx->worker_streams) TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     ctx->bell_streams.resize((size_t)std::min(cfg.io_workers, nstreams), nullptr);

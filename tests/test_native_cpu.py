@@ -123,7 +123,7 @@ def test_checksum_law_python_vs_oracle():
 
 
 def test_auto_transfer_and_first_window_rules(monkeypatch, tmp_path):
-    """auto: tmpfs + adaptive/doubling -> mapped_dma, tmpfs + static -> mapped, disk -> bounce,
+    """auto: tmpfs + adaptive -> mapped_hybrid, + doubling -> mapped_dma, + static -> mapped, disk -> bounce,
     never a copy-engine mode under a kernel profiler; the first copy-engine window is the
     whole cap when TBs outnumber resident slots, the largest power of two below a stride otherwise."""
     from paper_2109_05366_b200 import config as gcfg
@@ -135,7 +135,7 @@ def test_auto_transfer_and_first_window_rules(monkeypatch, tmp_path):
             "gpu.sm_count": 148, "gpu.threads_per_tb": 512, "gpufs.prefetch_bytes": 60 * KiB}
     monkeypatch.setattr(gcfg, "on_tmpfs", lambda p: True)
     c = ExperimentConfig({**base, "io.readahead": "adaptive"})
-    assert c.transfer() == "mapped_dma" and c.ra_max() == 16 * MiB
+    assert c.transfer() == "mapped_hybrid" and c.ra_max() == 16 * MiB
     assert c.ra_init() == 0  # the ondemand law has no first-window knob (4 requests, host_os.py:139)
     d = ExperimentConfig({**base, "io.readahead": "doubling"})
     assert d.transfer() == "mapped_dma" and d.ra_init() == d.ra_max() == 16 * MiB
