@@ -44,12 +44,26 @@ def parse():
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    p.add_argument("--size-gib", type=float, default=16.0, help="bytes per GPU")
+    p.add_argument("--size-gib", type=float, default=16.0, help="bytes per GPU (weak scaling)")
+    p.add_argument("--total-gib", type=float, default=None,
+                   help="bytes over all GPUs (strong scaling); default 64 (configs[4]) when N > 1")
     p.add_argument("--quick", action="store_true", help="headline only: skip comparison arms")
     p.add_argument("--set", action="append", default=[], metavar="KEY=VALUE")
     p.add_argument("--dir", default="/dev/shm")
     p.add_argument("--no-clocks", action="store_true", help="skip nvidia-smi sampling")
     return p.parse_args()
+
+
+def shard_plan(total_gib, size_gib: float, world: int):
+    """(total GiB or None, scaling, bytes per GPU).  N > 1 defaults to configs[4]: a 64 GiB
+    file split into 64/N GiB contiguous shards (strong scaling); --size-gib fixes the bytes
+    per GPU instead (weak scaling).  Shards are whole multiples of 64 MiB (1024 strides of
+    whole 64 KiB requests)."""
+    if total_gib is None and world > 1:
+        total_gib = 64.0
+    if total_gib is None:
+        return None, "weak", int(size_gib * GiB)
+    return total_gib, "strong", int(total_gib * GiB) // world // (64 * MiB) * (64 * MiB)
 
 
 def headline_overrides(size: int, n_gpus: int, directory: str) -> dict:
@@ -200,7 +214,6 @@ def fit_size(directory: str, size: int, n: int) -> int:
     """Bytes per GPU such that the n-shard file fits the file system holding it (an
     existing file of the right size counts as free); whole GiB, at least 1 GiB.  Logged
     when it has to shrink the shard."""
-    from paper_2109_05366_b200.runtime import SYNTH_VERSION  # noqa: F401
     try:
         st = os.statvfs(directory)
     except OSError:
@@ -281,11 +294,68 @@ def run_arm(cfg, path: str, rank: int, device: int, steps: int, warmup: int, dst
         mism = fs.verify(table, dst) if cfg["mode.verify"] else None
         csum = fs.checksum(dst, table.dst_bytes)
         ctas = fs.resident_ctas
+        transfer, fallback = fs.transfer, fs.fallback
     finally:
         fs.close()
     return {"stats": stats, "walls": walls, "table": table, "wl": wl, "mismatched_words": mism,
             "checksum": csum, "ctas": ctas, "clocks": sampler.summary() if sampler else None,
-            "dst": dst}
+            "dst": dst, "transfer": transfer, "fallback": fallback}
+
+
+def storage_label(cfg, transfer: str) -> str:
+    """Where the bytes come from and how the host serves them, per transfer."""
+    d = cfg["io.dir"]
+    how = {"mapped_dma": "pinned page-cache mapping, copy engine (no pread)",
+           "mapped": "pinned page-cache mapping, pulled by the CTA (no pread)",
+           "mapped_hybrid": "pinned page-cache mapping: windows >= 4 MiB by copy engine, smaller "
+                            "pulled by the CTA (no pread)",
+           "bounce": "O_DIRECT pread into a pinned pool, pulled by the CTA",
+           "dma": "O_DIRECT pread into a pinned pool, cudaMemcpyAsync to HBM",
+           "zerocopy": "O_DIRECT pread into per-CTA pinned staging, pulled by the CTA"}
+    fs = "tmpfs" if cfg["mode.ramfs"] else "disk"
+    return f"{fs} {d}: {how.get(transfer, transfer)}"
+
+
+def pread_daemon_line(arms: dict, io_peak) -> dict | None:
+    """The north_star data path (O_DIRECT pread -> pinned staging -> HBM) as a first-class
+    number beside the headline: the better of the bounce and dma arms, against the same
+    roofline."""
+    cands = {k: arms[k] for k in ("pread_bounce_adaptive", "pread_dma_adaptive")
+             if k in arms and "gbps" in arms[k]}
+    if not cands:
+        return None
+    name, a = max(cands.items(), key=lambda kv: kv[1]["gbps"])
+    return {"value": a["gbps"], "unit": "GB/s", "arm": name, "e2e": a["e2e_gbps"],
+            "roofline_frac": round(a["gbps"] / io_peak, 4) if io_peak else None,
+            "all": {k: v["gbps"] for k, v in cands.items()}}
+
+
+def cold_open_e2e(cfg, path: str, rank: int, device: int, dst) -> dict:
+    """One pass through the public API from a cold context: create the GpuFS, gopen (for the
+    mapped transfers: mmap + pin the shard's page-cache pages on the first run), run, close —
+    the setup a one-shot user pays, which the per-step e2e amortises away."""
+    import torch
+    from paper_2109_05366_b200.runtime import GpuFS
+    wl, table = shard_table(cfg, rank)
+    torch.cuda.synchronize(device)
+    t0 = time.perf_counter()
+    with GpuFS(cfg, max_request_bytes=wl.request_bytes) as fs:
+        fs.gopen(path, content_id=0)
+        r = fs.run(table, wl.request_bytes, dst)
+    el = time.perf_counter() - t0
+    nbytes = r.stats["user_bytes"]
+    return {"value": round(gbps(nbytes, el), 3), "unit": "GB/s", "seconds": round(el, 3),
+            "kernel_seconds": round(r.stats["kernel_ns"] / 1e9, 3),
+            "note": "create + gopen + first run (pins the mapped range) + close"}
+
+
+def topology() -> list | None:
+    """nvidia-smi topo -m of this box (PCIe / NUMA placement behind the aggregate roofline)."""
+    try:
+        out = subprocess.run(["nvidia-smi", "topo", "-m"], capture_output=True, text=True, timeout=30).stdout
+    except (OSError, subprocess.TimeoutExpired):
+        return None
+    return [ln.rstrip() for ln in out.splitlines() if ln.strip() and not ln.startswith("Legend")][:20]
 
 
 def gbps(nbytes: float, seconds: float) -> float:
@@ -388,34 +458,143 @@ def workload_label(size: int, cfg) -> str:
 
 
 # ------------------------------------------------------------------ reference arm
+#
+# Nothing on this arm imports the product package (paper_2109_05366_b200) or loads libgfs:
+# the input file comes from the oracle's generator, the TB programs from the reference's
+# own gen_sequential_strided (baseline/_ref, installed from /root/reference), and the timed
+# work is the reference algorithm restated in C (oracle/gfs_oracle.c) doing real O_DIRECT
+# preads — the reference itself is a pure-Python simulator with no compiled path.
+
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+# the headline configuration as the b200 arm resolves it (bench.headline_overrides with
+# io.ra_max_bytes / io.transfer auto on tmpfs: the ondemand law, 16 MiB windows)
+REF_PARAMS = {"page_size": 4 * KiB, "cache_bytes": 4 * GiB, "prefetch_bytes": 60 * KiB,
+              "request_bytes": 64 * KiB, "staging_bytes": 2 * MiB, "ra_max_bytes": 16 * MiB,
+              "ra_init_bytes": 0, "policy": "per-tb-lra", "resident_limit": 592,
+              "readahead": "adaptive", "ra_clamp": "segment", "n_tb": 1024}
+
+
+def import_reference():
+    """gpuiosim from baseline/_ref (the unmodified reference package), or None."""
+    if os.path.isdir(REF_DIR) and REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    try:
+        import gpuiosim.workloads  # noqa: F401
+        import gpuiosim.simulation  # noqa: F401
+        import gpuiosim.config  # noqa: F401
+        return sys.modules["gpuiosim"]
+    except ImportError:
+        return None
+
+
+def python_reference_timing() -> dict:
+    """The reference Python implementation itself timed on this box's host cores:
+    Simulation(C1, 42).run() (simulation.py:98-242) for the prefetch + per-tb-lra, prefetch +
+    global-lru-dealloc and no-prefetch arms of configs[0] (256 MiB, 128 TBs, 64 KiB requests,
+    4 KiB pages, 512 MiB cache).  One core (a single-threaded event loop); GB/s here is
+    simulated user bytes per wall second, beside the reference's own simulated bandwidth."""
+    ref = import_reference()
+    if ref is None:
+        return {"unavailable": f"gpuiosim not installed under {os.path.relpath(REF_DIR, ROOT)}"}
+    from gpuiosim.config import ExperimentConfig as RefConfig
+    from gpuiosim.simulation import Simulation as RefSimulation
+    base = {"workload.file_bytes": 256 * MiB, "workload.n_tb": 128, "workload.request_bytes": 64 * KiB,
+            "gpufs.page_size": 4 * KiB, "gpufs.cache_bytes": 512 * MiB, "repetitions": 1}
+    arms = {}
+    for name, over in (("prefetch_per_tb_lra", {"gpufs.prefetch_bytes": 60 * KiB, "gpufs.policy": "per-tb-lra"}),
+                       ("prefetch_global", {"gpufs.prefetch_bytes": 60 * KiB}),
+                       ("no_prefetch", {"gpufs.prefetch_bytes": 0})):
+        t0 = time.perf_counter()
+        rep = RefSimulation(RefConfig({**base, **over}), 42).run()
+        el = time.perf_counter() - t0
+        arms[name] = {"wall_s": round(el, 3), "user_bytes": rep["user_bytes"],
+                      "wall_gbps": round(gbps(rep["user_bytes"], el), 4),
+                      "simulated_io_gbps": round(rep["io_bandwidth_bps"] / 1e9, 3),
+                      "rpc_count": rep["rpc_count"]}
+    return {"impl": "gpuiosim (reference, unmodified, baseline/_ref)", "config": "configs[0] = C1: "
+            "256 MiB file, 128 TBs, 64 KiB requests, 4 KiB pages, 512 MiB cache, seed 42",
+            "cores": os.cpu_count(), "cores_used": 1, "arms": arms}
+
 
 def reference_main(args, dist: Dist) -> None:
     if dist.rank != 0:
         return
-    from paper_2109_05366_b200.runtime import ensure_synthetic
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as orc
     # rank 0 alone (the other ranks have already left): no barriers from here on; the CPU
     # implementation reads one GPU's shard of the workload
     size = fit_size(args.dir, int(args.size_gib * GiB), 1)
-    cfg = make_cfg(headline_overrides(size, 1, args.dir), args.set)
-    path = ensure_synthetic(cfg["io.dir"], 0, cfg["workload.file_bytes"])
+    path = os.path.join(args.dir, f"gfs_synth_c0_{size}.bin")
+    ok = path + ".ok"
+    if not (os.path.exists(path) and os.path.getsize(path) == size and os.path.exists(ok)
+            and open(ok).read().strip() == orc.SYNTH_STAMP):
+        orc.gen_file(path, 0, size)
+    P = dict(REF_PARAMS)
+    n_tb = P.pop("n_tb")
+    ref = import_reference()
+    if ref is not None:  # the reference's own program generator (workloads.py:66-81)
+        programs = ref.workloads.gen_sequential_strided([size], n_tb, size, P["request_bytes"],
+                                                        P["page_size"]).programs
+        prog_src = "gpuiosim.workloads.gen_sequential_strided (baseline/_ref)"
+    else:
+        stride = size // n_tb
+        programs = [[(0, t * stride, stride)] for t in range(n_tb)]
+        prog_src = "restated strides (reference package not installed)"
     threads = os.cpu_count() or 1
-    sample = size  # the whole workload per step (~1-2 s on 16 host cores)
+    groups = max(1, min(threads, n_tb))
+    per = n_tb // groups
+
+    def sample(k_groups: int) -> float:
+        """k_groups instances at once, instance g = TBs [g*per, (g+1)*per) with 1/groups of
+        the cache and of the residency; returns seconds."""
+        errs = []
+
+        def one(g):
+            try:
+                segs, po, do, _ = orc.programs_to_arrays(programs[g * per:(g + 1) * per])
+                prm = {**P, "cache_bytes": P["cache_bytes"] // groups,
+                       "resident_limit": max(1, P["resident_limit"] // groups)}
+                orc.run_raw(prm, [size], [True], segs, po, do, list(range(per)), source=orc.SRC_FILES,
+                            paths=[path], io_direct=True, materialize_dst=True, log=False)
+            except Exception as e:  # pragma: no cover
+                errs.append(e)
+        ths = [threading.Thread(target=one, args=(g,)) for g in range(k_groups)]
+        t0 = time.perf_counter()
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+        el = time.perf_counter() - t0
+        if errs:
+            raise errs[0]
+        return el
+
+    orc.lib()
     for _ in range(args.warmup):
-        cpu_oracle_sample(path, cfg, sample // 4, threads)
-    runs = [cpu_oracle_sample(path, cfg, sample, threads) for _ in range(args.steps)]
-    secs = sum(r["seconds"] for r in runs)
-    nbytes = sum(r["value"] * r["seconds"] * 1e9 for r in runs)
-    v = round(gbps(nbytes, secs), 3)
+        sample(max(1, groups // 4))
+    secs = [sample(groups) for _ in range(args.steps)]
+    nbytes = per * groups * (size // n_tb)
+    v = round(gbps(nbytes * len(secs), sum(secs)), 3)
+    py = python_reference_timing()
+    dec = (f"{groups} independent instances on {threads} host threads, instance g = TBs "
+           f"[{per}g, {per}(g+1)) of the {n_tb} with 1/{groups} of the cache and of the residency")
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": args.gpus,
-           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(secs / len(runs) * 1e3, 3),
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(sum(secs) / len(secs) * 1e3, 3),
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
-           "data": "synthetic", "config": {"workload": workload_label(size, cfg) + ", whole workload per step",
-                                           "sample_bytes": sample},
+           "data": "synthetic",
+           "config": {"workload": f"sequential strided gread, {size / GiB:g} GiB/GPU, cache < file "
+                                  f"(configs[1]), whole workload per step",
+                      "sample_bytes": nbytes, "programs": prog_src, "params": REF_PARAMS,
+                      "decomposition": dec, "same_config": "yes, split into independent instances as stated"},
            "cpu_baseline": {"value": v, "unit": "GB/s", "cores": threads, "kind": "port",
-                            "sample": runs[0]["sample"]},
+                            "sample": f"the whole {size / GiB:g} GiB workload per step: {dec}; "
+                                      f"O_DIRECT preads, bytes materialised in host buffers",
+                            "python_ref": py},
+           "python_reference": py,
            "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-           "note": "reference is a pure-Python simulator (no compiled path); the arm times its C "
-                   "restatement (oracle/gfs_oracle.c) doing real O_DIRECT reads on all host cores"}
+           "note": "the reference is a pure-Python simulator (no compiled path): the arm times its C "
+                   "restatement (oracle/gfs_oracle.c, the reference algorithm) doing real O_DIRECT reads "
+                   "on all host cores; python_reference times the reference package itself on C1"}
     print(json.dumps(out), flush=True)
 
 
@@ -437,15 +616,17 @@ def main() -> None:
     native.load()
     device = dist.local
     torch.cuda.set_device(device)
+    total_gib, scaling, want = shard_plan(args.total_gib, args.size_gib, dist.world)
     if dist.rank == 0:
-        prune_synthetic(args.dir, int(args.size_gib * GiB) * dist.world)
+        prune_synthetic(args.dir, want * dist.world)
     dist.barrier()  # every rank sizes the shard before rank 0 starts writing the file
-    size = int(dist.reduce([float(fit_size(args.dir, int(args.size_gib * GiB), dist.world))], "MIN")[0])
+    size = int(dist.reduce([float(fit_size(args.dir, want, dist.world))], "MIN")[0])
     cfg = make_cfg({**headline_overrides(size, dist.world, args.dir), "gpu.device": device}, args.set)
     path = ensure_file(cfg, dist)
 
     res = run_arm(cfg, path, dist.rank, device, args.steps, args.warmup,
                   sampler_index=None if args.no_clocks else device, dist=dist)
+    cold = cold_open_e2e(cfg, path, dist.rank, device, res["dst"]) if dist.world == 1 and not args.quick else None
     st = res["stats"]
     kernel_s = sum(s["kernel_ns"] for s in st) / 1e9
     wall_s = sum(res["walls"])
@@ -461,6 +642,7 @@ def main() -> None:
     probes = roofline_probes(path, size, device, dist) if not args.quick else {}
     if dist.rank == 0 and dist.world == 1 and not args.quick:
         arms, cpu_base = comparison_arms(cfg, path, device, res, probes)
+    topo = topology() if dist.rank == 0 else None
     if dist.rank != 0:
         dist.close()
         return
@@ -473,20 +655,24 @@ def main() -> None:
     prof = load_profile_summary(cfg.transfer())
     ms_step = kernel_s / len(st) * 1e3
     hbm_alg = 4 * nbytes  # PCIe->frame write, frame/pb read, user-buffer write, span read
+    transfer = res["transfer"]
     out = {
         "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": dist.world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "u8",
         "data": "synthetic",
-        "config": {"workload": workload_label(size, cfg),
+        "config": {"workload": workload_label(size, cfg) + (f", {total_gib:g} GiB over {dist.world} GPUs"
+                                                            if total_gib else ""),
+                   "shard_bytes_requested": want, "shard_shrunk": size != want,
                    "file_bytes": cfg["workload.file_bytes"], "bytes_per_gpu": size,
                    "n_tb": cfg["workload.n_tb"], "stride": size // cfg["workload.n_tb"],
                    "request": cfg["workload.request_bytes"], "page": cfg["gpufs.page_size"],
                    "prefetch": cfg["gpufs.prefetch_bytes"], "cache": cfg["gpufs.cache_bytes"],
                    "policy": cfg["gpufs.policy"], "readahead": cfg["io.readahead"],
-                   "ra_max": cfg.ra_max(), "transfer": cfg.transfer(),
+                   "ra_max": cfg.ra_max(), "transfer": transfer,
+                   "transfer_fallback": res.get("fallback"),
                    "io_workers": cfg.io_workers(), "resident_tbs": cfg.resident_limit(),
-                   "resident_ctas": res["ctas"], "storage": f"tmpfs {cfg['io.dir']} O_DIRECT (ramfs)",
+                   "resident_ctas": res["ctas"], "storage": storage_label(cfg, transfer),
                    "l2": f"inputs {size / GiB:g} GiB/GPU >> 126 MB L2; cold GPU page cache every step",
                    "parallelism": f"{dist.world} GPU shard(s), no data-path collective"},
         "per_gpu_gbps": round(per_gpu, 3),
@@ -510,6 +696,8 @@ def main() -> None:
                          if prof else None,
                          "source": "MEASURED_PEAKS.json" if not pk.get("fallback") else "fallback"},
         "cpu_baseline": cpu_base,
+        "pread_daemon": pread_daemon_line(arms, io_peak),
+        "cold_open_e2e": cold,
         "e2e": {"value": round(gbps(total_bytes, wall_s), 3), "unit": "GB/s",
                 "h2d_bytes_per_step": st[-1]["pcie_bytes"] + res["table"].segs.nbytes
                 + res["table"].prog_off.nbytes + res["table"].dst_off.nbytes,
@@ -522,7 +710,7 @@ def main() -> None:
         "counters": {k: st[-1][k] for k in ("rpc_count", "rpc_requested_bytes", "pb_hits",
                                              "pc_misses", "pc_allocs", "pc_remaps", "victims",
                                              "pb_discarded_bytes")},
-        "probes": probes, "arms": arms,
+        "probes": {**probes, "topology": topo}, "arms": arms,
     }
     print(json.dumps(out), flush=True)
     dist.close()
@@ -630,6 +818,7 @@ def comparison_arms(cfg, path: str, device: int, head, probes: dict) -> tuple[di
     cpu_base = None
     try:
         cpu_base = cpu_oracle_sample(path, cfg, size, threads)  # the whole shard
+        cpu_base["python_ref"] = python_reference_timing()  # the reference package itself, C1
     except Exception as e:
         cpu_base = {"error": str(e)[:300]}
     return arms, cpu_base

@@ -53,6 +53,7 @@
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
+#include <sys/stat.h>
 #include <unistd.h>
 
 #include "gfs_oracle.h"
@@ -89,6 +90,38 @@ void orc_gen_bytes(int64_t fid, int64_t off, int64_t n, uint8_t* buf) {
     memcpy(buf + (pos - off), ((uint8_t*)&w) + lo, (size_t)take);
     pos += take;
   }
+}
+
+/* Write the synthetic words of [offset, offset+length) of a file of `size` bytes (created
+ * or extended as needed): the reference arm's input, made without the product library. */
+int orc_gen_file_range(const char* path, int64_t content_id, int64_t size, int64_t offset, int64_t length) {
+  if (!path || size < 0 || offset < 0 || length < 0 || offset + length > size || (offset & 7)) return -1;
+  int fd = open(path, O_CREAT | O_WRONLY, 0644);
+  if (fd < 0) return -1;
+  struct stat sb;
+  if (fstat(fd, &sb) != 0 || (sb.st_size != size && ftruncate(fd, (off_t)size) != 0)) {
+    close(fd);
+    return -1;
+  }
+  const int64_t chunk = 8 << 20;
+  uint8_t* buf = (uint8_t*)malloc((size_t)chunk);
+  int rc = buf ? 0 : -1;
+  for (int64_t o = offset; rc == 0 && o < offset + length; o += chunk) {
+    int64_t n = offset + length - o < chunk ? offset + length - o : chunk;
+    orc_gen_bytes(content_id, o, n, buf);
+    for (int64_t done = 0; done < n;) {
+      ssize_t w = pwrite(fd, buf + done, (size_t)(n - done), (off_t)(o + done));
+      if (w < 0 && errno == EINTR) continue;
+      if (w <= 0) {
+        rc = -1;
+        break;
+      }
+      done += w;
+    }
+  }
+  free(buf);
+  if (close(fd) != 0) rc = -1;
+  return rc;
 }
 
 /* Position-sensitive checksum of a byte buffer viewed as little-endian u64

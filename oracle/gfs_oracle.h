@@ -66,6 +66,7 @@ uint64_t orc_page_tag(int64_t fid, int64_t page);
 uint64_t orc_word(int64_t fid, int64_t i);
 void orc_gen_bytes(int64_t fid, int64_t off, int64_t n, uint8_t* buf);
 uint64_t orc_checksum(const uint8_t* buf, int64_t n, int64_t word_base);
+int orc_gen_file_range(const char* path, int64_t content_id, int64_t size, int64_t offset, int64_t length);
 
 #ifdef __cplusplus
 }

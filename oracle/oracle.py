@@ -84,6 +84,8 @@ def lib():
         L.orc_checksum.restype = C.c_uint64
         L.orc_checksum.argtypes = [C.c_void_p, C.c_int64, C.c_int64]
         L.orc_gen_bytes.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_void_p]
+        L.orc_gen_file_range.argtypes = [C.c_char_p, C.c_int64, C.c_int64, C.c_int64, C.c_int64]
+        L.orc_gen_file_range.restype = C.c_int
         _lib = L
     return _lib
 
@@ -117,43 +119,84 @@ def run_oracle(cfg, workload, *, source: int = SRC_NONE, paths=None, io_direct: 
     """Run the restatement for `cfg` (paper_2109_05366_b200.config.ExperimentConfig)
     over `workload` (WorkloadSpec)."""
     from paper_2109_05366_b200.workloads import ProgramTable, dispatch_order
-    L = lib()
     table = ProgramTable.from_programs(workload.programs)
     n_files = len(workload.files)
-    sizes = np.asarray([workload.files[f] for f in range(n_files)], dtype=np.int64)
-    ro = np.asarray([1 if workload.read_only[f] else 0 for f in range(n_files)], dtype=np.uint8)
     if order is None:
         order = dispatch_order(table.n_tb, cfg["gpu.dispatch_order"], cfg["seed"])
+    params = {"page_size": cfg["gpufs.page_size"], "cache_bytes": cfg["gpufs.cache_bytes"],
+              "prefetch_bytes": cfg["gpufs.prefetch_bytes"], "request_bytes": workload.request_bytes,
+              "staging_bytes": cfg["rpc.staging_bytes"], "ra_max_bytes": cfg.ra_max(),
+              "ra_init_bytes": cfg.ra_init(), "policy": cfg["gpufs.policy"],
+              "resident_limit": cfg.resident_limit(), "raw_mode": bool(cfg["mode.gpu_cache_disabled"]),
+              "readahead": cfg["io.readahead"], "ra_clamp": cfg["io.ra_clamp"],
+              "pcie_disabled": bool(cfg["mode.pcie_disabled"])}
+    return run_raw(params, [workload.files[f] for f in range(n_files)],
+                   [workload.read_only[f] for f in range(n_files)], table.segs, table.prog_off,
+                   table.dst_off, order, source=source, paths=paths, io_direct=io_direct,
+                   materialize_dst=materialize_dst, log=log)
+
+
+def programs_to_arrays(programs):
+    """Per-TB programs [(file, offset, length), ...] -> (segs [n, 3], prog_off, dst_off, dst_bytes):
+    the flat layout every runner takes (TB t's bytes land at dst_off[t] in program order)."""
+    segs = np.asarray([s for prog in programs for s in prog], dtype=np.int64).reshape(-1, 3)
+    prog_off = np.zeros(len(programs) + 1, dtype=np.int64)
+    prog_off[1:] = np.cumsum([len(p) for p in programs])
+    lens = np.asarray([sum(ln for _, _, ln in p) for p in programs], dtype=np.int64)
+    dst_off = np.zeros(len(programs), dtype=np.int64)
+    if len(programs) > 1:
+        dst_off[1:] = np.cumsum(lens)[:-1]
+    return segs, prog_off, dst_off, int(lens.sum())
+
+
+def run_raw(params: dict, file_sizes, read_only, segs, prog_off, dst_off, order, *,
+            source: int = SRC_NONE, paths=None, io_direct: bool = False,
+            materialize_dst: bool = False, log: bool = True) -> OracleResult:
+    """The restatement over plain arrays (no import of the product package): params holds
+    page_size, cache_bytes, prefetch_bytes, request_bytes, staging_bytes, ra_max_bytes,
+    ra_init_bytes, policy (name), resident_limit, raw_mode, readahead (name), ra_clamp
+    (name), pcie_disabled."""
+    L = lib()
+    n_files = len(file_sizes)
+    sizes = np.asarray(file_sizes, dtype=np.int64)
+    ro = np.asarray([1 if r else 0 for r in read_only], dtype=np.uint8)
     order = np.ascontiguousarray(order, dtype=np.int32)
-    segs = np.ascontiguousarray(table.segs.reshape(-1))
+    segs = np.ascontiguousarray(np.asarray(segs, dtype=np.int64).reshape(-1))
     if segs.size == 0:
         segs = np.zeros(3, np.int64)
-    dst = np.zeros(max(table.dst_bytes, 1), dtype=np.uint8) if materialize_dst else None
+    prog_off = np.ascontiguousarray(prog_off, dtype=np.int64)
+    dst_off = np.ascontiguousarray(dst_off, dtype=np.int64)
+    n_tb = len(prog_off) - 1
+    dst_bytes = 0
+    for t in range(n_tb):
+        a, b = int(prog_off[t]), int(prog_off[t + 1])
+        dst_bytes = max(dst_bytes, int(dst_off[t]) + int(segs.reshape(-1, 3)[a:b, 2].sum()) if b > a else 0)
+    dst = np.zeros(max(dst_bytes, 1), dtype=np.uint8) if materialize_dst else None
     c = OrcCfg()
-    c.page_size = cfg["gpufs.page_size"]
-    c.cache_bytes = cfg["gpufs.cache_bytes"]
-    c.prefetch_bytes = cfg["gpufs.prefetch_bytes"]
-    c.request_bytes = workload.request_bytes
-    c.staging_bytes = cfg["rpc.staging_bytes"]
-    c.ra_max_bytes = cfg.ra_max()
-    c.ra_init_bytes = cfg.ra_init()
-    c.policy = 1 if cfg["gpufs.policy"] == "per-tb-lra" else 0
-    c.resident_limit = cfg.resident_limit()
-    c.raw_mode = int(bool(cfg["mode.gpu_cache_disabled"]))
-    c.readahead = READAHEAD[cfg["io.readahead"]]
-    c.ra_clamp = 1 if cfg["io.ra_clamp"] == "eof" else 0
-    c.pcie_disabled = int(bool(cfg["mode.pcie_disabled"]))
+    c.page_size = params["page_size"]
+    c.cache_bytes = params["cache_bytes"]
+    c.prefetch_bytes = params["prefetch_bytes"]
+    c.request_bytes = params["request_bytes"]
+    c.staging_bytes = params["staging_bytes"]
+    c.ra_max_bytes = params["ra_max_bytes"]
+    c.ra_init_bytes = params.get("ra_init_bytes", 0)
+    c.policy = 1 if params["policy"] == "per-tb-lra" else 0
+    c.resident_limit = params["resident_limit"]
+    c.raw_mode = int(bool(params.get("raw_mode", False)))
+    c.readahead = READAHEAD[params["readahead"]]
+    c.ra_clamp = 1 if params.get("ra_clamp", "segment") == "eof" else 0
+    c.pcie_disabled = int(bool(params.get("pcie_disabled", False)))
     c.log = int(log)
     c.n_files = n_files
-    c.n_tb = table.n_tb
+    c.n_tb = n_tb
     c.file_sizes = _ptr(sizes, C.c_int64)
     c.read_only = _ptr(ro, C.c_uint8)
-    c.prog_off = _ptr(table.prog_off, C.c_int64)
+    c.prog_off = _ptr(prog_off, C.c_int64)
     c.segs = _ptr(segs, C.c_int64)
     c.order = _ptr(order, C.c_int32)
-    c.dst_off = _ptr(table.dst_off, C.c_int64)
+    c.dst_off = _ptr(dst_off, C.c_int64)
     c.dst = _ptr(dst, C.c_uint8) if dst is not None else None
-    c.checksum_bytes = table.dst_bytes if dst is not None else 0
+    c.checksum_bytes = dst_bytes if dst is not None else 0
     c.source = source
     c.io_direct = int(io_direct)
     path_arr = None
@@ -178,8 +221,38 @@ def run_oracle(cfg, workload, *, source: int = SRC_NONE, paths=None, io_direct: 
                 L.orc_log_copy(h, kind, _ptr(arr, C.c_int64))
             setattr(res, attr, arr)
         if dst is not None:
-            res.dst = dst[:table.dst_bytes]
+            res.dst = dst[:dst_bytes]
             res.checksum = int(L.orc_result_checksum(h))
         return res
     finally:
         L.orc_destroy(h)
+
+
+SYNTH_STAMP = "W1"  # the content law's version tag, as stamped next to synthetic files
+
+
+def gen_file(path: str, content_id: int, size: int, threads: int = 0) -> None:
+    """Write a synthetic W(content_id, i) file with the oracle's generator (no product
+    library): `threads` writers over disjoint ranges, then the version stamp."""
+    import threading
+    L = lib()
+    threads = threads or os.cpu_count() or 1
+    with open(path, "wb") as fh:
+        fh.truncate(size)
+    step = ((size + threads - 1) // threads + 7) // 8 * 8
+    errs = []
+
+    def one(k):
+        lo = k * step
+        n = min(step, size - lo)
+        if n > 0 and L.orc_gen_file_range(os.fsencode(path), content_id, size, lo, n) != 0:
+            errs.append(k)
+    ths = [threading.Thread(target=one, args=(k,)) for k in range(threads)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    if errs:
+        raise OracleError(f"orc_gen_file_range failed for {path}")
+    with open(path + ".ok", "w") as fh:
+        fh.write(SYNTH_STAMP)

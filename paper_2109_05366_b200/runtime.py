@@ -137,14 +137,20 @@ class Consumer:
 class GpuFS:
     """One GPU's file layer: HBM page cache + RPC ring + host I/O daemon."""
 
+    # pinned page-cache transfers -> the pread daemon transfer moving the same bytes (used
+    # when the file's pages cannot be pinned: not memory-resident, or not enough pinnable RAM)
+    PIN_FALLBACK = {"mapped_dma": "dma", "mapped_hybrid": "bounce", "mapped": "bounce"}
+
     def __init__(self, cfg: ExperimentConfig, max_request_bytes: int = 0):
         self.cfg = cfg
         self._lib = native.load()
+        self._max_req = max_request_bytes
         self._ncfg = native_config(cfg, max_request_bytes)
         h = C.c_void_p()
         native.check(self._lib.gfs_create(C.byref(self._ncfg), C.byref(h)), "gfs_create")
         self._h = h
         self.files: dict[int, dict] = {}
+        self.fallback: str | None = None  # "<from> -> <to>: <why>" after a pin-failure fallback
 
     # -- lifecycle ----------------------------------------------------------
 
@@ -225,9 +231,15 @@ class GpuFS:
         names = native.stat_names()
         out = (C.c_int64 * len(names))()
         cons = consumer.native() if consumer is not None else None
-        native.check(self._lib.gfs_run_consume(self._h, C.byref(prog), dst_ptr, dst_bytes,
-                                               C.byref(cons) if cons is not None else None, out),
-                     "gfs_run")
+        rc = self._lib.gfs_run_consume(self._h, C.byref(prog), dst_ptr, dst_bytes,
+                                       C.byref(cons) if cons is not None else None, out)
+        if rc != 0 and self._pin_failed():
+            # the mapped transfers could not pin the file's pages: same run through the
+            # pread daemon (O_DIRECT pread -> pinned staging -> HBM), still on the GPU path
+            self._reopen_with(self.PIN_FALLBACK[self.transfer])
+            rc = self._lib.gfs_run_consume(self._h, C.byref(prog), dst_ptr, dst_bytes,
+                                           C.byref(cons) if cons is not None else None, out)
+        native.check(rc, "gfs_run")
         del keep
         res = RunResult(stats=dict(zip(names, list(out))))
         if self._ncfg.timeline:
@@ -238,6 +250,25 @@ class GpuFS:
             res.victims = self.log(native.LOG_VICTIMS)
             res.windows = self.log(native.LOG_WINDOWS)
         return res
+
+    def _pin_failed(self) -> bool:
+        msg = self._lib.gfs_last_error().decode(errors="replace")
+        return self.transfer in self.PIN_FALLBACK and "mapped transfers need" in msg
+
+    def _reopen_with(self, transfer: str) -> None:
+        why = self._lib.gfs_last_error().decode(errors="replace")
+        was = self.transfer
+        files = [self.files[f] for f in sorted(self.files)]
+        self.close()
+        self.cfg = self.cfg.copy_with({"io.transfer": transfer})
+        self._ncfg = native_config(self.cfg, self._max_req)
+        h = C.c_void_p()
+        native.check(self._lib.gfs_create(C.byref(self._ncfg), C.byref(h)), "gfs_create")
+        self._h = h
+        self.files = {}
+        for f in files:
+            self.gopen(f["path"], O_RDONLY if f["read_only"] else O_RDWR, f["content_id"])
+        self.fallback = f"{was} -> {transfer}: {why[:200]}"
 
     def gread(self, fid: int, offset: int, size: int, dst=None) -> RunResult:
         """One threadblock's gread of [offset, offset+size) (gpu_exec.py:107-129)."""

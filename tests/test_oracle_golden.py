@@ -124,3 +124,16 @@ def test_materialized_files_odirect(tmp_path):
                 pytest.skip("filesystem without O_DIRECT")
             raise
         assert res.dst.tobytes() == grng.content(0, 0, wl.total_bytes)
+
+
+def test_oracle_file_generator_matches_product(tmp_path):
+    """The reference arm writes its input with the oracle's generator (no product library);
+    the bytes and the version stamp equal the product's synthetic file."""
+    from paper_2109_05366_b200 import native
+    from paper_2109_05366_b200.runtime import SYNTH_VERSION
+    size = 3 * 1048576 + 12344
+    a, b = str(tmp_path / "a.bin"), str(tmp_path / "b.bin")
+    orc.gen_file(a, 2, size, threads=3)
+    native.gen_file(b, 2, size)
+    assert open(a, "rb").read() == open(b, "rb").read()
+    assert open(a + ".ok").read().strip() == SYNTH_VERSION == orc.SYNTH_STAMP
