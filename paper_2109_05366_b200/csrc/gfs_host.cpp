@@ -263,6 +263,7 @@ struct gfs_ctx {
   bool poisoned = false;
   int downgraded_from = -1;  // copy-engine transfer replaced by its SM-pull sibling (queue probe)
   int64_t ce_min = 4 << 20;  // mapped_hybrid: spans of at least this many bytes go by copy engine
+  int probe_attempts = 0;    // copy-queue probe rounds gfs_create needed (1 = first streams fine)
   // driver entry point resolved through cudart (libgfs does not link libcuda, so it
   // loads on machines without a driver; CUDA calls then fail loudly)
   CUresult (*write_value64)(CUstream, CUdeviceptr, cuuint64_t, unsigned int) = nullptr;
@@ -649,36 +650,47 @@ extern "C" int gfs_create(const gfs_config* cfg_in, gfs_ctx** out) {
     int nstreams = 2;
     if (const char* e = getenv("GFS_COPY_STREAMS")) nstreams = std::max(1, std::min(16, atoi(e)));  // experiments
     if (const char* e = getenv("GFS_CE_MIN_KIB")) ctx->ce_min = std::max(4, atoi(e)) * 1024ll;  // experiments
-    ctx->worker_streams.resize((size_t)std::min(cfg.io_workers, nstreams), nullptr);
-    for (auto& s : ctx->worker_streams) TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    ctx->bell_streams.resize((size_t)std::min(cfg.io_workers, nstreams), nullptr);
-    for (auto& s : ctx->bell_streams) TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     // Copy-engine transfers complete while the persistent kernel runs: their streams must
     // not share a hardware queue with the kernel's stream (CUDA_DEVICE_MAX_CONNECTIONS too
-    // small, or CUDA initialised before the package could raise it).  Probe it: a kernel on
-    // the run stream waits (bounded) for one value written by each copy / doorbell stream.
-    // If any write queues behind the kernel, fall back to the SM-pull transfer that moves
-    // the same bytes (mapped_dma / mapped_hybrid -> mapped, dma -> bounce).
-    std::vector<cudaStream_t> probe(ctx->worker_streams);
-    probe.insert(probe.end(), ctx->bell_streams.begin(), ctx->bell_streams.end());
+    // small, or CUDA initialised before the package could raise it; with enough queues a
+    // new stream can still land on the kernel stream's queue).  Probe it: a kernel on the
+    // run stream waits (bounded) for one value written by each copy / doorbell stream.  If a
+    // write queues behind the kernel, make new streams (up to 4 tries); if that never works,
+    // fall back to the SM-pull transfer moving the same bytes (mapped_dma / mapped_hybrid ->
+    // mapped, dma -> bounce).
     unsigned long long* d_flags = nullptr;
-    int* d_ok = nullptr;
-    TRY(cudaMalloc(&d_flags, probe.size() * 8 + 8));
-    d_ok = (int*)(d_flags + probe.size());
-    TRY(cudaMemsetAsync(d_flags, 0, probe.size() * 8 + 8, ctx->stream));
-    TRY(launch_queue_probe(d_flags, (int)probe.size(), 500ull * 1000000ull, d_ok, ctx->stream));
-    for (size_t i = 0; i < probe.size(); i++) {
-      if (ctx->write_value64((CUstream)probe[i], (CUdeviceptr)(d_flags + i), 1, 0) != CUDA_SUCCESS) {
-        cudaFree(d_flags);
-        return bail(fail(GFS_ECUDA, "cuStreamWriteValue64 failed on a copy stream"));
-      }
-      cudaStreamQuery(probe[i]);
-    }
-    TRY(cudaStreamSynchronize(ctx->stream));
+    TRY(cudaMalloc(&d_flags, (size_t)(4 * nstreams + 1) * 8));
     int ok = 0;
-    TRY(cudaMemcpy(&ok, d_ok, 4, cudaMemcpyDeviceToHost));
-    TRY(cudaDeviceSynchronize());
+    std::vector<cudaStream_t> retired;  // kept alive while retrying so new streams move on
+    for (int attempt = 0; attempt < 4 && !ok; attempt++) {
+      for (auto s : ctx->worker_streams) retired.push_back(s);
+      for (auto s : ctx->bell_streams) retired.push_back(s);
+      ctx->worker_streams.assign((size_t)std::min(cfg.io_workers, nstreams), nullptr);
+      ctx->bell_streams.assign((size_t)std::min(cfg.io_workers, nstreams), nullptr);
+      for (auto& s : ctx->worker_streams) TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+      for (auto& s : ctx->bell_streams) TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+      std::vector<cudaStream_t> probe(ctx->worker_streams);
+      probe.insert(probe.end(), ctx->bell_streams.begin(), ctx->bell_streams.end());
+      int* d_ok = (int*)(d_flags + probe.size());
+      TRY(cudaMemsetAsync(d_flags, 0, probe.size() * 8 + 8, ctx->stream));
+      TRY(launch_queue_probe(d_flags, (int)probe.size(), 500ull * 1000000ull, d_ok, ctx->stream));
+      for (size_t i = 0; i < probe.size(); i++) {
+        if (ctx->write_value64((CUstream)probe[i], (CUdeviceptr)(d_flags + i), 1, 0) != CUDA_SUCCESS) {
+          cudaFree(d_flags);
+          return bail(fail(GFS_ECUDA, "cuStreamWriteValue64 failed on a copy stream"));
+        }
+        cudaStreamQuery(probe[i]);
+      }
+      TRY(cudaStreamSynchronize(ctx->stream));
+      TRY(cudaMemcpy(&ok, d_ok, 4, cudaMemcpyDeviceToHost));
+      TRY(cudaDeviceSynchronize());
+      ctx->probe_attempts = attempt + 1;
+    }
+    for (auto s : retired) cudaStreamDestroy(s);
     cudaFree(d_flags);
+    if (ok && ctx->probe_attempts > 1)
+      fprintf(stderr, "libgfs: copy streams re-created %d time(s) to get hardware queues apart from the kernel's\n",
+              ctx->probe_attempts - 1);
     if (!ok) {
       const int was = cfg.transfer;
       cfg.transfer = was == GFS_XFER_DMA ? GFS_XFER_BOUNCE : GFS_XFER_MAPPED_ZC;
@@ -786,6 +798,7 @@ extern "C" int gfs_transfer(gfs_ctx* ctx, int* transfer, int* downgraded_from) {
   if (!ctx || !transfer) return fail(GFS_EINVAL, "gfs_transfer: null argument");
   *transfer = ctx->cfg.transfer;
   if (downgraded_from) *downgraded_from = ctx->downgraded_from;
+
   return GFS_OK;
 }
 
