@@ -371,7 +371,8 @@ def arm_summary(res) -> dict:
             "ms_per_step": round(sum(ns) / len(ns) / 1e6, 3),
             "rpc_count": st[-1]["rpc_count"], "pb_hits": st[-1]["pb_hits"],
             "pc_remaps": st[-1]["pc_remaps"], "pc_evictions": st[-1]["pc_evictions"],
-            "user_bytes": nbytes, "mismatched_words": res["mismatched_words"]}
+            "user_bytes": nbytes, "mismatched_words": res["mismatched_words"],
+            "transfer": res.get("transfer"), "fallback": res.get("fallback")}
 
 
 def cpu_oracle_sample(path: str, cfg, sample_bytes: int, threads: int) -> dict:
