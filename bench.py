@@ -293,13 +293,15 @@ def run_arm(cfg, path: str, rank: int, device: int, steps: int, warmup: int, dst
             dist.barrier()
         mism = fs.verify(table, dst) if cfg["mode.verify"] else None
         csum = fs.checksum(dst, table.dst_bytes)
+        # check_unique_mapping (gpu_cache.py:217-224) on the table the last step left
+        mapping = fs.check_unique_mapping() if cfg["mode.verify"] else None
         ctas = fs.resident_ctas
         transfer, fallback = fs.transfer, fs.fallback
     finally:
         fs.close()
     return {"stats": stats, "walls": walls, "table": table, "wl": wl, "mismatched_words": mism,
             "checksum": csum, "ctas": ctas, "clocks": sampler.summary() if sampler else None,
-            "dst": dst, "transfer": transfer, "fallback": fallback}
+            "dst": dst, "transfer": transfer, "fallback": fallback, "mapping": mapping}
 
 
 def storage_label(cfg, transfer: str) -> str:

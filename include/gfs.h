@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define GFS_ABI_VERSION 3  /* 3: io.readahead ondemand law, gfs_config.ra_clamp replaces async_ra */
+#define GFS_ABI_VERSION 4  /* 4: gfs_run_kernel (user kernels over gfs_device.cuh); 3: ondemand law, ra_clamp */
 
 enum { GFS_OK = 0, GFS_EINVAL = -1, GFS_ECUDA = -2, GFS_EIO = -3, GFS_ENOMEM = -4,
        GFS_ETIMEDOUT = -5, GFS_EDEVICE = -6, GFS_ESTATE = -7 };
@@ -185,6 +185,29 @@ typedef struct gfs_consumer {
 int gfs_run_consume(gfs_ctx* ctx, const gfs_program* prog, void* dst, uint64_t dst_bytes,
                     const gfs_consumer* cons, gfs_stats* out);
 
+/* ---- user kernels reading through the device-side gread (include/gfs_device.cuh;
+ * SURVEY §8(b), reference ThreadBlock._gread gpu_exec.py:107-239).  gfs_run_kernel prepares a
+ * run exactly as gfs_run does (cold page cache, fresh counters, daemon serving the RPC ring)
+ * for n_tb threadblocks whose programs are the user's kernel, then calls launch() once, from
+ * the calling thread, to launch that kernel on `stream`; it waits for the kernel and returns
+ * the run's counters (and logs) like gfs_run.  order: activation order of the TB ids
+ * (NULL = 0..n_tb-1).  Mapped transfers pin each open file whole.  The launch callback
+ * returns 0, or nonzero to abort the run (GFS_EINVAL).  The built-in lookahead is off for
+ * user kernels: a gread delivers only [offset, offset+size). ---- */
+typedef struct gfs_launch {
+  const void* dev;      /* device context (gfs_dev, gfs_device.cuh): pass *(const gfs_dev*)dev by value */
+  int64_t dev_bytes;    /* sizeof(gfs_dev) the library was built with (launchers check it) */
+  int32_t n_ctas;       /* grid: one CTA per resident TB slot */
+  int32_t cta_threads;  /* block size: must equal the kernel's BS */
+  int64_t smem_bytes;   /* dynamic shared memory the file layer needs */
+  void* stream;         /* cudaStream_t to launch on */
+  int32_t n_tb;
+  int32_t reserved;
+} gfs_launch;
+typedef int (*gfs_launch_fn)(const gfs_launch* launch, void* user);
+int gfs_run_kernel(gfs_ctx* ctx, int32_t n_tb, const int32_t* order, gfs_launch_fn launch, void* user,
+                   gfs_stats* out);
+
 /* ---- logs of the last run (metrics.deliveries, recorded trace, victim_log) ---- */
 int gfs_log_len(gfs_ctx* ctx, int kind, int64_t* n);
 int gfs_log_copy(gfs_ctx* ctx, int kind, int64_t* out, int64_t cap_records);
@@ -195,6 +218,21 @@ int gfs_checksum(gfs_ctx* ctx, const void* dev_buf, uint64_t nbytes, uint64_t wo
 /* count words of dev_buf (laid out as prog's user buffer) that differ from W(content of file) */
 int gfs_verify_dst(gfs_ctx* ctx, const gfs_program* prog, const void* dev_buf, uint64_t dst_bytes,
                    int64_t* mismatched_words);
+
+/* ---- end-of-run invariant: GpuPageCache.check_unique_mapping (gpu_cache.py:217-224,
+ * simulation.py:252-253) over the device page table the last run left.  Every mapped page
+ * must name a settled frame (VALID, unpinned, not in flight) keyed by that (file, page), no
+ * frame may be reachable from two pages, and no VALID frame of an open file may be
+ * unreachable.  Fills *out and returns GFS_EDEVICE when any count but mapped_pages is
+ * nonzero. ---- */
+typedef struct gfs_mapping_check {
+  int64_t mapped_pages;
+  int64_t duplicate_frames;
+  int64_t key_mismatches;
+  int64_t unsettled;
+  int64_t lost_frames;
+} gfs_mapping_check;
+int gfs_check_mapping(gfs_ctx* ctx, gfs_mapping_check* out);
 
 /* ---- synthetic files (K6): write W(content_id, i) words, multi-threaded ---- */
 int gfs_gen_file(const char* path, int64_t content_id, int64_t size, int threads);

@@ -45,6 +45,10 @@ cudaError_t occupancy_gread(int cta_threads, int* blocks_per_sm);
 cudaError_t launch_queue_probe(const unsigned long long* flags, int n, uint64_t timeout_ns, int* ok,
                                cudaStream_t st);
 int64_t gread_tma_offset(const gfs_consumer& k, int cta_threads);
+int64_t gread_launch_smem(const gfs_consumer& k, int cta_threads, int tma);
+cudaError_t launch_check_mapping(const DevFile* files, int n_files, const unsigned long long* fkey,
+                                 const uint32_t* fstate, uint32_t* owner, int64_t nframes,
+                                 unsigned long long* out, int sms, cudaStream_t st);
 cudaError_t launch_checksum(const void* buf, uint64_t nbytes, uint64_t word_base,
                             unsigned long long* out, int sms, cudaStream_t st);
 cudaError_t launch_verify_dst(const void* buf, const int64_t* segs, const int64_t* seg_dst,
@@ -219,6 +223,7 @@ struct gfs_ctx {
   unsigned long long* d_done_pos = nullptr;
   long long* d_stats = nullptr;
   unsigned long long* d_scratch = nullptr;
+  uint32_t* d_owner = nullptr;  // check_unique_mapping scratch (nframes), allocated on first use
   unsigned long long* h_served = nullptr;  // mapped: requests completed by the daemon
   DevBuf<int64_t> d_segs, d_prog_off, d_dst_off, d_seg_dst;
   DevBuf<int32_t> d_order;
@@ -539,7 +544,7 @@ static void free_all(gfs_ctx* ctx) {
     if (ev) cudaEventDestroy(ev);
   void* dev[] = {ctx->d_frames, ctx->d_fkey, ctx->d_fstate, ctx->d_own_q, ctx->d_retired, ctx->d_rpool, ctx->d_landed,
                  ctx->d_gfifo, ctx->d_recycled, ctx->d_g, ctx->d_landing, ctx->d_doorbell,
-                 ctx->d_done_pos, ctx->d_stats, ctx->d_scratch};
+                 ctx->d_done_pos, ctx->d_stats, ctx->d_scratch, ctx->d_owner};
   for (void* p : dev)
     if (p) cudaFree(p);
   ctx->d_segs.release();
@@ -965,9 +970,40 @@ static int validate_consumer(const gfs_consumer* k, const gfs_program* prog, boo
   return GFS_OK;
 }
 
+static int run_prepared(gfs_ctx* ctx, const gfs_program* prog, void* dst, const gfs_consumer* cons,
+                        gfs_launch_fn launch, void* user, gfs_stats* out, uint64_t w0);
+
 extern "C" int gfs_run(gfs_ctx* ctx, const gfs_program* prog, void* dst, uint64_t dst_bytes,
                        gfs_stats* out) {
   return gfs_run_consume(ctx, prog, dst, dst_bytes, nullptr, out);
+}
+
+// A user kernel over the device gread (gfs_device.cuh): n_tb TBs with empty built-in
+// programs; the kernel decides what each TB reads.
+extern "C" int gfs_run_kernel(gfs_ctx* ctx, int32_t n_tb, const int32_t* order, gfs_launch_fn launch,
+                              void* user, gfs_stats* out) {
+  const uint64_t w0 = now_ns();
+  if (!ctx || !launch || !out || n_tb < 0) return fail(GFS_EINVAL, "gfs_run_kernel: bad argument");
+  if (ctx->poisoned)
+    return fail(GFS_ESTATE, "context unusable: an earlier run's kernel never finished (destroy it)");
+  if (ctx->cfg.raw_mode) return fail(GFS_EINVAL, "gfs_run_kernel: raw mode has no page cache to read through");
+  std::vector<int64_t> prog_off((size_t)n_tb + 1, 0), dst_off((size_t)std::max(n_tb, 1), 0);
+  std::vector<int32_t> ord((size_t)std::max(n_tb, 1));
+  for (int i = 0; i < n_tb; i++) ord[i] = order ? order[i] : i;
+  gfs_program prog{};
+  prog.n_tb = n_tb;
+  prog.request_bytes = ctx->cfg.page_size;
+  prog.segs = nullptr;
+  prog.prog_off = prog_off.data();
+  prog.dst_off = dst_off.data();
+  prog.order = ord.data();
+  int rc = validate_program(ctx, &prog, 0, false);
+  if (rc) return rc;
+  const int xfer = ctx->cfg.transfer;
+  if (xfer == GFS_XFER_MAPPED || xfer == GFS_XFER_MAPPED_ZC || xfer == GFS_XFER_MAPPED_HYBRID)
+    for (auto& f : ctx->files)  // any byte of an open file may be read
+      if (f.open && f.size > 0 && (rc = map_range(f, 0, f.size))) return rc;
+  return run_prepared(ctx, &prog, nullptr, nullptr, launch, user, out, w0);
 }
 
 extern "C" int gfs_run_consume(gfs_ctx* ctx, const gfs_program* prog, void* dst, uint64_t dst_bytes,
@@ -992,17 +1028,32 @@ extern "C" int gfs_run_consume(gfs_ctx* ctx, const gfs_program* prog, void* dst,
       if (hi[f] > lo[f] && ctx->files[f].open && ctx->files[f].size > 0 && lo[f] < ctx->files[f].size)
         if ((rc = map_range(ctx->files[f], lo[f], hi[f]))) return rc;
   }
+  return run_prepared(ctx, prog, dst, cons, nullptr, nullptr, out, w0);
+}
+
+// The run itself, shared by gfs_run_consume (the built-in strided driver) and
+// gfs_run_kernel (a user kernel launched by `launch`).
+static int run_prepared(gfs_ctx* ctx, const gfs_program* prog, void* dst, const gfs_consumer* cons,
+                        gfs_launch_fn launch, void* user, gfs_stats* out, uint64_t w0) {
+  int rc;
   CUDA_TRY(cudaSetDevice(ctx->cfg.device));
   const gfs_config& cfg = ctx->cfg;
   int64_t n_segs = 0;
   if ((rc = upload_files(ctx)) || (rc = upload_program(ctx, prog, &n_segs))) return rc;
 
-  // log capacities: one delivery per page step, bounded by pages + 2 per request
+  // log capacities: one delivery per page step, bounded by pages + 2 per request.  A user
+  // kernel's reads are unknown: twice every open file's pages plus a margin per TB.
   int64_t pages = 0, requests = 0;
   for (int64_t s = 0; s < n_segs; s++) {
     int64_t len = prog->segs[3 * s + 2];
     pages += len / cfg.page_size + 2;
     requests += len / prog->request_bytes + 1;
+  }
+  if (launch) {
+    for (auto& f : ctx->files)
+      if (f.open) pages += 2 * f.npages;
+    pages += 64 * (int64_t)prog->n_tb;
+    requests = pages;
   }
   for (int k = 0; k < 5; k++) {
     ctx->log_cap[k] = 0;
@@ -1054,7 +1105,7 @@ extern "C" int gfs_run_consume(gfs_ctx* ctx, const gfs_program* prog, void* dst,
   c.raw_mode = cfg.raw_mode;
   c.log = cfg.log;
   c.timeline = cfg.timeline;
-  c.lookahead = cfg.lookahead;
+  c.lookahead = launch ? 0 : cfg.lookahead;  // user greads deliver only their own range
   c.landing_halves = ctx->landing_halves;
   c.stream_pieces = ctx->stream_pieces ? 1 : 0;
   c.stream_piece = ctx->stream_piece;
@@ -1118,7 +1169,26 @@ extern "C" int gfs_run_consume(gfs_ctx* ctx, const gfs_program* prog, void* dst,
   if (prog->n_tb > 0) {
     CUDA_TRY(cudaEventRecord(ctx->ev0, ctx->stream));
     cudaGetLastError();  // clear any stale non-sticky error before the launch check
-    CUDA_TRY(launch_gread(c, cfg.cta_threads, ctx->stream));
+    if (launch) {
+      gfs_launch L{};
+      L.dev = &c;
+      L.dev_bytes = (int64_t)sizeof(DevCtx);
+      L.n_ctas = ctx->n_ctas;
+      L.cta_threads = cfg.cta_threads;
+      L.smem_bytes = gread_launch_smem(c.cons, cfg.cta_threads, c.tma);
+      L.stream = (void*)ctx->stream;
+      L.n_tb = prog->n_tb;
+      const int lr = launch(&L, user);
+      cudaError_t le = cudaGetLastError();
+      if (lr != 0 || le != cudaSuccess) {
+        // nothing may be left running against the ring: wait for whatever did launch
+        cudaStreamSynchronize(ctx->stream);
+        reset_daemon(ctx);
+        return fail(GFS_EINVAL, "gfs_run_kernel: launch callback failed (%d, %s)", lr, cudaGetErrorString(le));
+      }
+    } else {
+      CUDA_TRY(launch_gread(c, cfg.cta_threads, ctx->stream));
+    }
     CUDA_TRY(cudaEventRecord(ctx->ev1, ctx->stream));
   }
   // wait (GIL is released by the ctypes caller); the kernel has its own device timeout
@@ -1229,6 +1299,36 @@ extern "C" int gfs_checksum(gfs_ctx* ctx, const void* dev_buf, uint64_t nbytes, 
   CUDA_TRY(cudaMemcpyAsync(&v, ctx->d_scratch, 8, cudaMemcpyDeviceToHost, ctx->stream));
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   *out = v;
+  return GFS_OK;
+}
+
+// check_unique_mapping (gpu_cache.py:217-224) over the page table the last run left.
+extern "C" int gfs_check_mapping(gfs_ctx* ctx, gfs_mapping_check* out) {
+  if (!ctx || !out) return fail(GFS_EINVAL, "gfs_check_mapping: null argument");
+  if (ctx->poisoned) return fail(GFS_ESTATE, "context unusable");
+  memset(out, 0, sizeof *out);
+  if (ctx->cfg.raw_mode || !ctx->has_run) return GFS_OK;  // no page cache / nothing cached yet
+  CUDA_TRY(cudaSetDevice(ctx->cfg.device));
+  if (!ctx->d_owner) CUDA_TRY(cudaMalloc(&ctx->d_owner, (size_t)ctx->nframes * 4));
+  int rc = upload_files(ctx);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemsetAsync(ctx->d_owner, 0xFF, (size_t)ctx->nframes * 4, ctx->stream));
+  CUDA_TRY(cudaMemsetAsync(ctx->d_scratch, 0, 64, ctx->stream));
+  CUDA_TRY(launch_check_mapping(ctx->d_files.p, (int)ctx->files.size(), ctx->d_fkey, ctx->d_fstate, ctx->d_owner,
+                                ctx->nframes, ctx->d_scratch, ctx->sms, ctx->stream));
+  unsigned long long v[5] = {0, 0, 0, 0, 0};
+  CUDA_TRY(cudaMemcpyAsync(v, ctx->d_scratch, sizeof v, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  out->mapped_pages = (int64_t)v[0];
+  out->duplicate_frames = (int64_t)v[1];
+  out->key_mismatches = (int64_t)v[2];
+  out->unsettled = (int64_t)v[3];
+  out->lost_frames = (int64_t)v[4];
+  if (v[1] || v[2] || v[3] || v[4])
+    return fail(GFS_EDEVICE,
+                "check_unique_mapping: %llu frames reached from two pages, %llu key mismatches, "
+                "%llu unsettled entries, %llu valid frames unreachable (of %llu mapped pages)",
+                v[1], v[2], v[3], v[4], v[0]);
   return GFS_OK;
 }
 

@@ -21,7 +21,7 @@ RA_CLAMP = {"segment": 0, "eof": 1}
 TRANSFER = {"zerocopy": 0, "dma": 1, "bounce": 2, "mapped_dma": 3, "mapped": 4,
             "mapped_hybrid": 5}
 O_RDONLY, O_RDWR = 0, 2
-ABI_VERSION = 3  # include/gfs.h GFS_ABI_VERSION: the struct layouts below
+ABI_VERSION = 4  # include/gfs.h GFS_ABI_VERSION: the struct layouts below
 LOG_DELIVERIES, LOG_RPCS, LOG_VICTIMS, LOG_WINDOWS, LOG_TIMELINE = 0, 1, 2, 3, 4
 LOG_WIDTH = {LOG_DELIVERIES: 3, LOG_RPCS: 4, LOG_VICTIMS: 3, LOG_WINDOWS: 2, LOG_TIMELINE: 4}
 TL_RPC, TL_GREAD, TL_CONSUME = 0, 1, 2
@@ -32,7 +32,9 @@ EXPORTS = ["gfs_create", "gfs_destroy", "gfs_gopen", "gfs_gclose", "gfs_file_siz
            "gfs_log_len", "gfs_log_copy", "gfs_checksum", "gfs_verify_dst", "gfs_gen_file",
            "gfs_last_error", "gfs_abi_version", "gfs_stat_count", "gfs_stat_name",
            "gfs_resident_ctas", "gfs_bench_storage", "gfs_bench_h2d", "gfs_bench_read_memcpy",
-           "gfs_replay", "gfs_gen_file_range", "gfs_transfer"]
+           "gfs_replay", "gfs_gen_file_range", "gfs_transfer", "gfs_run_kernel",
+           "gfs_check_mapping"]
+USER_LIB_PATH = os.path.join(PKG, "_lib", "libgfs_user.so")  # example user kernel (csrc/user_gemv.cu)
 
 
 class GfsConfig(C.Structure):
@@ -70,6 +72,20 @@ class GfsProgram(C.Structure):
     ]
 
 
+class GfsMappingCheck(C.Structure):
+    _fields_ = [("mapped_pages", C.c_int64), ("duplicate_frames", C.c_int64),
+                ("key_mismatches", C.c_int64), ("unsettled", C.c_int64), ("lost_frames", C.c_int64)]
+
+
+class GfsLaunch(C.Structure):
+    """gfs_launch: what gfs_run_kernel hands a user kernel's launch callback."""
+    _fields_ = [
+        ("dev", C.c_void_p), ("dev_bytes", C.c_int64), ("n_ctas", C.c_int32),
+        ("cta_threads", C.c_int32), ("smem_bytes", C.c_int64), ("stream", C.c_void_p),
+        ("n_tb", C.c_int32), ("reserved", C.c_int32),
+    ]
+
+
 _lib = None
 _nstats = None
 
@@ -104,6 +120,8 @@ def load(path: str = LIB_PATH):
     L.gfs_stat_name.argtypes = [i32]
     L.gfs_resident_ctas.argtypes = [vp]
     L.gfs_transfer.argtypes = [vp, C.POINTER(i32), C.POINTER(i32)]
+    L.gfs_run_kernel.argtypes = [vp, i32, C.POINTER(C.c_int32), vp, vp, vp]
+    L.gfs_check_mapping.argtypes = [vp, C.POINTER(GfsMappingCheck)]
     dp = C.POINTER(C.c_double)
     L.gfs_bench_storage.argtypes = [C.c_char_p, i64, i64, i32, i64, i32, dp]
     L.gfs_bench_h2d.argtypes = [i32, i64, i32, dp]
@@ -113,12 +131,32 @@ def load(path: str = LIB_PATH):
     for name in ("gfs_create", "gfs_gopen", "gfs_gclose", "gfs_file_size", "gfs_run",
                  "gfs_log_len", "gfs_log_copy", "gfs_checksum", "gfs_verify_dst", "gfs_gen_file",
                  "gfs_bench_storage", "gfs_bench_h2d", "gfs_bench_read_memcpy", "gfs_replay",
-                 "gfs_gen_file_range", "gfs_transfer"):
+                 "gfs_gen_file_range", "gfs_transfer", "gfs_run_kernel", "gfs_check_mapping"):
         getattr(L, name).restype = i32
     if L.gfs_abi_version() != ABI_VERSION:
         raise GfsError(f"{path} has ABI {L.gfs_abi_version()}, this package needs {ABI_VERSION}: rebuild it")
     _lib = L
     return L
+
+
+_user = None
+
+
+def load_user(path: str = USER_LIB_PATH):
+    """The example user-kernel library (a GEMV written against include/gfs_device.cuh and
+    driven by gfs_run_kernel, linked against libgfs.so like an application would be)."""
+    global _user
+    if _user is not None:
+        return _user
+    load()  # libgfs.so first: the user library resolves gfs_run_kernel from it
+    if not os.path.exists(path):
+        raise GfsError(f"{path} is not built; run `python -m paper_2109_05366_b200.build`")
+    U = C.CDLL(path)
+    vp, i32, i64 = C.c_void_p, C.c_int, C.c_int64
+    U.gfs_example_gemv.argtypes = [vp, i32, i64, i32, i64, i64, vp, vp, vp, i32, C.POINTER(C.c_int32), vp]
+    U.gfs_example_gemv.restype = i32
+    _user = U
+    return U
 
 
 def check(rc: int, what: str) -> None:

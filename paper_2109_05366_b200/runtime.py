@@ -241,6 +241,23 @@ class GpuFS:
                                            C.byref(cons) if cons is not None else None, out)
         native.check(rc, "gfs_run")
         del keep
+        return self._result(out, names)
+
+    def run_user(self, entry, *args, order=None) -> RunResult:
+        """A user kernel over the device-side gread (include/gfs_device.cuh): `entry` is the
+        application's C entry point, called as entry(ctx, *args, order, stats_out); it ends in
+        gfs_run_kernel, which prepares the run like gfs_run and launches the kernel.  Returns
+        the run's counters and logs like run()."""
+        names = native.stat_names()
+        out = (C.c_int64 * len(names))()
+        ordp = None
+        if order is not None:
+            order = np.ascontiguousarray(order, dtype=np.int32)
+            ordp = _ptr(order, C.c_int32)
+        native.check(entry(self._h, *args, ordp, out), "gfs_run_kernel")
+        return self._result(out, names)
+
+    def _result(self, out, names) -> RunResult:
         res = RunResult(stats=dict(zip(names, list(out))))
         if self._ncfg.timeline:
             res.timeline = self.log(native.LOG_TIMELINE)
@@ -293,6 +310,15 @@ class GpuFS:
         native.check(self._lib.gfs_checksum(self._h, buf.data_ptr(), n, word_base, C.byref(v)),
                      "gfs_checksum")
         return v.value
+
+    def check_unique_mapping(self) -> dict:
+        """GpuPageCache.check_unique_mapping (gpu_cache.py:217-224) on the device page table
+        the last run left; raises GfsError on a violation, else returns the counts."""
+        v = native.GfsMappingCheck()
+        rc = self._lib.gfs_check_mapping(self._h, C.byref(v))
+        out = {k: getattr(v, k) for k, _ in native.GfsMappingCheck._fields_}
+        native.check(rc, "check_unique_mapping")
+        return out
 
     def verify(self, table: ProgramTable, dst) -> int:
         prog, keep = self._program(table, 1, np.arange(table.n_tb, dtype=np.int32))
@@ -444,6 +470,7 @@ class Simulation:
         self.result: RunResult | None = None
         self.checksum: int | None = None
         self.mismatched_words: int | None = None
+        self.mapping: dict | None = None  # check_unique_mapping counts of the last run
 
     def run(self, keep_output: bool = False) -> MetricsReport:
         if self.trace is not None:
@@ -465,6 +492,8 @@ class Simulation:
                 self.mismatched_words = fs.verify(table, dst)
                 res.stats["tag_mismatches"] += int(self.mismatched_words > 0)
             self.checksum = fs.checksum(dst, table.dst_bytes)
+            # simulation.py:252-253: the cache's unique-mapping invariant after every run
+            self.mapping = fs.check_unique_mapping() if not cfg["mode.gpu_cache_disabled"] else None
             if keep_output:
                 self.output = dst
         self.result = res

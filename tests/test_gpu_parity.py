@@ -338,6 +338,8 @@ def test_headline_config_full_size_against_oracle():
     assert st["user_bytes"] == 16 * GiB and st["pc_misses"] == pages
     assert st["pc_allocs"] == frames and st["pc_remaps"] == st["victims"] == pages - frames
     assert st["word_mismatches"] == 0 and res["mismatched_words"] == 0
+    # check_unique_mapping: the 4 GiB cache ends full, every frame mapped exactly once
+    assert res["mapping"]["mapped_pages"] == frames and res["mapping"]["duplicate_frames"] == 0
 
 
 @pytest.mark.parametrize("request_bytes", [64 * KiB, 10_000])

@@ -4,7 +4,8 @@ not divide pages, caches above and below the union — under every transfer and 
 copies, lookahead on.  Schedules are free here (hundreds of TBs racing for shared pages),
 so only schedule-invariant quantities are compared: every delivered byte must satisfy the
 file's word law (device check during the pass and `gfs_verify_dst` after it), and
-`greads` / `user_bytes` must equal the program's closed form (gpu_exec.py:95-129).  Each
+`greads` / `user_bytes` must equal the program's closed form (gpu_exec.py:95-129), and the
+page table must pass check_unique_mapping (gpu_cache.py:217-224) after every pass.  Each
 case runs twice on one context to shake out races between the passes."""
 
 import os
@@ -87,3 +88,5 @@ def test_random_multisegment_programs_full_residency(k):
             assert st["greads"] == want_greads, (k, rep, st["greads"], want_greads, over)
             assert st["word_mismatches"] == 0, (k, rep, over)
             assert fs.verify(table, dst) == 0, (k, rep, over)
+            m = fs.check_unique_mapping()  # raises on a duplicate / stale / lost mapping
+            assert m["mapped_pages"] > 0, (k, rep, m)

@@ -39,6 +39,17 @@ def test_library_exports_every_declared_symbol(lib):
     assert lib.gfs_abi_version() == native.ABI_VERSION
 
 
+def test_user_kernel_library_links_against_libgfs(lib):
+    """The example user kernel (csrc/user_gemv.cu over include/gfs_device.cuh) is built like
+    an application: its own .so, resolving gfs_run_kernel from libgfs.so."""
+    U = native.load_user()
+    assert hasattr(U, "gfs_example_gemv")
+    import subprocess
+    out = subprocess.run(["nm", "-D", "--undefined-only", native.USER_LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "gfs_run_kernel" in out
+
+
 def test_stat_names_match_oracle_counters(lib):
     import oracle as orc
     names = native.stat_names()
@@ -57,7 +68,8 @@ def test_struct_layouts_match_header(lib, tmp_path):
     if cc is None:
         pytest.skip("no host C compiler")
     checks = {"gfs_config": native.GfsConfig, "gfs_program": native.GfsProgram,
-              "gfs_consumer": native.GfsConsumer}
+              "gfs_consumer": native.GfsConsumer, "gfs_launch": native.GfsLaunch,
+              "gfs_mapping_check": native.GfsMappingCheck}
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "gfs.h"', "int main(void) {"]
     for cname, py in checks.items():
         lines.append(f'printf("{cname} %zu\\n", sizeof({cname}));')
