@@ -158,7 +158,7 @@ struct Smem {
   long long st[GFS_NSTATS];
   // batched page walk (gread_batch): one entry per page of the batch
   struct {
-    int n_empty, k, status, nvict, nret, ret_lane0, own_lane0, j0, ret_pool;
+    int n_empty, k, status, nvict, nret, ret_lane0, own_lane0, j0, ret_pool, src_half;
     unsigned tail_mask, part_mask;  // pages with a sub-16 B EOF tail / a partial delivery
     int64_t total;                  // bytes this batch delivers
     int64_t rpc_n;
@@ -174,8 +174,11 @@ struct Smem {
   int fresh_done;            // this CTA saw the never-used frames run out (they never return)
   // lookahead: file bytes [la_lo, la_hi) of la_fid were delivered ahead of their gread
   int64_t la_fid, la_lo, la_hi;
-  // the landing half holding the current span (the private buffer's bytes)
-  int span_half;
+  // landing halves: span_half holds the private buffer's bytes; fetch_half received the last
+  // synchronous span (its page 0 is read from there; it becomes span_half only when the span
+  // refills the private buffer, i.e. brings more than one page); pull_half is where a pending
+  // CTA pull (bounce / mapped transfers) lands
+  int span_half, fetch_half, pull_half, src_half;
   // streamed windows, per landing half: the last request into it and how much has landed
   uint32_t st_seq[2];
   int64_t st_n[2], st_landed[2];
@@ -201,6 +204,9 @@ struct Smem {
     unsigned long long pos;
   } hp[2];
   uint32_t hp_age;
+  uint32_t rpc_out;  // this TB's requests outstanding (submitted, not yet waited for)
+  int64_t pull_off;            // file offset of the span waiting to be pulled
+  int64_t dbg_land_off[2], dbg_land_n[2];  // what each landing half last received (diagnostics)
   uint32_t pb_absent[MAX_PB_ENTRIES / 32];  // private-buffer entries consumed / dropped
 };
 
@@ -267,6 +273,27 @@ __device__ void log_rec(const DevCtx& c, int kind, long long a, long long b, lon
 }
 
 // Timeline record (thread 0; gfs_config.timeline): what a CTA was doing, and when.
+// First K1 word mismatch of the run (diagnostics only; rare by construction).
+__device__ void note_mismatch(const DevCtx& c, const Smem& s, int64_t fid, int64_t file_off, uint64_t got,
+                              int64_t span_off, int pages) {
+  if (atomicCAS(&c.g->dbg[0], 0ull, 1ull) != 0ull) return;
+  c.g->dbg[1] = (unsigned long long)s.tb;
+  c.g->dbg[2] = (unsigned long long)fid;
+  c.g->dbg[3] = (unsigned long long)file_off;
+  c.g->dbg[4] = got;
+  c.g->dbg[5] = (unsigned long long)s.b.src_half;
+  c.g->dbg[6] = (unsigned long long)span_off;
+  c.g->dbg[7] = (unsigned long long)pages | ((unsigned long long)blockIdx.x << 32);
+  c.g->dbg[8] = (unsigned long long)s.dbg_land_off[s.b.src_half];
+  c.g->dbg[9] = (unsigned long long)s.dbg_land_n[s.b.src_half];
+  c.g->dbg[10] = (unsigned long long)s.pb_base;
+  c.g->dbg[11] = (unsigned long long)s.pb_off_adj;
+  c.g->dbg[12] = (unsigned long long)s.pb_count;
+  c.g->dbg[13] = (unsigned long long)(s.b.j0);
+  c.g->dbg[14] = (unsigned long long)s.g_lo;
+  c.g->dbg[15] = (unsigned long long)s.g_hi;
+}
+
 __device__ void tl_rec(const DevCtx& c, int kind, int tb, long long bytes, uint64_t t0, uint64_t t1) {
   if (!c.timeline) return;
   unsigned long long i = atomicAdd(&c.g->log_n[GFS_LOG_TIMELINE], 1ull);
@@ -681,9 +708,15 @@ __device__ bool rpc_submit(const DevCtx& c, Smem& s, int64_t fid, int64_t off, i
   const unsigned long long local = atomicAdd(&c.g->req_local, 1ull);
   const unsigned long long pos = c.g->req_base + local;
   uint64_t t0 = globaltimer();
-  if (local >= Q) {  // ring position pos - Q (same entry) must have completed, i.e. been read
+  if (local >= Q) {
+    // ring position pos - Q (same entry) must have been copied out by the daemon: its
+    // answer came back (done_pos, device memory, the cheap check) or the daemon marked the
+    // entry consumed (mapped host memory).  The second check matters: a pending readahead
+    // window may stay unanswered-for (not waited on) for any number of requests, and its
+    // own CTA may be the one waiting here.
     const unsigned long long need = pos - Q + 1;
-    while (ld_volatile_u64(&c.done_pos[pos & c.ring_mask]) < need) {
+    while (ld_volatile_u64(&c.done_pos[pos & c.ring_mask]) < need &&
+           ld_acquire_sys(&c.ring_consumed[pos & c.ring_mask]) != (uint32_t)need) {
       if (!keep_waiting(c, t0, 20)) return false;
       __nanosleep(200);
     }
@@ -701,6 +734,13 @@ __device__ bool rpc_submit(const DevCtx& c, Smem& s, int64_t fid, int64_t off, i
   st_release_sys(&e->seq, seq);
   *seq_out = seq;
   *pos_out = pos;
+  // the reference's slot partition (rpc.py:25-28, 82-89): TB tb owns slot tb % n_slots and
+  // a request finding that slot occupied is a collision.  Counted on the real timing; the
+  // device does not serialise on it (every resident CTA has its own mailbox).
+  // (this TB's own outstanding readahead windows are not collisions: the reference's OS
+  // readahead runs inside the host's pread, not through the slot)
+  if (atomicAdd(&c.slot_busy[s.tb % c.ref_slots], 1u) > s.rpc_out) ST(slot_collisions)++;
+  s.rpc_out++;
   return true;
 }
 
@@ -742,6 +782,8 @@ __device__ int64_t rpc_wait(const DevCtx& c, Smem& s, int64_t fid, int64_t off, 
           s.pull_n = n;
           s.pull_buf = -1;
           s.pull_src = c.files[fid].map + off;
+          s.pull_off = off;
+          s.pull_half = half;
         }
         break;
       }
@@ -761,11 +803,16 @@ __device__ int64_t rpc_wait(const DevCtx& c, Smem& s, int64_t fid, int64_t off, 
           s.pull_n = n;
           s.pull_buf = *(volatile const int32_t*)&r->buf;
           s.pull_src = c.bounce + (int64_t)s.pull_buf * c.bounce_bytes;
+          s.pull_off = off;
+          s.pull_half = half;
           s.pull_seq = seq;
         } else if (c.transfer == GFS_XFER_MAPPED_ZC && n > 0) {  // straight from the page cache
           s.pull_n = n;
           s.pull_buf = -1;
           s.pull_src = c.files[fid].map + off;
+          s.pull_off = off;
+          s.pull_half = half;
+          s.pull_off = off;
         }
         break;
       }
@@ -777,6 +824,8 @@ __device__ int64_t rpc_wait(const DevCtx& c, Smem& s, int64_t fid, int64_t off, 
     }
   }
   atomicMax(&c.done_pos[pos & c.ring_mask], pos + 1);
+  atomicSub(&c.slot_busy[s.tb % c.ref_slots], 1u);  // slot released when the data is ready (rpc.py:104-113)
+  s.rpc_out--;
   if (c.stream_pieces && n > 0) {  // the doorbell comes after the first piece
     s.st_seq[half] = seq;
     s.st_n[half] = n;
@@ -813,10 +862,13 @@ __device__ bool wait_landed(const DevCtx& c, Smem& s, int h, int64_t need) {
 }
 
 // Where the current span (page 0 + private-buffer pages) lives.
-__device__ __forceinline__ const uint8_t* span_base(const DevCtx& c, const Smem& s) {
+__device__ __forceinline__ const uint8_t* half_base(const DevCtx& c, int h) {
   if (c.transfer == GFS_XFER_ZEROCOPY)
-    return c.staging + ((int64_t)blockIdx.x * c.landing_halves + s.span_half) * c.slot_bytes;
-  return c.landing + ((int64_t)blockIdx.x * c.landing_halves + s.span_half) * c.slot_bytes;
+    return c.staging + ((int64_t)blockIdx.x * c.landing_halves + h) * c.slot_bytes;
+  return c.landing + ((int64_t)blockIdx.x * c.landing_halves + h) * c.slot_bytes;
+}
+__device__ __forceinline__ const uint8_t* span_base(const DevCtx& c, const Smem& s) {
+  return half_base(c, s.span_half);
 }
 
 // Submit and wait (the reference's synchronous RPC).
@@ -1158,7 +1210,7 @@ __device__ int64_t fetch_span_od(const DevCtx& c, Smem& s, int64_t fid, int64_t 
   if (hs < 0 || !od_submit(c, s, fid, page, span, hs, false)) return -1;
   if (!od_submit_run(c, s, fid, hs)) return -1;
   const int64_t n = od_wait(c, s, hs);
-  s.span_half = hs;
+  s.fetch_half = hs;
   return n;
 }
 
@@ -1190,7 +1242,7 @@ __device__ int64_t fetch_span(const DevCtx& c, Smem& s, int64_t fid, int64_t pag
     ST(rpc_requested_bytes) += span;
     account_transfer(c, s, n);
   }
-  s.span_half = h;
+  s.fetch_half = h;
   *span_out = span;
   return n;
 }
@@ -1232,7 +1284,11 @@ __device__ void copy_bytes(uint8_t* dst, const uint8_t* src, int64_t n) {
 template <int BS>
 __device__ void pull_span(const DevCtx& c, Smem& s) {
   if (s.pull_n <= 0) return;
-  copy_bytes<BS, SRC_SYS>((uint8_t*)span_base(c, s), s.pull_src, s.pull_n);
+  copy_bytes<BS, SRC_SYS>((uint8_t*)half_base(c, s.pull_half), s.pull_src, s.pull_n);
+  if (threadIdx.x == 0) {
+    s.dbg_land_off[s.pull_half] = s.pull_off;
+    s.dbg_land_n[s.pull_half] = s.pull_n;
+  }
   // the landing slot is read next by cp.async.bulk (async proxy): order these generic-proxy
   // stores before it (each writing thread fences, the barrier below publishes)
   asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -1587,9 +1643,15 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
         s.b.nb[0] = (int32_t)nb0;
         s.b.src_off[0] = 0;
         const int64_t m = (n + pg - 1) / pg;
-        if (m > 1) pb_fill(c, s, fid, page, m, n - nb0);
+        if (m > 1) {  // the span refills the private buffer, in the half it landed in
+          pb_fill(c, s, fid, page, m, n - nb0);
+          s.span_half = s.fetch_half;
+        }
       }
     }
+    // every page of a batch comes from one half: the fetched span's (page 0, and the
+    // private-buffer pages it brought), or the private buffer's
+    s.b.src_half = j0 ? s.fetch_half : s.span_half;
     if (status == 0 && j0 < kk) {
       if (pb_run(s, fid, p0 + j0, kk - j0) < kk - j0) {  // planned but absent: file shrank
         set_error(c, ERR_IO, (int)fid, (unsigned long long)(p0 + j0));
@@ -1603,7 +1665,7 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
   }
   __syncthreads();
   if (s.b.status != 0) return -1;
-  span_buf = span_base(c, s);  // an RPC may have switched landing halves
+  span_buf = half_base(c, s.b.src_half);  // an RPC may have switched landing halves
   if (w0) {  // private-buffer pages' bytes and span offsets; bind frames to their pages
     if (lane >= s.b.j0 && lane < kk) {
       const int64_t i = p0 + lane - s.pb_base;
@@ -1631,7 +1693,7 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
       // streamed window: the batch's span bytes must have landed
       int64_t need = 0;
       for (int j = 0; j < kk; j++) need = max(need, (int64_t)s.b.src_off[j] + s.b.nb[j]);
-      if (!wait_landed(c, s, s.span_half, need)) set_error(c, ERR_TIMEOUT, 24, 0);
+      if (!wait_landed(c, s, s.b.src_half, need)) set_error(c, ERR_TIMEOUT, 24, 0);
       s.b.tail_mask = tm;
       s.b.part_mask = pm;
       s.b.total = want;
@@ -1703,7 +1765,9 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
           const int64_t wi = wbase + 2 * v;
           const uint64_t tag = block_tag(cid, wi);
           const uint64_t lo = ((uint64_t)q.y << 32) | q.x, hi = ((uint64_t)q.w << 32) | q.z;
-          bad += (lo != mix64(tag ^ (uint64_t)wi)) + (hi != mix64(tag ^ (uint64_t)(wi + 1)));
+          const int nb2 = (lo != mix64(tag ^ (uint64_t)wi)) + (hi != mix64(tag ^ (uint64_t)(wi + 1)));
+          if (nb2) note_mismatch(c, s, fid, wi * 8, lo, s.b.src_off[0] + b0 + 16 * v, kk);
+          bad += nb2;
         }
         __syncwarp();
         if ((tid & 31) == 0) mbar_arrive(&s.tma_empty[st]);
@@ -1765,7 +1829,9 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
         const int64_t wi = (ps >> 3) + 2 * w;
         const uint64_t tag = block_tag(cid, wi);
         const uint64_t lo = ((uint64_t)q[u].y << 32) | q[u].x, hi = ((uint64_t)q[u].w << 32) | q[u].z;
-        bad += (lo != mix64(tag ^ (uint64_t)wi)) + (hi != mix64(tag ^ (uint64_t)(wi + 1)));
+        const int nb2 = (lo != mix64(tag ^ (uint64_t)wi)) + (hi != mix64(tag ^ (uint64_t)(wi + 1)));
+        if (nb2) note_mismatch(c, s, fid, wi * 8, lo, s.b.src_off[j] + 16 * w, kk);
+        bad += nb2;
       }
     }
   }
@@ -1936,7 +2002,7 @@ __device__ int64_t gread(const DevCtx& c, Smem& s, int64_t fid, int64_t offset, 
   const int64_t pg = c.page_size;
   const DevFile& F = c.files[fid];
   const int64_t fs = F.size;
-  const uint8_t* span_buf = span_base(c, s);
+  const uint8_t* span_buf = half_base(c, 0);  // raw mode: one span in half 0
   if (tid == 0) {
     ST(greads)++;
     s.g_lo = offset;
@@ -2070,6 +2136,7 @@ __device__ int64_t gread(const DevCtx& c, Smem& s, int64_t fid, int64_t offset, 
             act = A_PBHIT;
             s.nb = nb;
             s.src_off = (page - s.pb_base) * pg - s.pb_off_adj;
+            s.src_half = s.span_half;
           } else {
             int64_t span;
             int64_t n = fetch_span(c, s, fid, page, seg_end, &span, sync_m);
@@ -2078,11 +2145,12 @@ __device__ int64_t gread(const DevCtx& c, Smem& s, int64_t fid, int64_t offset, 
               s.n = n;
               s.nb = n < pg ? n : pg;
               s.src_off = 0;
+              s.src_half = s.fetch_half;
             }
           }
         }
       }
-      if ((act == A_PBHIT || act == A_RPC) && !wait_landed(c, s, s.span_half, s.src_off + s.nb))
+      if ((act == A_PBHIT || act == A_RPC) && !wait_landed(c, s, s.src_half, s.src_off + s.nb))
         act = A_ABORT;
       if (has_error(c)) act = A_ABORT;
       s.act = act;
@@ -2125,7 +2193,7 @@ __device__ int64_t gread(const DevCtx& c, Smem& s, int64_t fid, int64_t offset, 
       want = (g_end < pend ? g_end : pend) - g_pos;
     }
     const bool whole = d && in_page == 0 && want == nb && (((uintptr_t)d & 15) == 0);
-    const uint8_t* src = span_base(c, s) + s.src_off;
+    const uint8_t* src = half_base(c, s.src_half) + s.src_off;
     int bad = c.transfer != GFS_XFER_ZEROCOPY
                   ? copy_page_in<BS, SRC_HBM>(fmem, whole ? d : nullptr, src, nb, page * pg,
                                               c.verify ? F.content_id : -1)
@@ -2146,7 +2214,10 @@ __device__ int64_t gread(const DevCtx& c, Smem& s, int64_t fid, int64_t offset, 
       if (page_bad) ST(tag_mismatches)++;
       if (act == A_RPC) {
         int64_t m = (s.n + pg - 1) / pg;
-        if (m > 1) pb_fill(c, s, fid, page, m, s.n - nb);
+        if (m > 1) {
+          pb_fill(c, s, fid, page, m, s.n - nb);
+          s.span_half = s.fetch_half;
+        }
       }
       ST(user_bytes) += want;
       log_rec(c, GFS_LOG_DELIVERIES, s.tb, fid, page, 0);
@@ -2166,9 +2237,11 @@ __device__ void cta_begin(const DevCtx& c, Smem& s) {
   if (threadIdx.x == 0) {
     for (int i = 0; i < GFS_NSTATS; i++) s.st[i] = 0;
     s.pull_n = 0;
-    s.span_half = 0;
+    s.span_half = s.fetch_half = s.pull_half = s.src_half = 0;
     s.hp[0].pending = s.hp[1].pending = 0;
     s.hp_age = 0;
+    s.dbg_land_off[0] = s.dbg_land_off[1] = -1;
+    s.dbg_land_n[0] = s.dbg_land_n[1] = 0;
     s.st_seq[0] = s.st_seq[1] = 0;
     s.st_n[0] = s.st_n[1] = 0;
     s.st_landed[0] = s.st_landed[1] = 0;
@@ -2229,6 +2302,7 @@ __device__ void tb_begin(const DevCtx& c, Smem& s, int tb) {
     s.seg_lo = 0;
     s.seg_hi = 0;
     s.seg_ord = 0;
+    s.rpc_out = 0;
   }
   __syncthreads();
 }

@@ -224,6 +224,7 @@ struct gfs_ctx {
   long long* d_stats = nullptr;
   unsigned long long* d_scratch = nullptr;
   uint32_t* d_owner = nullptr;  // check_unique_mapping scratch (nframes), allocated on first use
+  uint32_t* d_slot_busy = nullptr;  // [rpc_slots]: the reference slot partition's occupancy
   unsigned long long* h_served = nullptr;  // mapped: requests completed by the daemon
   DevBuf<int64_t> d_segs, d_prog_off, d_dst_off, d_seg_dst;
   DevBuf<int32_t> d_order;
@@ -234,6 +235,7 @@ struct gfs_ctx {
 
   // mapped pinned host memory
   RpcReq* h_ring = nullptr;
+  uint32_t* h_consumed = nullptr;  // [ring_size]: seq of the request the daemon last copied out of each entry
   RpcResp* h_resp = nullptr;
   uint8_t* h_staging = nullptr;
 
@@ -386,6 +388,9 @@ static void worker_main(gfs_ctx* ctx, int wid) {
     ctx->w_phase[wid].store(1, std::memory_order_relaxed);
     const int64_t off = e->offset, size = e->size;
     const int fid = e->fid, slot = e->slot & 0x3FFFFFFF, half = (e->slot >> 30) & 1;
+    // the entry's fields are copied out: the device may reuse it (ring wrap) from now on,
+    // whether or not the CTA that asked has come back for its answer yet
+    __atomic_store_n(&ctx->h_consumed[h & mask], seq, __ATOMIC_RELEASE);
     int64_t n;
     uint8_t* buf;
     int b = 0;
@@ -515,6 +520,7 @@ static void reset_daemon(gfs_ctx* ctx) {
   cudaGetLastError();
   const uint64_t served = __atomic_load_n(ctx->h_served, __ATOMIC_ACQUIRE);
   memset(ctx->h_ring, 0, (size_t)ctx->ring_size * sizeof(RpcReq));
+  memset(ctx->h_consumed, 0, (size_t)ctx->ring_size * 4);
   memset(ctx->h_resp, 0, (size_t)ctx->n_ctas * ctx->landing_halves * sizeof(RpcResp));
   if (ctx->h_release) memset(ctx->h_release, 0, ctx->bounce_last.size() * 4);
   std::fill(ctx->bounce_last.begin(), ctx->bounce_last.end(), 0u);
@@ -544,7 +550,7 @@ static void free_all(gfs_ctx* ctx) {
     if (ev) cudaEventDestroy(ev);
   void* dev[] = {ctx->d_frames, ctx->d_fkey, ctx->d_fstate, ctx->d_own_q, ctx->d_retired, ctx->d_rpool, ctx->d_landed,
                  ctx->d_gfifo, ctx->d_recycled, ctx->d_g, ctx->d_landing, ctx->d_doorbell,
-                 ctx->d_done_pos, ctx->d_stats, ctx->d_scratch, ctx->d_owner};
+                 ctx->d_done_pos, ctx->d_stats, ctx->d_scratch, ctx->d_owner, ctx->d_slot_busy};
   for (void* p : dev)
     if (p) cudaFree(p);
   ctx->d_segs.release();
@@ -556,7 +562,7 @@ static void free_all(gfs_ctx* ctx) {
   for (auto& l : ctx->d_logs) l.release();
   for (auto ev : ctx->bounce_ev)
     if (ev) cudaEventDestroy(ev);
-  void* host[] = {ctx->h_ring, ctx->h_resp, ctx->h_staging, ctx->h_served, ctx->h_bounce,
+  void* host[] = {ctx->h_ring, ctx->h_consumed, ctx->h_resp, ctx->h_staging, ctx->h_served, ctx->h_bounce,
                   ctx->h_release};
   for (void* p : host)
     if (p) cudaFreeHost(p);
@@ -588,6 +594,8 @@ extern "C" int gfs_create(const gfs_config* cfg_in, gfs_ctx** out) {
   if (cfg.cta_threads != 128 && cfg.cta_threads != 256 && cfg.cta_threads != 512) cfg.cta_threads = 256;
   if (cfg.io_workers < 1) cfg.io_workers = 1;
   if (cfg.io_workers > 256) cfg.io_workers = 256;
+  if (cfg.rpc_slots == 0) cfg.rpc_slots = 128;  // rpc.n_slots default (config.py)
+  if (cfg.rpc_slots < 1) return fail(GFS_EINVAL, "rpc_slots must be >= 1");
   const int64_t nframes = cfg.cache_bytes / cfg.page_size;
   if (nframes >= (int64_t)PT_INFLIGHT) return fail(GFS_EINVAL, "too many frames (%lld)", (long long)nframes);
   const int64_t quota = nframes / cfg.resident_limit;  // gpu_cache.py:32-34
@@ -731,8 +739,10 @@ extern "C" int gfs_create(const gfs_config* cfg_in, gfs_ctx** out) {
   TRY(cudaMalloc(&ctx->d_done_pos, (size_t)ctx->ring_size * 8));
   TRY(cudaMalloc(&ctx->d_stats, (size_t)ctx->n_ctas * GFS_NSTATS * 8));
   TRY(cudaMalloc(&ctx->d_scratch, 64));
+  TRY(cudaMalloc(&ctx->d_slot_busy, (size_t)cfg.rpc_slots * 4));
   TRY(cudaHostAlloc(&ctx->h_ring, (size_t)ctx->ring_size * sizeof(RpcReq),
                     cudaHostAllocMapped | cudaHostAllocPortable));
+  TRY(cudaHostAlloc(&ctx->h_consumed, (size_t)ctx->ring_size * 4, cudaHostAllocMapped | cudaHostAllocPortable));
   TRY(cudaHostAlloc(&ctx->h_resp, (size_t)ctx->n_ctas * ctx->landing_halves * sizeof(RpcResp),
                     cudaHostAllocMapped | cudaHostAllocPortable));
   if (cfg.transfer == GFS_XFER_ZEROCOPY)
@@ -753,6 +763,7 @@ extern "C" int gfs_create(const gfs_config* cfg_in, gfs_ctx** out) {
     TRY(cudaMalloc(&ctx->d_landing, (size_t)(ctx->n_ctas * ctx->landing_halves * ctx->slot_bytes)));
   }
   memset(ctx->h_ring, 0, (size_t)ctx->ring_size * sizeof(RpcReq));
+  memset(ctx->h_consumed, 0, (size_t)ctx->ring_size * 4);
   memset(ctx->h_resp, 0, (size_t)ctx->n_ctas * ctx->landing_halves * sizeof(RpcResp));
   TRY(cudaHostAlloc(&ctx->h_served, 64, cudaHostAllocMapped | cudaHostAllocPortable));
   memset(ctx->h_served, 0, 64);
@@ -1086,6 +1097,7 @@ static int run_prepared(gfs_ctx* ctx, const gfs_program* prog, void* dst, const 
   CUDA_TRY(cudaMemsetAsync(ctx->d_g, 0, sizeof(DevGlobals), ctx->stream));
   CUDA_TRY(cudaMemsetAsync(ctx->d_stats, 0, (size_t)ctx->n_ctas * GFS_NSTATS * 8, ctx->stream));
   CUDA_TRY(cudaMemsetAsync(ctx->d_done_pos, 0, (size_t)ctx->ring_size * 8, ctx->stream));
+  CUDA_TRY(cudaMemsetAsync(ctx->d_slot_busy, 0, (size_t)cfg.rpc_slots * 4, ctx->stream));
 
   DevCtx c{};
   c.page_size = cfg.page_size;
@@ -1136,6 +1148,7 @@ static int run_prepared(gfs_ctx* ctx, const gfs_program* prog, void* dst, const 
   c.recycled = ctx->d_recycled;
   c.g = ctx->d_g;
   c.ring = ctx->h_ring;
+  c.ring_consumed = ctx->h_consumed;
   c.host_served = ctx->h_served;
   c.resp = ctx->h_resp;
   c.staging = ctx->h_staging;
@@ -1145,6 +1158,8 @@ static int run_prepared(gfs_ctx* ctx, const gfs_program* prog, void* dst, const 
   c.bounce_bytes = ctx->slot_bytes;
   c.doorbell = ctx->d_doorbell;
   c.done_pos = ctx->d_done_pos;
+  c.slot_busy = ctx->d_slot_busy;
+  c.ref_slots = cfg.rpc_slots;
   c.stats = ctx->d_stats;
   if (cons) c.cons = *cons;
   else c.cons.kind = GFS_CONSUME_NONE;
@@ -1225,6 +1240,14 @@ static int run_prepared(gfs_ctx* ctx, const gfs_program* prog, void* dst, const 
   out->v[GFS_STAT_host_requests] = ctx->n_served.load();
   out->v[GFS_STAT_io_workers] = ctx->cfg.io_workers;
   for (int k = 0; k < 5; k++) ctx->log_n[k] = std::min(g.log_n[k], ctx->log_cap[k]);
+  if (g.dbg[0] && getenv("GFS_DEBUG_MISMATCH"))
+    fprintf(stderr, "gfs: first K1 word mismatch: tb %llu cta %llu fid %llu file offset %llu read %#llx "
+            "landing half %llu span offset %llu batch pages %llu\n", g.dbg[1], g.dbg[7] >> 32, g.dbg[2], g.dbg[3],
+            g.dbg[4], g.dbg[5], g.dbg[6], g.dbg[7] & 0xFFFFFFFFull);
+  if (g.dbg[0] && getenv("GFS_DEBUG_MISMATCH"))
+    fprintf(stderr, "gfs:   landing half last pulled file offset %llu (%llu bytes); pb_base %llu pb_off_adj %llu "
+            "pb_count %llu j0 %llu; gread [%llu, %llu)\n", g.dbg[8], g.dbg[9], g.dbg[10], g.dbg[11], g.dbg[12],
+            g.dbg[13], g.dbg[14], g.dbg[15]);
   ctx->has_run = true;
   out->v[GFS_STAT_wall_ns] = (int64_t)(now_ns() - w0);
   if (g.error) {

@@ -65,6 +65,11 @@ struct DevGlobals {
   int error_info;
   unsigned long long error_arg;
   unsigned long long done_ctas;
+  // first K1 word mismatch seen (diagnostics, GFS_DEBUG_MISMATCH): set, tb, fid, file
+  // offset of the word, the word read, landing half, span offset, batch pages | cta << 32,
+  // then the landing half's last pull (file offset, bytes), pb_base, pb_off_adj, pb_count,
+  // batch first page, j0
+  unsigned long long dbg[16];
 };
 
 enum { ERR_NONE = 0, ERR_ALL_INFLIGHT = 1, ERR_NO_FRAME = 2, ERR_IO = 3, ERR_TIMEOUT = 4,
@@ -117,6 +122,7 @@ struct DevCtx {
   DevGlobals* g;
   // RPC (mapped pinned host memory, device-usable pointers)
   RpcReq* ring;
+  const uint32_t* ring_consumed;  // [ring_mask + 1]: seq the daemon last copied out of each entry
   // Requests completed by the daemon so far (mapped host memory).  Read once per launch
   // as the ring base: every earlier request is complete when a launch starts, so the
   // daemon's next expected position equals it — also under profiler kernel replay,
@@ -133,6 +139,9 @@ struct DevCtx {
   int64_t bounce_bytes;
   // ring reuse guard (device)
   unsigned long long* done_pos;  // [ring_mask + 1]: last completed ring position + 1 per entry
+  // the reference's RPC slot partition (rpc.n_slots): requests outstanding per slot tb % n
+  uint32_t* slot_busy;
+  int32_t ref_slots;
   // fused consumer (gfs_run_consume)
   gfs_consumer cons;
   // counters (device): [n_ctas][GFS_NSTATS]

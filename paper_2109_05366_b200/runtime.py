@@ -64,6 +64,7 @@ def native_config(cfg: ExperimentConfig, max_request_bytes: int = 0) -> native.G
     c.numa_pin = int(bool(cfg["io.numa_pin"]))
     c.lookahead = int(bool(cfg["gpu.lookahead"]))
     c.ra_clamp = native.RA_CLAMP[cfg["io.ra_clamp"]]
+    c.rpc_slots = cfg["rpc.n_slots"]
     return c
 
 

@@ -15,6 +15,6 @@ timeout 1200 python bench.py > $O/bench.log 2>&1; echo "bench rc=$?" >> $O/bench
 timeout 900 python bench.py --impl reference > $O/bench_ref.log 2>&1; echo "ref rc=$?" >> $O/bench_ref.log
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches.csv \
   python bench.py --quick --steps 2 --warmup 1 --no-clocks > $O/bench_ncu.log 2>&1
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:gread_driver -c 1 -o $O/gread_full -f \
+timeout 1200 ncu --replay-mode application --set full --clock-control none --import-source on -k regex:gread_driver -c 1 -o $O/gread_full -f \
   python tools/profile_run.py --size-gib 2 > $O/ncu_full.log 2>&1
 tail -3 $O/pytest_gpu.log 2>/dev/null; tail -2 $O/smoke.log; tail -c 1200 $O/bench.log; tail -c 600 $O/bench_ref.log
