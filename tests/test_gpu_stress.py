@@ -6,7 +6,7 @@ so only schedule-invariant quantities are compared: every delivered byte must sa
 file's word law (device check during the pass and `gfs_verify_dst` after it), and
 `greads` / `user_bytes` must equal the program's closed form (gpu_exec.py:95-129), and the
 page table must pass check_unique_mapping (gpu_cache.py:217-224) after every pass.  Each
-case runs twice on one context to shake out races between the passes."""
+case runs three times on one context to shake out races between the passes."""
 
 import os
 
@@ -19,7 +19,7 @@ from paper_2109_05366_b200.workloads import ProgramTable
 pytestmark = pytest.mark.gpu
 
 KiB, MiB = 1 << 10, 1 << 20
-N_CASES = 48
+N_CASES = 72
 TRANSFERS = ["mapped_dma", "mapped", "bounce", "dma", "zerocopy", "mapped_hybrid"]
 FILE_BYTES = [512 * MiB + 12345, 320 * MiB]
 
@@ -80,7 +80,7 @@ def test_random_multisegment_programs_full_residency(k):
         for cid, p in enumerate(paths):
             fs.gopen(p, content_id=cid)
         dst = torch.empty(table.dst_bytes, dtype=torch.uint8, device="cuda")
-        for rep in range(2):
+        for rep in range(3):
             dst.fill_(0xA5)
             r = fs.run(table, request, dst)
             st = r.stats
