@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define GFS_ABI_VERSION 5  /* 5: rpc_slots; 4: gfs_run_kernel (user kernels over gfs_device.cuh); 3: ondemand law */
+#define GFS_ABI_VERSION 6  /* 6: pull_helpers; 5: rpc_slots; 4: gfs_run_kernel (user kernels over gfs_device.cuh); 3: ondemand law */
 
 enum { GFS_OK = 0, GFS_EINVAL = -1, GFS_ECUDA = -2, GFS_EIO = -3, GFS_ENOMEM = -4,
        GFS_ETIMEDOUT = -5, GFS_EDEVICE = -6, GFS_ESTATE = -7 };
@@ -95,6 +95,8 @@ typedef struct gfs_config {
   int32_t ra_clamp;        /* io.ra_clamp: GFS_RA_CLAMP_* (ondemand) */
   int32_t rpc_slots;       /* rpc.n_slots (0 = 128): the reference's slot partition tb % n_slots,
                               for the slot_collisions counter (rpc.py:25-28, 82-89) */
+  int32_t pull_helpers;    /* gpu.pull_helpers: CTAs without a TB help pull other CTAs' spans
+                              from pinned host memory (mapped / small mapped_hybrid spans) */
 } gfs_config;
 
 /* One gread program set (workloads.py:24-31 programs, flattened).

@@ -205,6 +205,12 @@ struct Smem {
   } hp[2];
   uint32_t hp_age;
   uint32_t rpc_out;  // this TB's requests outstanding (submitted, not yet waited for)
+  int pjob_active[2];  // landing half h has a posted pull job (pull helpers)
+  int pull_job;        // half whose pull job pull_span finishes, -1 = none
+  int hj_stop, hj_k;   // pull-job chunk broadcast (owner finish / helper loop)
+  const uint8_t* hj_src;
+  uint8_t* hj_dst;
+  int64_t hj_n;
   int64_t pull_off;            // file offset of the span waiting to be pulled
   int64_t dbg_land_off[2], dbg_land_n[2];  // what each landing half last received (diagnostics)
   uint32_t pb_absent[MAX_PB_ENTRIES / 32];  // private-buffer entries consumed / dropped
@@ -699,6 +705,96 @@ __device__ __forceinline__ void account_transfer(const DevCtx& c, Smem& s, int64
   }
 }
 
+// ------------------------------------------------------------ pull helpers
+//
+// Spans that a CTA pulls itself from pinned host memory (mapped transfers; small
+// mapped_hybrid spans) are posted at submit time as chunked jobs.  CTAs without a TB (the
+// dispatcher ran dry: few TBs, or the tail of a pass) claim chunks of any posted job and
+// copy them into its landing half; the owner claims and copies what is left when it gets
+// to the span, then waits for the chunks in flight.  Each chunk is copied exactly once:
+// claims come from one atomic counter that carries the job's sequence number and chunk
+// count, and a job slot is reposted only after all its chunks are done.
+
+template <int BS, int SRC>
+__device__ void copy_bytes(uint8_t* dst, const uint8_t* src, int64_t n);
+__device__ __forceinline__ const uint8_t* half_base(const DevCtx& c, int h);
+
+__device__ __forceinline__ int pj_id(int h) { return (int)blockIdx.x * 2 + h; }
+
+// Whether a span of n bytes that the CTA would pull goes through a job.
+__device__ __forceinline__ bool pj_wanted(const DevCtx& c, int64_t n) {
+  if (!c.helpers || n < 2 * c.pull_chunk) return false;
+  if (c.transfer == GFS_XFER_MAPPED_ZC) return true;
+  if (c.transfer == GFS_XFER_MAPPED_HYBRID) return n < c.ce_min;  // the daemon's rule (gfs_host.cpp)
+  return false;
+}
+
+// Post the pull of [off, off + n) of fid into landing half h (thread 0).
+__device__ void pj_post(const DevCtx& c, Smem& s, int64_t fid, int64_t off, int64_t n, int h) {
+  const int j = pj_id(h);
+  PullJob& J = c.pjobs[j];
+  const unsigned long long nch = (unsigned long long)((n + c.pull_chunk - 1) / c.pull_chunk);
+  const unsigned long long seq = ((atomicAdd(&J.ctl, 0ull) >> 48) + 1) & 0xFFFFull;
+  J.src = c.files[fid].map + off;
+  J.dst = (uint8_t*)half_base(c, h);
+  J.bytes = n;
+  J.done = 0;
+  __threadfence();  // the descriptor before the claims it enables
+  atomicExch(&J.ctl, (seq << 48) | (nch << 32));
+  atomicOr(&c.pjob_bits[j >> 5], 1u << (j & 31));
+  s.pjob_active[h] = 1;
+}
+
+// Claim a chunk of job j (one thread): its index, or -1 when every chunk is taken.  The
+// chunk's source / destination / bytes go to s.hj_*.
+__device__ int pj_claim(const DevCtx& c, Smem& s, int j) {
+  PullJob& J = c.pjobs[j];
+  const unsigned long long old = atomicAdd(&J.ctl, 1ull);
+  const uint32_t k = (uint32_t)old, n = (uint32_t)(old >> 32) & 0xFFFFu;
+  if (k >= n) return -1;
+  if (k == n - 1) atomicAnd(&c.pjob_bits[j >> 5], ~(1u << (j & 31)));  // nothing left to claim
+  __threadfence();  // descriptor reads after the claim (posted before the ctl that enabled it)
+  const int64_t o = (int64_t)k * c.pull_chunk;
+  const int64_t bytes = (int64_t)__ldcg((const long long*)&J.bytes);
+  s.hj_src = (const uint8_t*)__ldcg((const unsigned long long*)&J.src) + o;
+  s.hj_dst = (uint8_t*)__ldcg((const unsigned long long*)&J.dst) + o;
+  s.hj_n = bytes - o < c.pull_chunk ? bytes - o : c.pull_chunk;
+  return (int)k;
+}
+
+// Copy the claimed chunk in s.hj_* (all threads) and count it done.
+template <int BS>
+__device__ void pj_copy_done(const DevCtx& c, Smem& s, int j) {
+  copy_bytes<BS, SRC_SYS>(s.hj_dst, s.hj_src, s.hj_n);
+  asm volatile("fence.proxy.async.global;" ::: "memory");  // read next by TMA (async proxy)
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(&c.pjobs[j].done, 1u);
+  }
+}
+
+// Wait until every chunk of job j is done (thread 0).  False on abort.
+__device__ bool pj_wait_done(const DevCtx& c, int j) {
+  PullJob& J = c.pjobs[j];
+  const uint32_t n = (uint32_t)(atomicAdd(&J.ctl, 0ull) >> 32) & 0xFFFFu;
+  const uint64_t t0 = globaltimer();
+  while (ld_acquire_gpu(&J.done) < n) {
+    if (!keep_waiting(c, t0, 25)) return false;
+    __nanosleep(200);
+  }
+  return true;
+}
+
+// A posted job whose bytes the CTA will not use (a dropped window, thread 0): claim what is
+// left without copying, wait for the helpers' chunks in flight.
+__device__ bool pj_cancel(const DevCtx& c, Smem& s, int h) {
+  const int j = pj_id(h);
+  while (pj_claim(c, s, j) >= 0) atomicAdd(&c.pjobs[j].done, 1u);
+  s.pjob_active[h] = 0;
+  return pj_wait_done(c, j);
+}
+
 // Submit one request for this CTA's slot into landing half `half` (thread 0): rpc.py:82-102.
 // Returns false on abort; *seq_out / *pos_out identify it for rpc_wait.
 __device__ bool rpc_submit(const DevCtx& c, Smem& s, int64_t fid, int64_t off, int64_t size, int half,
@@ -741,6 +837,10 @@ __device__ bool rpc_submit(const DevCtx& c, Smem& s, int64_t fid, int64_t off, i
   // readahead runs inside the host's pread, not through the slot)
   if (atomicAdd(&c.slot_busy[s.tb % c.ref_slots], 1u) > s.rpc_out) ST(slot_collisions)++;
   s.rpc_out++;
+  // a span the CTA will pull from the pinned mapping: post it so idle CTAs start on it now
+  const int64_t fsz = c.files[fid].size;
+  const int64_t nexp = off >= fsz ? 0 : (size < fsz - off ? size : fsz - off);  // the daemon's answer
+  if (pj_wanted(c, nexp)) pj_post(c, s, fid, off, nexp, half);
   return true;
 }
 
@@ -779,11 +879,18 @@ __device__ int64_t rpc_wait(const DevCtx& c, Smem& s, int64_t fid, int64_t off, 
         n = (int64_t)((v >> 32) & 0x7FFFFFFFull);
         if (n == 0x7FFFFFFFll) n = -1;
         if ((v >> 63) && n > 0) {
-          s.pull_n = n;
-          s.pull_buf = -1;
-          s.pull_src = c.files[fid].map + off;
-          s.pull_off = off;
-          s.pull_half = half;
+          if (s.pjob_active[half]) {
+            s.pull_job = half;
+          } else {
+            s.pull_n = n;
+            s.pull_buf = -1;
+            s.pull_src = c.files[fid].map + off;
+            s.pull_off = off;
+            s.pull_half = half;
+          }
+        } else if (s.pjob_active[half] && n > 0) {  // copied by the engine after all: a rule mismatch
+          set_error(c, ERR_IO, (int)fid, (unsigned long long)off);
+          return -1;
         }
         break;
       }
@@ -806,6 +913,8 @@ __device__ int64_t rpc_wait(const DevCtx& c, Smem& s, int64_t fid, int64_t off, 
           s.pull_off = off;
           s.pull_half = half;
           s.pull_seq = seq;
+        } else if (c.transfer == GFS_XFER_MAPPED_ZC && n > 0 && s.pjob_active[half]) {
+          s.pull_job = half;  // posted: the owner finishes it in pull_span
         } else if (c.transfer == GFS_XFER_MAPPED_ZC && n > 0) {  // straight from the page cache
           s.pull_n = n;
           s.pull_buf = -1;
@@ -1087,6 +1196,11 @@ __device__ int64_t od_wait(const DevCtx& c, Smem& s, int h) {
 __device__ int od_drain(const DevCtx& c, Smem& s, int h) {
   const int64_t n = od_wait(c, s, h);
   if (n < 0 || !wait_landed(c, s, h, n)) return -1;
+  if (s.pull_job >= 0) {  // never pulled: stop the helpers on it
+    const int pj = s.pull_job;
+    s.pull_job = -1;
+    if (!pj_cancel(c, s, pj)) return -1;
+  }
   if (s.pull_n > 0) {  // never pulled: hand a bounce buffer straight back
     if (s.pull_buf >= 0) {
       __threadfence_system();
@@ -1283,6 +1397,24 @@ __device__ void copy_bytes(uint8_t* dst, const uint8_t* src, int64_t n) {
 // CTA's HBM landing slot in one bulk pass, then hand the buffer back to its worker.
 template <int BS>
 __device__ void pull_span(const DevCtx& c, Smem& s) {
+  if (s.pull_job >= 0) {  // a posted job: claim and copy what the helpers left, wait for theirs
+    const int h = s.pull_job, j = pj_id(h);
+    for (;;) {
+      if (threadIdx.x == 0) s.hj_k = pj_claim(c, s, j);
+      __syncthreads();
+      const int k = s.hj_k;
+      if (k < 0) break;
+      pj_copy_done<BS>(c, s, j);  // ends with a barrier: s.hj_* may be rewritten after it
+    }
+    if (threadIdx.x == 0) {
+      if (!pj_wait_done(c, j)) set_error(c, ERR_TIMEOUT, 25, 0);
+      s.pjob_active[h] = 0;
+      s.pull_job = -1;
+      s.dbg_land_off[h] = -2;  // (pulled by a job)
+    }
+    __syncthreads();
+    return;
+  }
   if (s.pull_n <= 0) return;
   copy_bytes<BS, SRC_SYS>((uint8_t*)half_base(c, s.pull_half), s.pull_src, s.pull_n);
   if (threadIdx.x == 0) {
@@ -1521,7 +1653,11 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
   if (c.policy == GFS_POLICY_GLOBAL_LRU) nmax = (int)min((int64_t)nmax, max((int64_t)1, c.nframes / 4));
   uint32_t* pt = F.pt;
   uint64_t t_start = 0;
-  if (tid == 0) t_start = globaltimer();
+  long long wait0 = 0;
+  if (tid == 0) {
+    t_start = globaltimer();
+    wait0 = ST(wait_ns);
+  }
   if (c.readahead == GFS_RA_ONDEMAND) {  // markers and pending windows at the walk position
     if (tid == 0) {
       if (!od_top(c, s, fid, p0)) set_error(c, ERR_IO, (int)fid, (unsigned long long)p0);
@@ -1698,7 +1834,7 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
       s.b.part_mask = pm;
       s.b.total = want;
       const uint64_t t1 = globaltimer();
-      ST(meta_ns) += (long long)(t1 - t_start);
+      ST(meta_ns) += (long long)(t1 - t_start) - (ST(wait_ns) - wait0);  // RPC waits counted apart
       s.t_copy0 = t1;
     }
   }
@@ -2241,6 +2377,8 @@ __device__ void cta_begin(const DevCtx& c, Smem& s) {
     s.hp[0].pending = s.hp[1].pending = 0;
     s.hp_age = 0;
     s.dbg_land_off[0] = s.dbg_land_off[1] = -1;
+    s.pjob_active[0] = s.pjob_active[1] = 0;
+    s.pull_job = -1;
     s.dbg_land_n[0] = s.dbg_land_n[1] = 0;
     s.st_seq[0] = s.st_seq[1] = 0;
     s.st_n[0] = s.st_n[1] = 0;
@@ -2320,6 +2458,7 @@ __device__ void tb_end(const DevCtx& c, Smem& s) {
     s.pb_count = 0;
     if (c.policy == GFS_POLICY_PER_TB_LRA && s.own_len > 0)
       ret_pos = atomicAdd(rp_tail(c, (int)(blockIdx.x % (unsigned)c.ret_npools)), (unsigned long long)s.own_len);
+    atomicAdd(&c.g->tbs_done, 1ull);
   }
   __syncthreads();
   if (c.policy == GFS_POLICY_PER_TB_LRA && s.own_len > 0) {
@@ -2330,6 +2469,54 @@ __device__ void tb_end(const DevCtx& c, Smem& s) {
     }
   }
   __syncthreads();
+}
+
+// A CTA the dispatcher has no TB for: copy chunks of other CTAs' posted pull jobs until every
+// TB is done (all threads).
+template <int BS>
+__device__ void pull_helper(const DevCtx& c, Smem& s) {
+  if (!c.helpers) return;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int nw = (c.n_ctas * 2 + 31) / 32;
+  for (;;) {
+    if (tid < 32) {
+      bool stop = false;
+      int j = -1, k = -1;
+      if (lane == 0) stop = has_error(c) || ld_volatile_u64(&c.g->tbs_done) >= (unsigned long long)c.n_tb;
+      stop = __shfl_sync(0xffffffffu, stop, 0);
+      for (int w0 = 0; !stop && w0 < nw && k < 0; w0 += 32) {
+        const int w = (w0 + lane + (int)blockIdx.x) % nw;  // CTAs start at different words
+        const uint32_t bits = w0 + lane < nw ? ld_acquire_gpu(&c.pjob_bits[w]) : 0u;
+        unsigned cand = __ballot_sync(0xffffffffu, bits != 0u);
+        while (cand && k < 0) {
+          const int src = __ffs(cand) - 1;
+          cand &= cand - 1;
+          if (lane == src) {
+            const int b = __ffs(bits) - 1;
+            j = w * 32 + b;
+            k = pj_claim(c, s, j);
+          }
+          k = __shfl_sync(0xffffffffu, k, src);
+          j = __shfl_sync(0xffffffffu, j, src);
+        }
+      }
+      if (lane == 0) {
+        s.hj_stop = stop;
+        s.hj_k = k;
+        s.k = j;
+      }
+    }
+    __syncthreads();
+    const bool stop = s.hj_stop;
+    const int k = s.hj_k, j = (int)s.k;
+    __syncthreads();
+    if (stop) break;
+    if (k < 0) {
+      __nanosleep(1000);
+      continue;
+    }
+    pj_copy_done<BS>(c, s, j);
+  }
 }
 
 // CTA end: word mismatches seen by the K1 checks, counters out.

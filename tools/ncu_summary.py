@@ -69,18 +69,25 @@ def main():
                          capture_output=True, text=True).stdout
     srows = list(csv.reader(io.StringIO(src)))
     hot = []
-    if len(srows) > 3 and "Warp Stall Sampling (All Samples)" in srows[2]:
-        iS = srows[2].index("Warp Stall Sampling (All Samples)")
-        for r in srows[3:]:
-            if len(r) > iS and r[0] not in ("", "-") and r[2] == "-":
-                try:
-                    hot.append((int(r[iS]), int(r[0]), r[1].strip()[:100]))
-                except ValueError:
-                    pass
+    # the page lists one section per source file ("File Path" / "File Name" rows), each with
+    # its own header row
+    cur, iS = "?", None
+    for r in srows:
+        if r and r[0] in ("File Path", "File Name") and len(r) > 1:
+            cur = os.path.basename(r[1])
+            continue
+        if r and r[0] == "Line No":
+            iS = r.index("Warp Stall Sampling (All Samples)") if "Warp Stall Sampling (All Samples)" in r else None
+            continue
+        if iS is not None and len(r) > iS and r[0] not in ("", "-") and r[2] == "-":
+            try:
+                hot.append((int(r[iS]), f"{cur}:{int(r[0])}", r[1].strip()[:100]))
+            except ValueError:
+                pass
+    if hot:
         tot = sum(h[0] for h in hot) or 1
         hot.sort(reverse=True)
-        summary["hot_source_lines"] = [{"line": f"gfs_kernels.cu:{ln}", "samples": n,
-                                        "share": round(n / tot, 4), "source": sl}
+        summary["hot_source_lines"] = [{"line": ln, "samples": n, "share": round(n / tot, 4), "source": sl}
                                        for n, ln, sl in hot[:a.source_top]]
     with open(os.path.join(a.outdir, f"ncu_{a.tag}_summary.json"), "w") as fh:
         json.dump(summary, fh, indent=1)
