@@ -313,7 +313,9 @@ def storage_label(cfg, transfer: str) -> str:
                             "pulled by the CTA (no pread)",
            "bounce": "O_DIRECT pread into a pinned pool, pulled by the CTA",
            "dma": "O_DIRECT pread into a pinned pool, cudaMemcpyAsync to HBM",
-           "zerocopy": "O_DIRECT pread into per-CTA pinned staging, pulled by the CTA"}
+           "zerocopy": "O_DIRECT pread into per-CTA pinned staging, pulled by the CTA",
+           "pread_hybrid": "O_DIRECT pread into a pinned pool; spans >= 4 MiB by cudaMemcpyAsync, "
+                           "smaller pulled by the CTA"}
     fs = "tmpfs" if cfg["mode.ramfs"] else "disk"
     return f"{fs} {d}: {how.get(transfer, transfer)}"
 
@@ -322,7 +324,7 @@ def pread_daemon_line(arms: dict, io_peak) -> dict | None:
     """The north_star data path (O_DIRECT pread -> pinned staging -> HBM) as a first-class
     number beside the headline: the better of the bounce and dma arms, against the same
     roofline."""
-    cands = {k: arms[k] for k in ("pread_bounce_adaptive", "pread_dma_adaptive")
+    cands = {k: arms[k] for k in ("pread_bounce_adaptive", "pread_dma_adaptive", "pread_hybrid_adaptive")
              if k in arms and "gbps" in arms[k]}
     if not cands:
         return None
@@ -799,6 +801,7 @@ def comparison_arms(cfg, path: str, device: int, head, probes: dict) -> tuple[di
         "pread_bounce_static": {"io.transfer": "bounce", "io.readahead": "static"},
         "pread_zerocopy_adaptive": {"io.transfer": "zerocopy"},
         "pread_dma_adaptive": {"io.transfer": "dma"},
+        "pread_hybrid_adaptive": {"io.transfer": "pread_hybrid"},
         "mapped_dma_adaptive": {"io.transfer": "mapped_dma"},
         "static_prefetch": {"io.readahead": "static"},
         "global_lru_prefetch": {"gpufs.policy": "global-lru-dealloc"},

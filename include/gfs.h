@@ -51,9 +51,11 @@ enum { GFS_RA_CLAMP_SEGMENT = 0, GFS_RA_CLAMP_EOF = 1 };
  *          from the pinned page-cache mapping into its HBM landing slot itself;
  * mapped_hybrid = mapped, but spans of >= 4 MiB go by copy engine (mapped_dma): SM pulls
  *          cap at ~51.5 GB/s on PCIe Gen5 x16, large copy-engine copies reach ~55, small
- *          copy-engine copies pay a fixed cost each */
+ *          copy-engine copies pay a fixed cost each;
+ * pread_hybrid = the pread daemon for any file: O_DIRECT pread into a pinned pool, then spans
+ *          of >= 4 MiB by cudaMemcpyAsync (dma), smaller ones pulled by the CTA (bounce) */
 enum { GFS_XFER_ZEROCOPY = 0, GFS_XFER_DMA = 1, GFS_XFER_BOUNCE = 2, GFS_XFER_MAPPED = 3,
-       GFS_XFER_MAPPED_ZC = 4, GFS_XFER_MAPPED_HYBRID = 5 };
+       GFS_XFER_MAPPED_ZC = 4, GFS_XFER_MAPPED_HYBRID = 5, GFS_XFER_PREAD_HYBRID = 6 };
 /* gopen flags: read-only files are the only ones prefetched (prefetcher.py:22-24) */
 enum { GFS_O_RDONLY = 0, GFS_O_RDWR = 2 };
 /* log kinds (deterministic mode) */

@@ -867,7 +867,7 @@ __device__ int64_t rpc_wait(const DevCtx& c, Smem& s, int64_t fid, int64_t off, 
       }
       __nanosleep(256);
     }
-  } else if (c.transfer == GFS_XFER_MAPPED_HYBRID) {
+  } else if (c.transfer == GFS_XFER_MAPPED_HYBRID || c.transfer == GFS_XFER_PREAD_HYBRID) {
     // the daemon answers either by copy engine (doorbell in HBM, data already in the landing
     // slot) or by mailbox (the CTA pulls the span from the pinned page-cache mapping)
     // (both answers arrive through the HBM doorbell, so nothing polls host memory: bit 63
@@ -879,7 +879,15 @@ __device__ int64_t rpc_wait(const DevCtx& c, Smem& s, int64_t fid, int64_t off, 
         n = (int64_t)((v >> 32) & 0x7FFFFFFFull);
         if (n == 0x7FFFFFFFll) n = -1;
         if ((v >> 63) && n > 0) {
-          if (s.pjob_active[half]) {
+          if (c.transfer == GFS_XFER_PREAD_HYBRID) {  // in pool buffer r->buf (written before the doorbell)
+            const RpcResp* r = &c.resp[(int64_t)slot * c.landing_halves + half];
+            s.pull_n = n;
+            s.pull_buf = (int32_t)ld_acquire_sys((const uint32_t*)&r->buf);
+            s.pull_src = c.bounce + (int64_t)s.pull_buf * c.bounce_bytes;
+            s.pull_seq = seq;
+            s.pull_off = off;
+            s.pull_half = half;
+          } else if (s.pjob_active[half]) {
             s.pull_job = half;
           } else {
             s.pull_n = n;
@@ -1171,7 +1179,10 @@ __device__ bool od_submit(const DevCtx& c, Smem& s, int64_t fid, int64_t page, i
   s.hp[h].span = span;
   s.hp[h].age = ++s.hp_age;
   s.hp[h].pending = pending;
-  s.hp[h].deferred = pending && c.transfer == GFS_XFER_BOUNCE;
+  // a window pulled out of a host pool buffer would hold that buffer until adopted
+  const int64_t nexp = span < c.files[fid].size - page * c.page_size ? span : c.files[fid].size - page * c.page_size;
+  s.hp[h].deferred = pending && (c.transfer == GFS_XFER_BOUNCE ||
+                                 (c.transfer == GFS_XFER_PREAD_HYBRID && nexp < c.ce_min));
   if (s.hp[h].deferred) return true;
   if (!wait_landed(c, s, h, s.st_n[h])) return false;
   return rpc_submit(c, s, fid, page * c.page_size, span, h, &s.hp[h].seq, &s.hp[h].pos);

@@ -257,6 +257,7 @@ struct gfs_ctx {
   // bounce mode: the same pool, mapped; the GPU writes release words after pulling a span
   uint32_t* h_release = nullptr;       // [io_workers * nbounce] (mapped)
   std::vector<uint32_t> bounce_last;   // seq last stored in each buffer (0 = free)
+  std::vector<char> bounce_ce;         // pread_hybrid: the buffer's last use was a copy-engine copy
   std::atomic<uint64_t> req_head{0};
   // daemon accounting for the current run (ns summed over workers)
   std::atomic<int64_t> t_pread{0}, t_idle{0}, t_xfer{0}, n_served{0};
@@ -359,11 +360,12 @@ static void worker_main(gfs_ctx* ctx, int wid) {
   const bool dma = ctx->cfg.transfer == GFS_XFER_DMA;
   const bool bounce = ctx->cfg.transfer == GFS_XFER_BOUNCE;
   const bool hybrid = ctx->cfg.transfer == GFS_XFER_MAPPED_HYBRID;
+  const bool phyb = ctx->cfg.transfer == GFS_XFER_PREAD_HYBRID;  // pread: large spans dma, small pulled
   const bool mapped_ce = ctx->cfg.transfer == GFS_XFER_MAPPED;     // copy engine from the mapping
   const bool mapped_zc = ctx->cfg.transfer == GFS_XFER_MAPPED_ZC;  // the CTA pulls it itself
   const bool from_map = mapped_ce || mapped_zc || hybrid;
   const int64_t ce_min = ctx->ce_min;  // hybrid: spans this large go by copy engine
-  cudaStream_t st = (dma || mapped_ce || hybrid)
+  cudaStream_t st = (dma || mapped_ce || hybrid || phyb)
                         ? ctx->worker_streams[(size_t)wid % ctx->worker_streams.size()]
                         : nullptr;
   if (st) cudaSetDevice(ctx->cfg.device);
@@ -400,8 +402,12 @@ static void worker_main(gfs_ctx* ctx, int wid) {
       b = wid * ctx->nbounce + (int)(nreq % (uint64_t)ctx->nbounce);
       if (nreq >= (uint64_t)ctx->nbounce) cudaEventSynchronize(ctx->bounce_ev[b]);
       buf = ctx->h_bounce + (int64_t)b * ctx->slot_bytes;
-    } else if (bounce) {  // next pool buffer, once the CTA that used it last pulled it out
+    } else if (bounce || phyb) {  // next pool buffer, once the CTA that used it last pulled it out
       b = wid * ctx->nbounce + (int)(nreq % (uint64_t)ctx->nbounce);
+      if (phyb && ctx->bounce_ce[b]) {  // (pread_hybrid) or its copy engine copy drained
+        cudaEventSynchronize(ctx->bounce_ev[b]);
+        ctx->bounce_ce[b] = 0;
+      }
       const uint32_t last = ctx->bounce_last[b];
       uint64_t sp = 0;
       while (last && __atomic_load_n(&ctx->h_release[b], __ATOMIC_ACQUIRE) != last) {
@@ -438,8 +444,8 @@ static void worker_main(gfs_ctx* ctx, int wid) {
     if (n < 0) ctx->worker_error.store((int)-n);
     // count it before completing: a launch that starts after this completion must see it
     __atomic_fetch_add(ctx->h_served, 1ull, __ATOMIC_SEQ_CST);
-    if (dma || mapped_ce || hybrid) {
-      const bool copy = !hybrid || n >= ce_min;  // hybrid: small spans are pulled by the CTA
+    if (dma || mapped_ce || hybrid || phyb) {
+      const bool copy = !(hybrid || phyb) || n >= ce_min;  // hybrids: small spans are pulled by the CTA
       cudaError_t ce = cudaSuccess;
       cudaStream_t bs = ctx->bell_streams[(size_t)wid % ctx->bell_streams.size()];
       const int64_t li = (int64_t)slot * ctx->landing_halves + half;
@@ -447,7 +453,17 @@ static void worker_main(gfs_ctx* ctx, int wid) {
       const bool streamed = copy && ctx->stream_pieces && n >= 2 * piece;
       if (n > 0 && copy && !streamed) {
         ce = cudaMemcpyAsync(ctx->d_landing + li * ctx->slot_bytes, buf, (size_t)n, cudaMemcpyHostToDevice, st);
-        if (ce == cudaSuccess && dma) ce = cudaEventRecord(ctx->bounce_ev[b], st);
+        if (ce == cudaSuccess && (dma || phyb)) ce = cudaEventRecord(ctx->bounce_ev[b], st);
+        if (phyb) {  // the copy engine frees the buffer: no CTA release to wait for
+          ctx->bounce_ce[b] = 1;
+          ctx->bounce_last[b] = 0;
+        }
+      }
+      if (phyb && n <= 0) ctx->bounce_last[b] = 0;  // nothing to pull: the buffer stays free
+      if (phyb && !copy && n > 0) {  // the CTA pulls it from pool buffer b: say which, before the doorbell
+        RpcResp* r = &ctx->h_resp[li];
+        r->buf = b;
+        __atomic_thread_fence(__ATOMIC_RELEASE);
       }
       if (streamed) {
         // the window in pieces: after each, a landed marker; after the first, the doorbell —
@@ -526,6 +542,7 @@ static void reset_daemon(gfs_ctx* ctx) {
   memset(ctx->h_resp, 0, (size_t)ctx->n_ctas * ctx->landing_halves * sizeof(RpcResp));
   if (ctx->h_release) memset(ctx->h_release, 0, ctx->bounce_last.size() * 4);
   std::fill(ctx->bounce_last.begin(), ctx->bounce_last.end(), 0u);
+  std::fill(ctx->bounce_ce.begin(), ctx->bounce_ce.end(), (char)0);  // worker streams were synchronized
   if (ctx->d_doorbell) cudaMemset(ctx->d_doorbell, 0, (size_t)ctx->n_ctas * ctx->landing_halves * 8);
   if (ctx->d_landed) cudaMemset(ctx->d_landed, 0, (size_t)ctx->n_ctas * ctx->landing_halves * 8);
   ctx->req_head.store(served);
@@ -587,6 +604,8 @@ extern "C" int gfs_create(const gfs_config* cfg_in, gfs_ctx** out) {
   if (cfg.staging_bytes < 1) return fail(GFS_EINVAL, "staging_bytes must be >= 1");
   if (cfg.policy != GFS_POLICY_GLOBAL_LRU && cfg.policy != GFS_POLICY_PER_TB_LRA)
     return fail(GFS_EINVAL, "unknown policy %d", cfg.policy);
+  if (cfg.transfer < GFS_XFER_ZEROCOPY || cfg.transfer > GFS_XFER_PREAD_HYBRID)
+    return fail(GFS_EINVAL, "unknown transfer %d", cfg.transfer);
   if (cfg.readahead < GFS_RA_STATIC || cfg.readahead > GFS_RA_ONDEMAND)
     return fail(GFS_EINVAL, "unknown readahead mode %d", cfg.readahead);
   if (cfg.readahead != GFS_RA_STATIC && (cfg.ra_max_bytes < cfg.page_size || cfg.ra_max_bytes % cfg.page_size))
@@ -653,7 +672,7 @@ extern "C" int gfs_create(const gfs_config* cfg_in, gfs_ctx** out) {
   TRY(cudaEventCreate(&ctx->ev0));
   TRY(cudaEventCreate(&ctx->ev1));
   if (cfg.transfer == GFS_XFER_DMA || cfg.transfer == GFS_XFER_MAPPED ||
-      cfg.transfer == GFS_XFER_MAPPED_HYBRID) {
+      cfg.transfer == GFS_XFER_MAPPED_HYBRID || cfg.transfer == GFS_XFER_PREAD_HYBRID) {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult qr;
     TRY(cudaGetDriverEntryPoint("cuStreamWriteValue64", &fn, cudaEnableDefault, &qr));
@@ -708,7 +727,7 @@ extern "C" int gfs_create(const gfs_config* cfg_in, gfs_ctx** out) {
               ctx->probe_attempts - 1);
     if (!ok) {
       const int was = cfg.transfer;
-      cfg.transfer = was == GFS_XFER_DMA ? GFS_XFER_BOUNCE : GFS_XFER_MAPPED_ZC;
+      cfg.transfer = (was == GFS_XFER_DMA || was == GFS_XFER_PREAD_HYBRID) ? GFS_XFER_BOUNCE : GFS_XFER_MAPPED_ZC;
       ctx->cfg.transfer = cfg.transfer;
       ctx->downgraded_from = was;
       for (auto s : ctx->worker_streams) cudaStreamDestroy(s);
@@ -772,13 +791,14 @@ extern "C" int gfs_create(const gfs_config* cfg_in, gfs_ctx** out) {
   TRY(cudaHostAlloc(&ctx->h_served, 64, cudaHostAllocMapped | cudaHostAllocPortable));
   memset(ctx->h_served, 0, 64);
   if (cfg.transfer == GFS_XFER_DMA || cfg.transfer == GFS_XFER_MAPPED ||
-      cfg.transfer == GFS_XFER_MAPPED_HYBRID) {
+      cfg.transfer == GFS_XFER_MAPPED_HYBRID || cfg.transfer == GFS_XFER_PREAD_HYBRID) {
     TRY(cudaMalloc(&ctx->d_landing, (size_t)(ctx->n_ctas * ctx->landing_halves * ctx->slot_bytes)));
     // experiments: GFS_STREAM_PIECE_MIB (0 = off, the default: whole-window copies measured
     // faster on the headline, 54.0 vs 51.9 GB/s with 4 MiB pieces)
     ctx->stream_piece = 0;
     if (const char* e = getenv("GFS_STREAM_PIECE_MIB")) ctx->stream_piece = (int64_t)atoi(e) << 20;
     ctx->stream_pieces = ctx->stream_piece > 0 && !cfg.raw_mode && cfg.transfer != GFS_XFER_MAPPED_HYBRID &&
+                         cfg.transfer != GFS_XFER_PREAD_HYBRID &&
                          ctx->slot_bytes >= 2 * ctx->stream_piece;
     TRY(cudaMalloc(&ctx->d_landed, (size_t)ctx->n_ctas * ctx->landing_halves * 8));
     TRY(cudaMemset(ctx->d_landed, 0, (size_t)ctx->n_ctas * ctx->landing_halves * 8));
@@ -786,6 +806,19 @@ extern "C" int gfs_create(const gfs_config* cfg_in, gfs_ctx** out) {
     TRY(cudaMemset(ctx->d_doorbell, 0, (size_t)ctx->n_ctas * ctx->landing_halves * 8));
     ctx->bell_ev.resize((size_t)cfg.io_workers, nullptr);
     for (auto& ev : ctx->bell_ev) TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  }
+  if (cfg.transfer == GFS_XFER_PREAD_HYBRID) {
+    // a pool both the copy engine (large spans) and the CTAs (small spans, mapped) read
+    ctx->nbounce = (int)std::max<int64_t>(2, (48ll << 20) / (ctx->slot_bytes * cfg.io_workers));
+    if (ctx->nbounce > 8) ctx->nbounce = 8;
+    const int64_t nb = (int64_t)cfg.io_workers * ctx->nbounce;
+    TRY(cudaHostAlloc(&ctx->h_bounce, (size_t)(ctx->slot_bytes * nb), cudaHostAllocMapped | cudaHostAllocPortable));
+    TRY(cudaHostAlloc(&ctx->h_release, (size_t)nb * 4, cudaHostAllocMapped | cudaHostAllocPortable));
+    memset(ctx->h_release, 0, (size_t)nb * 4);
+    ctx->bounce_last.assign((size_t)nb, 0);
+    ctx->bounce_ce.assign((size_t)nb, 0);
+    ctx->bounce_ev.resize((size_t)nb, nullptr);
+    for (auto& ev : ctx->bounce_ev) TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   }
   if (cfg.transfer == GFS_XFER_DMA) {
     // ~48 MiB of bounce buffers in total (LLC-sized), at least 2 per worker

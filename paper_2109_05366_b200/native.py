@@ -19,7 +19,7 @@ POLICY = {"global-lru-dealloc": 0, "per-tb-lra": 1}
 READAHEAD = {"static": 0, "doubling": 1, "adaptive": 2}  # adaptive = ondemand law
 RA_CLAMP = {"segment": 0, "eof": 1}
 TRANSFER = {"zerocopy": 0, "dma": 1, "bounce": 2, "mapped_dma": 3, "mapped": 4,
-            "mapped_hybrid": 5}
+            "mapped_hybrid": 5, "pread_hybrid": 6}
 O_RDONLY, O_RDWR = 0, 2
 ABI_VERSION = 6  # include/gfs.h GFS_ABI_VERSION: the struct layouts below
 LOG_DELIVERIES, LOG_RPCS, LOG_VICTIMS, LOG_WINDOWS, LOG_TIMELINE = 0, 1, 2, 3, 4

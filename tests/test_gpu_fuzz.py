@@ -17,7 +17,7 @@ from paper_2109_05366_b200.workloads import build_workload
 pytestmark = pytest.mark.gpu
 
 N_CASES = 40
-TRANSFERS = ["zerocopy", "bounce", "dma", "mapped", "mapped_dma", "mapped_hybrid"]
+TRANSFERS = ["zerocopy", "bounce", "dma", "mapped", "mapped_dma", "mapped_hybrid", "pread_hybrid"]
 COUNTERS = ["greads", "user_bytes", "cache_hit_user_bytes", "pc_lookups", "pc_hits",
             "pc_hit_pending", "pc_misses", "pc_allocs", "pc_evictions", "pc_remaps", "pb_hits",
             "pb_misses", "pb_filled_bytes", "pb_consumed_bytes", "pb_discarded_bytes", "rpc_count",

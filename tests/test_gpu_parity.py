@@ -43,7 +43,7 @@ def oracle_checksum(cfg, seed):
 
 @pytest.mark.parametrize("name", gu.case_names())
 @pytest.mark.parametrize("transfer", ["zerocopy", "bounce", "dma", "mapped", "mapped_dma", "mapped_dma+ldg",
-                                      "mapped_hybrid"])
+                                      "mapped_hybrid", "pread_hybrid"])
 def test_golden_case_on_device(name, transfer, synth_dir):
     g = gu.load(name)
     transfer, _, k1 = transfer.partition("+")  # K1 copies by TMA (default) or vector loads
@@ -262,7 +262,7 @@ def test_lookahead_is_invisible(request_bytes, readahead, synth_dir):
     assert a.checksum == b.checksum and a.mismatched_words == b.mismatched_words == 0
 
 
-@pytest.mark.parametrize("transfer", ["mapped_dma", "dma", "mapped", "bounce", "zerocopy", "mapped_hybrid"])
+@pytest.mark.parametrize("transfer", ["mapped_dma", "dma", "mapped", "bounce", "zerocopy", "mapped_hybrid", "pread_hybrid"])
 @pytest.mark.parametrize("n_tb,ra_max,req", [(8, 256 * KiB, 64 * KiB), (48, 1 * MiB, 64 * KiB),
                                              (192, 512 * KiB, 16 * KiB)])
 def test_ondemand_readahead_vs_oracle(transfer, n_tb, ra_max, req, synth_dir):

@@ -20,7 +20,7 @@ from test_readahead_law import BOUNDED, _prefix
 
 pytestmark = pytest.mark.gpu
 
-TRANSFERS = ["mapped_dma", "mapped", "bounce", "zerocopy", "dma", "mapped_hybrid"]
+TRANSFERS = ["mapped_dma", "mapped", "bounce", "zerocopy", "dma", "mapped_hybrid", "pread_hybrid"]
 
 
 def run_device(cfg, wl, transfer):

@@ -20,7 +20,7 @@ pytestmark = pytest.mark.gpu
 
 KiB, MiB = 1 << 10, 1 << 20
 N_CASES = 72
-TRANSFERS = ["mapped_dma", "mapped", "bounce", "dma", "zerocopy", "mapped_hybrid"]
+TRANSFERS = ["mapped_dma", "mapped", "bounce", "dma", "zerocopy", "mapped_hybrid", "pread_hybrid"]
 FILE_BYTES = [512 * MiB + 12345, 320 * MiB]
 
 
