@@ -527,8 +527,11 @@ def reference_main(args, dist: Dist) -> None:
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as orc
     # rank 0 alone (the other ranks have already left): no barriers from here on; the CPU
-    # implementation reads one GPU's shard of the workload
-    size = fit_size(args.dir, int(args.size_gib * GiB), 1)
+    # implementation reads one GPU's shard of the workload (the b200 arm's shard plan: 16 GiB
+    # at N = 1, configs[4]'s 64 GiB / N with N GPUs)
+    world = max(args.gpus, dist.world)
+    total_gib, scaling, want = shard_plan(args.total_gib, args.size_gib, world)
+    size = fit_size(args.dir, want, 1)
     path = os.path.join(args.dir, f"gfs_synth_c0_{size}.bin")
     ok = path + ".ok"
     if not (os.path.exists(path) and os.path.getsize(path) == size and os.path.exists(ok)
@@ -585,10 +588,14 @@ def reference_main(args, dist: Dist) -> None:
            f"[{per}g, {per}(g+1)) of the {n_tb} with 1/{groups} of the cache and of the residency")
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(sum(secs) / len(secs) * 1e3, 3),
-           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+           "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "u8",
            "data": "synthetic",
-           "config": {"workload": f"sequential strided gread, {size / GiB:g} GiB/GPU, cache < file "
-                                  f"(configs[1]), whole workload per step",
+           "config": {"workload": f"sequential strided gread, {size / GiB:g} GiB/GPU, "
+                                  f"{'cache < file' if REF_PARAMS['cache_bytes'] < size else 'cache >= file'} "
+                                  + ("(configs[1])" if total_gib is None else
+                                     f"(configs[4]: {total_gib:g} GiB over {world} GPUs; the CPU "
+                                     f"reference reads one GPU's shard, on rank 0)")
+                                  + ", whole shard per step",
                       "sample_bytes": nbytes, "programs": prog_src, "params": REF_PARAMS,
                       "decomposition": dec, "same_config": "yes, split into independent instances as stated"},
            "cpu_baseline": {"value": v, "unit": "GB/s", "cores": threads, "kind": "port",

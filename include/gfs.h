@@ -123,7 +123,8 @@ typedef struct gfs_program {
   X(rpc_requested_bytes) X(slot_collisions) X(preads) X(pread_bytes) X(storage_bytes)       \
   X(pcie_bytes) X(pcie_transfers) X(victims) X(kernel_ns) X(wall_ns) X(ctas) X(word_mismatches) \
   X(wait_ns) X(meta_ns) X(copy_ns) X(lookup_ns) X(alloc_ns) X(install_ns) X(host_pread_ns) \
-  X(host_idle_ns) X(host_xfer_ns) X(host_requests) X(io_workers)
+  X(host_idle_ns) X(host_xfer_ns) X(host_requests) X(io_workers) X(pull_jobs) X(helper_chunks) \
+  X(pull_wait_ns)
 
 enum {
 #define GFS_X(name) GFS_STAT_##name,

@@ -743,12 +743,15 @@ __device__ void pj_post(const DevCtx& c, Smem& s, int64_t fid, int64_t off, int6
   atomicExch(&J.ctl, (seq << 48) | (nch << 32));
   atomicOr(&c.pjob_bits[j >> 5], 1u << (j & 31));
   s.pjob_active[h] = 1;
+  ST(pull_jobs)++;
 }
 
 // Claim a chunk of job j (one thread): its index, or -1 when every chunk is taken.  The
 // chunk's source / destination / bytes go to s.hj_*.
 __device__ int pj_claim(const DevCtx& c, Smem& s, int j) {
   PullJob& J = c.pjobs[j];
+  const unsigned long long cur = ld_volatile_u64(&J.ctl);  // a plain look first: no atomic on a drained job
+  if ((uint32_t)cur >= ((uint32_t)(cur >> 32) & 0xFFFFu)) return -1;
   const unsigned long long old = atomicAdd(&J.ctl, 1ull);
   const uint32_t k = (uint32_t)old, n = (uint32_t)(old >> 32) & 0xFFFFu;
   if (k >= n) return -1;
@@ -1418,7 +1421,9 @@ __device__ void pull_span(const DevCtx& c, Smem& s) {
       pj_copy_done<BS>(c, s, j);  // ends with a barrier: s.hj_* may be rewritten after it
     }
     if (threadIdx.x == 0) {
+      const uint64_t tw = globaltimer();
       if (!pj_wait_done(c, j)) set_error(c, ERR_TIMEOUT, 25, 0);
+      ST(pull_wait_ns) += (long long)(globaltimer() - tw);
       s.pjob_active[h] = 0;
       s.pull_job = -1;
       s.dbg_land_off[h] = -2;  // (pulled by a job)
@@ -2489,6 +2494,7 @@ __device__ void pull_helper(const DevCtx& c, Smem& s) {
   if (!c.helpers) return;
   const int tid = threadIdx.x, lane = tid & 31;
   const int nw = (c.n_ctas * 2 + 31) / 32;
+  unsigned backoff = 500;
   for (;;) {
     if (tid < 32) {
       bool stop = false;
@@ -2497,7 +2503,7 @@ __device__ void pull_helper(const DevCtx& c, Smem& s) {
       stop = __shfl_sync(0xffffffffu, stop, 0);
       for (int w0 = 0; !stop && w0 < nw && k < 0; w0 += 32) {
         const int w = (w0 + lane + (int)blockIdx.x) % nw;  // CTAs start at different words
-        const uint32_t bits = w0 + lane < nw ? ld_acquire_gpu(&c.pjob_bits[w]) : 0u;
+        const uint32_t bits = w0 + lane < nw ? *(volatile const uint32_t*)&c.pjob_bits[w] : 0u;
         unsigned cand = __ballot_sync(0xffffffffu, bits != 0u);
         while (cand && k < 0) {
           const int src = __ffs(cand) - 1;
@@ -2522,11 +2528,14 @@ __device__ void pull_helper(const DevCtx& c, Smem& s) {
     const int k = s.hj_k, j = (int)s.k;
     __syncthreads();
     if (stop) break;
-    if (k < 0) {
-      __nanosleep(1000);
+    if (k < 0) {  // nothing posted: back off (idle CTAs must not crowd the L2 / atomics units)
+      __nanosleep(backoff);
+      backoff = backoff < 16000 ? 2 * backoff : 16000;
       continue;
     }
+    backoff = 500;
     pj_copy_done<BS>(c, s, j);
+    if (tid == 0) ST(helper_chunks)++;
   }
 }
 
