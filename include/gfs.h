@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define GFS_ABI_VERSION 6  /* 6: pull_helpers; 5: rpc_slots; 4: gfs_run_kernel (user kernels over gfs_device.cuh); 3: ondemand law */
+#define GFS_ABI_VERSION 8  /* 8: k1_direct; 5: rpc_slots; 4: gfs_run_kernel (user kernels over gfs_device.cuh); 3: ondemand law */
 
 enum { GFS_OK = 0, GFS_EINVAL = -1, GFS_ECUDA = -2, GFS_EIO = -3, GFS_ENOMEM = -4,
        GFS_ETIMEDOUT = -5, GFS_EDEVICE = -6, GFS_ESTATE = -7 };
@@ -97,8 +97,9 @@ typedef struct gfs_config {
   int32_t ra_clamp;        /* io.ra_clamp: GFS_RA_CLAMP_* (ondemand) */
   int32_t rpc_slots;       /* rpc.n_slots (0 = 128): the reference's slot partition tb % n_slots,
                               for the slot_collisions counter (rpc.py:25-28, 82-89) */
-  int32_t pull_helpers;    /* gpu.pull_helpers: CTAs without a TB help pull other CTAs' spans
-                              from pinned host memory (mapped / small mapped_hybrid spans) */
+  int32_t k1_direct;       /* gpu.k1_direct: spans of the mapped transfers that the CTA would pull
+                              are read by the span copy (K1) straight from the pinned file mapping
+                              into frames + user buffer (one pass, no HBM landing copy) */
 } gfs_config;
 
 /* One gread program set (workloads.py:24-31 programs, flattened).
@@ -123,8 +124,7 @@ typedef struct gfs_program {
   X(rpc_requested_bytes) X(slot_collisions) X(preads) X(pread_bytes) X(storage_bytes)       \
   X(pcie_bytes) X(pcie_transfers) X(victims) X(kernel_ns) X(wall_ns) X(ctas) X(word_mismatches) \
   X(wait_ns) X(meta_ns) X(copy_ns) X(lookup_ns) X(alloc_ns) X(install_ns) X(host_pread_ns) \
-  X(host_idle_ns) X(host_xfer_ns) X(host_requests) X(io_workers) X(pull_jobs) X(helper_chunks) \
-  X(pull_wait_ns)
+  X(host_idle_ns) X(host_xfer_ns) X(host_requests) X(io_workers)
 
 enum {
 #define GFS_X(name) GFS_STAT_##name,

@@ -109,7 +109,6 @@ __device__ void run_threadblocks(const DevCtx& c, Body&& body) {
     if (__syncthreads_or(has_error(c))) break;  // one decision for the whole CTA
     tb_end<BS>(c, s);
   }
-  pull_helper<BS>(c, s);  // no TB left: help the other CTAs pull their spans
   cta_end(c, s, t.bad_words);
 }
 

@@ -205,12 +205,7 @@ struct Smem {
   } hp[2];
   uint32_t hp_age;
   uint32_t rpc_out;  // this TB's requests outstanding (submitted, not yet waited for)
-  int pjob_active[2];  // landing half h has a posted pull job (pull helpers)
-  int pull_job;        // half whose pull job pull_span finishes, -1 = none
-  int hj_stop, hj_k;   // pull-job chunk broadcast (owner finish / helper loop)
-  const uint8_t* hj_src;
-  uint8_t* hj_dst;
-  int64_t hj_n;
+  int direct[2];       // half h's span is read straight from the pinned file mapping (K1 direct)
   int64_t pull_off;            // file offset of the span waiting to be pulled
   int64_t dbg_land_off[2], dbg_land_n[2];  // what each landing half last received (diagnostics)
   uint32_t pb_absent[MAX_PB_ENTRIES / 32];  // private-buffer entries consumed / dropped
@@ -705,99 +700,6 @@ __device__ __forceinline__ void account_transfer(const DevCtx& c, Smem& s, int64
   }
 }
 
-// ------------------------------------------------------------ pull helpers
-//
-// Spans that a CTA pulls itself from pinned host memory (mapped transfers; small
-// mapped_hybrid spans) are posted at submit time as chunked jobs.  CTAs without a TB (the
-// dispatcher ran dry: few TBs, or the tail of a pass) claim chunks of any posted job and
-// copy them into its landing half; the owner claims and copies what is left when it gets
-// to the span, then waits for the chunks in flight.  Each chunk is copied exactly once:
-// claims come from one atomic counter that carries the job's sequence number and chunk
-// count, and a job slot is reposted only after all its chunks are done.
-
-template <int BS, int SRC>
-__device__ void copy_bytes(uint8_t* dst, const uint8_t* src, int64_t n);
-__device__ __forceinline__ const uint8_t* half_base(const DevCtx& c, int h);
-
-__device__ __forceinline__ int pj_id(int h) { return (int)blockIdx.x * 2 + h; }
-
-// Whether a span of n bytes that the CTA would pull goes through a job.
-__device__ __forceinline__ bool pj_wanted(const DevCtx& c, int64_t n) {
-  if (!c.helpers || n < 2 * c.pull_chunk) return false;
-  if (c.transfer == GFS_XFER_MAPPED_ZC) return true;
-  if (c.transfer == GFS_XFER_MAPPED_HYBRID) return n < c.ce_min;  // the daemon's rule (gfs_host.cpp)
-  return false;
-}
-
-// Post the pull of [off, off + n) of fid into landing half h (thread 0).
-__device__ void pj_post(const DevCtx& c, Smem& s, int64_t fid, int64_t off, int64_t n, int h) {
-  const int j = pj_id(h);
-  PullJob& J = c.pjobs[j];
-  const unsigned long long nch = (unsigned long long)((n + c.pull_chunk - 1) / c.pull_chunk);
-  const unsigned long long seq = ((atomicAdd(&J.ctl, 0ull) >> 48) + 1) & 0xFFFFull;
-  J.src = c.files[fid].map + off;
-  J.dst = (uint8_t*)half_base(c, h);
-  J.bytes = n;
-  J.done = 0;
-  __threadfence();  // the descriptor before the claims it enables
-  atomicExch(&J.ctl, (seq << 48) | (nch << 32));
-  atomicOr(&c.pjob_bits[j >> 5], 1u << (j & 31));
-  s.pjob_active[h] = 1;
-  ST(pull_jobs)++;
-}
-
-// Claim a chunk of job j (one thread): its index, or -1 when every chunk is taken.  The
-// chunk's source / destination / bytes go to s.hj_*.
-__device__ int pj_claim(const DevCtx& c, Smem& s, int j) {
-  PullJob& J = c.pjobs[j];
-  const unsigned long long cur = ld_volatile_u64(&J.ctl);  // a plain look first: no atomic on a drained job
-  if ((uint32_t)cur >= ((uint32_t)(cur >> 32) & 0xFFFFu)) return -1;
-  const unsigned long long old = atomicAdd(&J.ctl, 1ull);
-  const uint32_t k = (uint32_t)old, n = (uint32_t)(old >> 32) & 0xFFFFu;
-  if (k >= n) return -1;
-  if (k == n - 1) atomicAnd(&c.pjob_bits[j >> 5], ~(1u << (j & 31)));  // nothing left to claim
-  __threadfence();  // descriptor reads after the claim (posted before the ctl that enabled it)
-  const int64_t o = (int64_t)k * c.pull_chunk;
-  const int64_t bytes = (int64_t)__ldcg((const long long*)&J.bytes);
-  s.hj_src = (const uint8_t*)__ldcg((const unsigned long long*)&J.src) + o;
-  s.hj_dst = (uint8_t*)__ldcg((const unsigned long long*)&J.dst) + o;
-  s.hj_n = bytes - o < c.pull_chunk ? bytes - o : c.pull_chunk;
-  return (int)k;
-}
-
-// Copy the claimed chunk in s.hj_* (all threads) and count it done.
-template <int BS>
-__device__ void pj_copy_done(const DevCtx& c, Smem& s, int j) {
-  copy_bytes<BS, SRC_SYS>(s.hj_dst, s.hj_src, s.hj_n);
-  asm volatile("fence.proxy.async.global;" ::: "memory");  // read next by TMA (async proxy)
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(&c.pjobs[j].done, 1u);
-  }
-}
-
-// Wait until every chunk of job j is done (thread 0).  False on abort.
-__device__ bool pj_wait_done(const DevCtx& c, int j) {
-  PullJob& J = c.pjobs[j];
-  const uint32_t n = (uint32_t)(atomicAdd(&J.ctl, 0ull) >> 32) & 0xFFFFu;
-  const uint64_t t0 = globaltimer();
-  while (ld_acquire_gpu(&J.done) < n) {
-    if (!keep_waiting(c, t0, 25)) return false;
-    __nanosleep(200);
-  }
-  return true;
-}
-
-// A posted job whose bytes the CTA will not use (a dropped window, thread 0): claim what is
-// left without copying, wait for the helpers' chunks in flight.
-__device__ bool pj_cancel(const DevCtx& c, Smem& s, int h) {
-  const int j = pj_id(h);
-  while (pj_claim(c, s, j) >= 0) atomicAdd(&c.pjobs[j].done, 1u);
-  s.pjob_active[h] = 0;
-  return pj_wait_done(c, j);
-}
-
 // Submit one request for this CTA's slot into landing half `half` (thread 0): rpc.py:82-102.
 // Returns false on abort; *seq_out / *pos_out identify it for rpc_wait.
 __device__ bool rpc_submit(const DevCtx& c, Smem& s, int64_t fid, int64_t off, int64_t size, int half,
@@ -840,10 +742,6 @@ __device__ bool rpc_submit(const DevCtx& c, Smem& s, int64_t fid, int64_t off, i
   // readahead runs inside the host's pread, not through the slot)
   if (atomicAdd(&c.slot_busy[s.tb % c.ref_slots], 1u) > s.rpc_out) ST(slot_collisions)++;
   s.rpc_out++;
-  // a span the CTA will pull from the pinned mapping: post it so idle CTAs start on it now
-  const int64_t fsz = c.files[fid].size;
-  const int64_t nexp = off >= fsz ? 0 : (size < fsz - off ? size : fsz - off);  // the daemon's answer
-  if (pj_wanted(c, nexp)) pj_post(c, s, fid, off, nexp, half);
   return true;
 }
 
@@ -855,6 +753,7 @@ __device__ int64_t rpc_wait(const DevCtx& c, Smem& s, int64_t fid, int64_t off, 
   const uint64_t t0 = globaltimer();
   const uint64_t tw = globaltimer();
   int64_t n;
+  s.direct[half] = 0;  // what lands in this half now: the answer says
   if (c.transfer == GFS_XFER_DMA || c.transfer == GFS_XFER_MAPPED) {
     const unsigned long long* bell = &c.doorbell[(int64_t)slot * c.landing_halves + half];
     for (;;) {
@@ -890,8 +789,8 @@ __device__ int64_t rpc_wait(const DevCtx& c, Smem& s, int64_t fid, int64_t off, 
             s.pull_seq = seq;
             s.pull_off = off;
             s.pull_half = half;
-          } else if (s.pjob_active[half]) {
-            s.pull_job = half;
+          } else if (c.k1_direct) {
+            s.direct[half] = 1;  // K1 reads it from the mapping: no pull, no landing copy
           } else {
             s.pull_n = n;
             s.pull_buf = -1;
@@ -899,9 +798,6 @@ __device__ int64_t rpc_wait(const DevCtx& c, Smem& s, int64_t fid, int64_t off, 
             s.pull_off = off;
             s.pull_half = half;
           }
-        } else if (s.pjob_active[half] && n > 0) {  // copied by the engine after all: a rule mismatch
-          set_error(c, ERR_IO, (int)fid, (unsigned long long)off);
-          return -1;
         }
         break;
       }
@@ -924,8 +820,8 @@ __device__ int64_t rpc_wait(const DevCtx& c, Smem& s, int64_t fid, int64_t off, 
           s.pull_off = off;
           s.pull_half = half;
           s.pull_seq = seq;
-        } else if (c.transfer == GFS_XFER_MAPPED_ZC && n > 0 && s.pjob_active[half]) {
-          s.pull_job = half;  // posted: the owner finishes it in pull_span
+        } else if (c.transfer == GFS_XFER_MAPPED_ZC && n > 0 && c.k1_direct) {
+          s.direct[half] = 1;  // K1 reads it from the mapping: no pull, no landing copy
         } else if (c.transfer == GFS_XFER_MAPPED_ZC && n > 0) {  // straight from the page cache
           s.pull_n = n;
           s.pull_buf = -1;
@@ -1210,11 +1106,6 @@ __device__ int64_t od_wait(const DevCtx& c, Smem& s, int h) {
 __device__ int od_drain(const DevCtx& c, Smem& s, int h) {
   const int64_t n = od_wait(c, s, h);
   if (n < 0 || !wait_landed(c, s, h, n)) return -1;
-  if (s.pull_job >= 0) {  // never pulled: stop the helpers on it
-    const int pj = s.pull_job;
-    s.pull_job = -1;
-    if (!pj_cancel(c, s, pj)) return -1;
-  }
   if (s.pull_n > 0) {  // never pulled: hand a bounce buffer straight back
     if (s.pull_buf >= 0) {
       __threadfence_system();
@@ -1411,26 +1302,6 @@ __device__ void copy_bytes(uint8_t* dst, const uint8_t* src, int64_t n) {
 // CTA's HBM landing slot in one bulk pass, then hand the buffer back to its worker.
 template <int BS>
 __device__ void pull_span(const DevCtx& c, Smem& s) {
-  if (s.pull_job >= 0) {  // a posted job: claim and copy what the helpers left, wait for theirs
-    const int h = s.pull_job, j = pj_id(h);
-    for (;;) {
-      if (threadIdx.x == 0) s.hj_k = pj_claim(c, s, j);
-      __syncthreads();
-      const int k = s.hj_k;
-      if (k < 0) break;
-      pj_copy_done<BS>(c, s, j);  // ends with a barrier: s.hj_* may be rewritten after it
-    }
-    if (threadIdx.x == 0) {
-      const uint64_t tw = globaltimer();
-      if (!pj_wait_done(c, j)) set_error(c, ERR_TIMEOUT, 25, 0);
-      ST(pull_wait_ns) += (long long)(globaltimer() - tw);
-      s.pjob_active[h] = 0;
-      s.pull_job = -1;
-      s.dbg_land_off[h] = -2;  // (pulled by a job)
-    }
-    __syncthreads();
-    return;
-  }
   if (s.pull_n <= 0) return;
   copy_bytes<BS, SRC_SYS>((uint8_t*)half_base(c, s.pull_half), s.pull_src, s.pull_n);
   if (threadIdx.x == 0) {
@@ -1817,13 +1688,16 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
   }
   __syncthreads();
   if (s.b.status != 0) return -1;
-  span_buf = half_base(c, s.b.src_half);  // an RPC may have switched landing halves
+  const bool direct = s.direct[s.b.src_half];
+  // an RPC may have switched landing halves; a direct span is read at its file offsets
+  span_buf = direct ? F.map : half_base(c, s.b.src_half);
   if (w0) {  // private-buffer pages' bytes and span offsets; bind frames to their pages
     if (lane >= s.b.j0 && lane < kk) {
       const int64_t i = p0 + lane - s.pb_base;
       s.b.nb[lane] = (int32_t)(i == s.pb_count ? s.pb_last_nb : pg);
       s.b.src_off[lane] = i * pg - s.pb_off_adj;
     }
+    if (direct && lane < kk) s.b.src_off[lane] = (p0 + lane) * pg;
     if (lane < kk) c.fkey[s.b.frame[lane]] = page_key(fid, p0 + lane);
     __syncwarp();
     // which pages need the byte-wise tail copy or a partial delivery, and the batch's bytes
@@ -1869,6 +1743,7 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
   const bool contiguous = s.b.src_off[kk - 1] == s.b.src_off[0] + (int64_t)(kk - 1) * pg;
   bool full_pages = true;
   for (int j = 0; j < kk; j++) full_pages &= s.b.nb[j] == pg;
+  const bool sys_src = c.transfer == GFS_XFER_ZEROCOPY || direct;  // pinned host memory
   const bool use_tma = c.tma && c.transfer != GFS_XFER_ZEROCOPY && contiguous && full_pages &&
                        (((uintptr_t)src4) & 15) == 0;
   if (use_tma) {
@@ -1960,7 +1835,7 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
         const int j = (int)(vsh >= 0 ? v >> vsh : v / vpp);
         const int64_t w = v - (int64_t)j * vpp;
         const uint4* sp = contiguous ? src4 + v : (const uint4*)(span_buf + s.b.src_off[j]) + w;
-        q[u] = (w << 4) < s.b.nb[j] ? (c.transfer != GFS_XFER_ZEROCOPY ? ld16<SRC_HBM>(sp) : ld16<SRC_SYS>(sp))
+        q[u] = (w << 4) < s.b.nb[j] ? (!sys_src ? ld16<SRC_HBM>(sp) : ld16<SRC_SYS>(sp))
                                     : make_uint4(0, 0, 0, 0);
       }
     }
@@ -1994,7 +1869,7 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
     const uint8_t* sp = span_buf + s.b.src_off[j];
     uint8_t* fp = c.frames + (int64_t)s.b.frame[j] * pg;
     for (int64_t i = (nbj & ~(int64_t)15) + tid; i < nbj; i += BS) {
-      const uint8_t b = c.transfer != GFS_XFER_ZEROCOPY ? ld1<SRC_HBM>(sp + i) : ld1<SRC_SYS>(sp + i);
+      const uint8_t b = !sys_src ? ld1<SRC_HBM>(sp + i) : ld1<SRC_SYS>(sp + i);
       fp[i] = b;
       if (chk) {
         const int64_t fo = (p0 + j) * pg + i;
@@ -2180,7 +2055,8 @@ __device__ int64_t gread(const DevCtx& c, Smem& s, int64_t fid, int64_t offset, 
     int64_t n = s.n;
     if (n < 0) return -1;
     if (dst) {
-      if (c.transfer != GFS_XFER_ZEROCOPY) copy_bytes<BS, SRC_HBM>(dst, span_buf, n);
+      if (s.direct[0]) copy_bytes<BS, SRC_SYS>(dst, F.map + offset, n);  // straight from the mapping
+      else if (c.transfer != GFS_XFER_ZEROCOPY) copy_bytes<BS, SRC_HBM>(dst, span_buf, n);
       else copy_bytes<BS, SRC_SYS>(dst, span_buf, n);
     }
     __syncthreads();
@@ -2345,8 +2221,9 @@ __device__ int64_t gread(const DevCtx& c, Smem& s, int64_t fid, int64_t offset, 
       want = (g_end < pend ? g_end : pend) - g_pos;
     }
     const bool whole = d && in_page == 0 && want == nb && (((uintptr_t)d & 15) == 0);
-    const uint8_t* src = half_base(c, s.src_half) + s.src_off;
-    int bad = c.transfer != GFS_XFER_ZEROCOPY
+    const bool direct = s.direct[s.src_half];  // straight from the pinned mapping (K1 direct)
+    const uint8_t* src = direct ? F.map + page * pg : half_base(c, s.src_half) + s.src_off;
+    int bad = c.transfer != GFS_XFER_ZEROCOPY && !direct
                   ? copy_page_in<BS, SRC_HBM>(fmem, whole ? d : nullptr, src, nb, page * pg,
                                               c.verify ? F.content_id : -1)
                   : copy_page_in<BS, SRC_SYS>(fmem, whole ? d : nullptr, src, nb, page * pg,
@@ -2393,8 +2270,7 @@ __device__ void cta_begin(const DevCtx& c, Smem& s) {
     s.hp[0].pending = s.hp[1].pending = 0;
     s.hp_age = 0;
     s.dbg_land_off[0] = s.dbg_land_off[1] = -1;
-    s.pjob_active[0] = s.pjob_active[1] = 0;
-    s.pull_job = -1;
+    s.direct[0] = s.direct[1] = 0;
     s.dbg_land_n[0] = s.dbg_land_n[1] = 0;
     s.st_seq[0] = s.st_seq[1] = 0;
     s.st_n[0] = s.st_n[1] = 0;
@@ -2474,7 +2350,6 @@ __device__ void tb_end(const DevCtx& c, Smem& s) {
     s.pb_count = 0;
     if (c.policy == GFS_POLICY_PER_TB_LRA && s.own_len > 0)
       ret_pos = atomicAdd(rp_tail(c, (int)(blockIdx.x % (unsigned)c.ret_npools)), (unsigned long long)s.own_len);
-    atomicAdd(&c.g->tbs_done, 1ull);
   }
   __syncthreads();
   if (c.policy == GFS_POLICY_PER_TB_LRA && s.own_len > 0) {
@@ -2485,58 +2360,6 @@ __device__ void tb_end(const DevCtx& c, Smem& s) {
     }
   }
   __syncthreads();
-}
-
-// A CTA the dispatcher has no TB for: copy chunks of other CTAs' posted pull jobs until every
-// TB is done (all threads).
-template <int BS>
-__device__ void pull_helper(const DevCtx& c, Smem& s) {
-  if (!c.helpers) return;
-  const int tid = threadIdx.x, lane = tid & 31;
-  const int nw = (c.n_ctas * 2 + 31) / 32;
-  unsigned backoff = 500;
-  for (;;) {
-    if (tid < 32) {
-      bool stop = false;
-      int j = -1, k = -1;
-      if (lane == 0) stop = has_error(c) || ld_volatile_u64(&c.g->tbs_done) >= (unsigned long long)c.n_tb;
-      stop = __shfl_sync(0xffffffffu, stop, 0);
-      for (int w0 = 0; !stop && w0 < nw && k < 0; w0 += 32) {
-        const int w = (w0 + lane + (int)blockIdx.x) % nw;  // CTAs start at different words
-        const uint32_t bits = w0 + lane < nw ? *(volatile const uint32_t*)&c.pjob_bits[w] : 0u;
-        unsigned cand = __ballot_sync(0xffffffffu, bits != 0u);
-        while (cand && k < 0) {
-          const int src = __ffs(cand) - 1;
-          cand &= cand - 1;
-          if (lane == src) {
-            const int b = __ffs(bits) - 1;
-            j = w * 32 + b;
-            k = pj_claim(c, s, j);
-          }
-          k = __shfl_sync(0xffffffffu, k, src);
-          j = __shfl_sync(0xffffffffu, j, src);
-        }
-      }
-      if (lane == 0) {
-        s.hj_stop = stop;
-        s.hj_k = k;
-        s.k = j;
-      }
-    }
-    __syncthreads();
-    const bool stop = s.hj_stop;
-    const int k = s.hj_k, j = (int)s.k;
-    __syncthreads();
-    if (stop) break;
-    if (k < 0) {  // nothing posted: back off (idle CTAs must not crowd the L2 / atomics units)
-      __nanosleep(backoff);
-      backoff = backoff < 16000 ? 2 * backoff : 16000;
-      continue;
-    }
-    backoff = 500;
-    pj_copy_done<BS>(c, s, j);
-    if (tid == 0) ST(helper_chunks)++;
-  }
 }
 
 // CTA end: word mismatches seen by the K1 checks, counters out.

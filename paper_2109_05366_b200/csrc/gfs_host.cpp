@@ -225,8 +225,6 @@ struct gfs_ctx {
   unsigned long long* d_scratch = nullptr;
   uint32_t* d_owner = nullptr;  // check_unique_mapping scratch (nframes), allocated on first use
   uint32_t* d_slot_busy = nullptr;  // [rpc_slots]: the reference slot partition's occupancy
-  PullJob* d_pjobs = nullptr;       // [n_ctas * 2] pull jobs (pull helpers)
-  uint32_t* d_pjob_bits = nullptr;  // [(n_ctas * 2 + 31) / 32]
   unsigned long long* h_served = nullptr;  // mapped: requests completed by the daemon
   DevBuf<int64_t> d_segs, d_prog_off, d_dst_off, d_seg_dst;
   DevBuf<int32_t> d_order;
@@ -569,7 +567,7 @@ static void free_all(gfs_ctx* ctx) {
     if (ev) cudaEventDestroy(ev);
   void* dev[] = {ctx->d_frames, ctx->d_fkey, ctx->d_fstate, ctx->d_own_q, ctx->d_retired, ctx->d_rpool, ctx->d_landed,
                  ctx->d_gfifo, ctx->d_recycled, ctx->d_g, ctx->d_landing, ctx->d_doorbell,
-                 ctx->d_done_pos, ctx->d_stats, ctx->d_scratch, ctx->d_owner, ctx->d_slot_busy, ctx->d_pjobs, ctx->d_pjob_bits};
+                 ctx->d_done_pos, ctx->d_stats, ctx->d_scratch, ctx->d_owner, ctx->d_slot_busy};
   for (void* p : dev)
     if (p) cudaFree(p);
   ctx->d_segs.release();
@@ -761,8 +759,7 @@ extern "C" int gfs_create(const gfs_config* cfg_in, gfs_ctx** out) {
   TRY(cudaMalloc(&ctx->d_stats, (size_t)ctx->n_ctas * GFS_NSTATS * 8));
   TRY(cudaMalloc(&ctx->d_scratch, 64));
   TRY(cudaMalloc(&ctx->d_slot_busy, (size_t)cfg.rpc_slots * 4));
-  TRY(cudaMalloc(&ctx->d_pjobs, (size_t)ctx->n_ctas * 2 * sizeof(PullJob)));
-  TRY(cudaMalloc(&ctx->d_pjob_bits, (size_t)(ctx->n_ctas * 2 + 31) / 32 * 4));
+
   TRY(cudaHostAlloc(&ctx->h_ring, (size_t)ctx->ring_size * sizeof(RpcReq),
                     cudaHostAllocMapped | cudaHostAllocPortable));
   TRY(cudaHostAlloc(&ctx->h_consumed, (size_t)ctx->ring_size * 4, cudaHostAllocMapped | cudaHostAllocPortable));
@@ -1135,8 +1132,7 @@ static int run_prepared(gfs_ctx* ctx, const gfs_program* prog, void* dst, const 
   CUDA_TRY(cudaMemsetAsync(ctx->d_stats, 0, (size_t)ctx->n_ctas * GFS_NSTATS * 8, ctx->stream));
   CUDA_TRY(cudaMemsetAsync(ctx->d_done_pos, 0, (size_t)ctx->ring_size * 8, ctx->stream));
   CUDA_TRY(cudaMemsetAsync(ctx->d_slot_busy, 0, (size_t)cfg.rpc_slots * 4, ctx->stream));
-  CUDA_TRY(cudaMemsetAsync(ctx->d_pjobs, 0, (size_t)ctx->n_ctas * 2 * sizeof(PullJob), ctx->stream));
-  CUDA_TRY(cudaMemsetAsync(ctx->d_pjob_bits, 0, (size_t)(ctx->n_ctas * 2 + 31) / 32 * 4, ctx->stream));
+
 
   DevCtx c{};
   c.page_size = cfg.page_size;
@@ -1199,10 +1195,7 @@ static int run_prepared(gfs_ctx* ctx, const gfs_program* prog, void* dst, const 
   c.done_pos = ctx->d_done_pos;
   c.slot_busy = ctx->d_slot_busy;
   c.ref_slots = cfg.rpc_slots;
-  c.helpers = cfg.pull_helpers && !cfg.raw_mode;
-  c.pjobs = ctx->d_pjobs;
-  c.pjob_bits = ctx->d_pjob_bits;
-  c.pull_chunk = 32 << 10;
+  c.k1_direct = cfg.k1_direct && (cfg.transfer == GFS_XFER_MAPPED_ZC || cfg.transfer == GFS_XFER_MAPPED_HYBRID);
   c.ce_min = ctx->ce_min;
   c.stats = ctx->d_stats;
   if (cons) c.cons = *cons;

@@ -559,7 +559,6 @@ __global__ void __launch_bounds__(BS, 4) gread_driver(DevCtx c) {
     if (tb < 0) break;
     if (!run_tb<BS>(c, s, cons_smem, tb, bad_words, acc)) break;
   }
-  pull_helper<BS>(c, s);  // no TB left for this CTA: help the others pull their spans
   consume_flush<BS>(c, cons_smem, acc);
   cta_end(c, s, bad_words);
 }

@@ -47,18 +47,6 @@ struct DevFile {
   const uint8_t* map; // mapped transfers: device pointer of the pinned file mapping
 };
 
-// A span being pulled from pinned host memory into a landing half by several CTAs at once
-// (the owner and idle "pull helper" CTAs), in chunks claimed from ctl.  One per landing
-// half per resident CTA (device memory, zeroed per run).
-struct alignas(64) PullJob {
-  unsigned long long ctl;  // seq << 48 | nchunks << 32 | next chunk to claim
-  const uint8_t* src;      // pinned host (mapped) source
-  uint8_t* dst;            // landing half
-  int64_t bytes;
-  uint32_t done;           // chunks copied
-  uint32_t pad[7];
-};
-
 // Global run state in device memory (zeroed per run).
 struct DevGlobals {
   unsigned long long next_tb;      // dispatcher ticket
@@ -77,7 +65,6 @@ struct DevGlobals {
   int error_info;
   unsigned long long error_arg;
   unsigned long long done_ctas;
-  unsigned long long tbs_done;     // TBs finished (pull helpers stop when all are)
   // first K1 word mismatch seen (diagnostics, GFS_DEBUG_MISMATCH): set, tb, fid, file
   // offset of the word, the word read, landing half, span offset, batch pages | cta << 32,
   // then the landing half's last pull (file offset, bytes), pb_base, pb_off_adj, pb_count,
@@ -155,12 +142,9 @@ struct DevCtx {
   // the reference's RPC slot partition (rpc.n_slots): requests outstanding per slot tb % n
   uint32_t* slot_busy;
   int32_t ref_slots;
-  // pull helpers (gpu.pull_helpers): CTAs without a TB copy chunks of other CTAs' spans
-  int32_t helpers;
-  PullJob* pjobs;            // [n_ctas * 2]
-  uint32_t* pjob_bits;       // [(n_ctas * 2 + 31) / 32]: job has unclaimed chunks
-  int64_t pull_chunk;        // bytes per chunk
-  int64_t ce_min;            // mapped_hybrid: spans of at least this size go by copy engine
+  int32_t k1_direct;         // pulled spans (mapped, small mapped_hybrid) are read by K1 straight
+                             // from the pinned file mapping: no landing copy
+  int64_t ce_min;            // mapped_hybrid / pread_hybrid: spans of at least this size go by copy engine
   // fused consumer (gfs_run_consume)
   gfs_consumer cons;
   // counters (device): [n_ctas][GFS_NSTATS]

@@ -65,7 +65,7 @@ def native_config(cfg: ExperimentConfig, max_request_bytes: int = 0) -> native.G
     c.lookahead = int(bool(cfg["gpu.lookahead"]))
     c.ra_clamp = native.RA_CLAMP[cfg["io.ra_clamp"]]
     c.rpc_slots = cfg["rpc.n_slots"]
-    c.pull_helpers = int(bool(cfg["gpu.pull_helpers"]))
+    c.k1_direct = int(bool(cfg["gpu.k1_direct"]))
     return c
 
 

@@ -53,9 +53,7 @@ def main():
                    "transfer": fs.transfer, "ctas": st["ctas"], "rpc_count": st["rpc_count"],
                    "per_cta_ms": {k: round(st[k] / max(1, min(n_tb, st["ctas"])) / 1e6, 2)
                                   for k in ("wait_ns", "meta_ns", "copy_ns", "install_ns")},
-                   "kernel_ms": round(st["kernel_ns"] / 1e6, 2),
-                   "pull_jobs": st.get("pull_jobs"), "helper_chunks": st.get("helper_chunks"),
-                   "pull_wait_ms_per_cta": round(st.get("pull_wait_ns", 0) / max(1, min(n_tb, st["ctas"])) / 1e6, 3)}
+                   "kernel_ms": round(st["kernel_ns"] / 1e6, 2)}
             if a.timeline and r.timeline is not None:
                 d = timeline.decode(r.timeline)
                 for kind, name in ((0, "rpc"), (1, "gread")):
