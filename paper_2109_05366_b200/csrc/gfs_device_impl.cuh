@@ -159,6 +159,10 @@ struct Smem {
   // batched page walk (gread_batch): one entry per page of the batch
   struct {
     int n_empty, k, status, nvict, nret, ret_lane0, own_lane0, j0, ret_pool, src_half;
+    int early, fb_h, fb_od;         // page 0's RPC submitted before the frame work (fetch_begin)
+    int64_t fb_span;
+    uint32_t fb_seq;
+    unsigned long long fb_pos;
     unsigned tail_mask, part_mask;  // pages with a sub-16 B EOF tail / a partial delivery
     int64_t total;                  // bytes this batch delivers
     int64_t rpc_n;
@@ -722,17 +726,16 @@ __device__ bool rpc_submit(const DevCtx& c, Smem& s, int64_t fid, int64_t off, i
       __nanosleep(200);
     }
   }
-  __threadfence();
   RpcReq* e = &c.ring[pos & c.ring_mask];
-  volatile RpcReq* ve = e;
-  ve->offset = off;
-  ve->size = size;
-  ve->fid = (int32_t)fid;
-  ve->slot = (int32_t)(slot | ((unsigned)half << 30));  // landing half in bit 30
-  ve->tb = s.tb;
   const uint32_t seq = (uint32_t)(pos + 1);
-  __threadfence_system();
-  st_release_sys(&e->seq, seq);
+  const unsigned long long lap = ring_lap(pos, Q);  // every word carries it (see RpcReq)
+  const unsigned long long w0 = ((unsigned long long)off << 16) | lap;
+  const unsigned long long w1 = ((unsigned long long)(uint32_t)size << 32) | ((unsigned long long)(fid & 0xFFFF) << 16) | lap;
+  const unsigned long long w2 = ((unsigned long long)(uint32_t)s.tb << 32) |
+                                ((unsigned long long)((slot | ((unsigned)half << 15)) & 0xFFFF) << 16) | lap;
+  asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(&e->w[0]), "l"(w0) : "memory");
+  asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(&e->w[1]), "l"(w1) : "memory");
+  asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(&e->w[2]), "l"(w2) : "memory");
   *seq_out = seq;
   *pos_out = pos;
   // the reference's slot partition (rpc.py:25-28, 82-89): TB tb owns slot tb % n_slots and
@@ -1213,26 +1216,6 @@ __device__ int64_t od_plan_sync(const DevCtx& c, Smem& s, int64_t fid, int64_t p
   return q - p0;
 }
 
-// The synchronous span (thread 0): requested, then the decided asynchronous run, then
-// waited for; it becomes the private buffer's span.  Returns bytes, -1 on abort.
-__device__ int64_t fetch_span_od(const DevCtx& c, Smem& s, int64_t fid, int64_t page, int64_t sync_pages,
-                                 int64_t* span_out) {
-  const int64_t pg = c.page_size, fs = c.files[fid].size;
-  int64_t span = sync_pages * pg;
-  if (span > fs - page * pg) span = fs - page * pg;
-  *span_out = span;
-  if (span <= 0) {
-    s.od.run_n = 0;
-    return 0;
-  }
-  const int hs = od_pick_half(c, s, -1);
-  if (hs < 0 || !od_submit(c, s, fid, page, span, hs, false)) return -1;
-  if (!od_submit_run(c, s, fid, hs)) return -1;
-  const int64_t n = od_wait(c, s, hs);
-  s.fetch_half = hs;
-  return n;
-}
-
 // TB done: drop windows it did not reach.
 __device__ int od_drain_all(const DevCtx& c, Smem& s) {
   for (int h = 0; h < 2; h++)
@@ -1242,19 +1225,56 @@ __device__ int od_drain_all(const DevCtx& c, Smem& s) {
 
 // The span starting at `page` (thread 0): request_span + RPC (prefetcher.py:13-25,
 // rpc.py:82-229); under ondemand readahead the synchronous span of the request's missing
-// pages (sync_pages from od_plan_sync; < 0 = plan it here, claims [page, page + 1)).
-// Returns bytes, -1 on abort.
-__device__ int64_t fetch_span(const DevCtx& c, Smem& s, int64_t fid, int64_t page, int64_t seg_end,
-                              int64_t* span_out, int64_t sync_pages = -1) {
+// pages (sync_pages from od_plan_sync; < 0 = plan it here, claims [page, page + 1)).  In two
+// halves so that a batch overlaps the RPC round trip with its frame allocation and eviction
+// (the request is the same; only its wait moves): fetch_begin submits, fetch_end waits and
+// accounts.  False / -1 on abort.
+__device__ bool fetch_begin(const DevCtx& c, Smem& s, int64_t fid, int64_t page, int64_t seg_end,
+                            int64_t sync_pages) {
+  const int64_t pg = c.page_size;
   if (c.readahead == GFS_RA_ONDEMAND && c.files[fid].read_only) {
     if (sync_pages < 0) sync_pages = od_plan_sync(c, s, fid, page, page, page + 1);
-    return fetch_span_od(c, s, fid, page, sync_pages, span_out);
+    const int64_t fs = c.files[fid].size;
+    int64_t span = sync_pages * pg;
+    if (span > fs - page * pg) span = fs - page * pg;
+    s.b.fb_od = 1;
+    s.b.fb_span = span;
+    s.b.fb_h = -1;
+    if (span <= 0) {
+      s.od.run_n = 0;
+      return true;
+    }
+    const int hs = od_pick_half(c, s, -1);
+    if (hs < 0 || !od_submit(c, s, fid, page, span, hs, false)) return false;
+    if (!od_submit_run(c, s, fid, hs)) return false;
+    s.b.fb_h = hs;
+    return true;
   }
-  const int64_t pg = c.page_size;
   int h = 0;
-  if (c.readahead == GFS_RA_ONDEMAND && (h = od_pick_half(c, s, -1)) < 0) return -1;  // non-RO file
+  if (c.readahead == GFS_RA_ONDEMAND && (h = od_pick_half(c, s, -1)) < 0) return false;  // non-RO file
   const int64_t span = rpc_span(c, s, fid, page, seg_end);
-  const int64_t n = span > 0 ? rpc_call(c, s, fid, page * pg, span, h) : 0;
+  s.b.fb_od = 0;
+  s.b.fb_h = h;
+  s.b.fb_span = span;
+  if (span > 0) {
+    if (!wait_landed(c, s, h, s.st_n[h])) return false;  // the half's previous window is in
+    if (!rpc_submit(c, s, fid, page * pg, span, h, &s.b.fb_seq, &s.b.fb_pos)) return false;
+  }
+  return true;
+}
+
+__device__ int64_t fetch_end(const DevCtx& c, Smem& s, int64_t fid, int64_t page, int64_t* span_out) {
+  const int64_t span = s.b.fb_span;
+  *span_out = span;
+  if (s.b.fb_od) {
+    if (span <= 0) return 0;
+    const int64_t n = od_wait(c, s, s.b.fb_h);
+    s.fetch_half = s.b.fb_h;
+    return n;
+  }
+  const int h = s.b.fb_h;
+  const int64_t pg = c.page_size;
+  const int64_t n = span > 0 ? rpc_wait(c, s, fid, page * pg, s.b.fb_seq, s.b.fb_pos, h) : 0;
   if (n >= 0) {
     log_rec(c, GFS_LOG_RPCS, s.tb, fid, page * pg, span);
     ST(rpc_count)++;
@@ -1262,8 +1282,13 @@ __device__ int64_t fetch_span(const DevCtx& c, Smem& s, int64_t fid, int64_t pag
     account_transfer(c, s, n);
   }
   s.fetch_half = h;
-  *span_out = span;
   return n;
+}
+
+__device__ int64_t fetch_span(const DevCtx& c, Smem& s, int64_t fid, int64_t page, int64_t seg_end,
+                              int64_t* span_out, int64_t sync_pages = -1) {
+  if (!fetch_begin(c, s, fid, page, seg_end, sync_pages)) return -1;
+  return fetch_end(c, s, fid, page, span_out);
 }
 
 // ------------------------------------------------------------------ copies (all threads)
@@ -1572,6 +1597,9 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
 
   // (B) thread 0: how many of them this batch can serve, and their frames
   if (tid == 0) {
+    const uint64_t tb0 = globaltimer();
+    ST(lookup_ns) += (long long)(tb0 - t_start);  // batch phase A: claims (incl. ondemand top)
+    s.t_copy0 = tb0;
     int kp = 1;
     s.b.sync_m = -1;
     if (pb_has(s, fid, p0)) {
@@ -1588,6 +1616,16 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
     }
     int kk = c.policy == GFS_POLICY_GLOBAL_LRU ? plan_global(c, s, kp) : plan_per_tb(c, s, kp);
     if (has_error(c)) kk = 0;
+    // page 0's RPC goes out now: its round trip overlaps the evictions of (C)
+    s.b.early = 0;
+    if (kk >= 1 && !pb_has(s, fid, p0)) {
+      if (fetch_begin(c, s, fid, p0, seg_end, s.b.sync_m)) {
+        s.b.early = 1;
+      } else {
+        if (!has_error(c)) set_error(c, ERR_IO, (int)fid, (unsigned long long)p0);
+        kk = 0;
+      }
+    }
     s.b.k = kk;
   }
   __syncthreads();
@@ -1646,6 +1684,7 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
   // Page 0 of the batch is a private-buffer hit or the RPC's own page; every later page
   // is a private-buffer hit (planned in (B)), taken as one run.
   if (tid == 0) {
+    ST(alloc_ns) += (long long)(globaltimer() - s.t_copy0);  // batch phases B + C: plan, RPC out, evictions
     int status = 0, j0 = 0;
     ST(pc_lookups) += kk;
     ST(pc_misses) += kk;
@@ -1654,7 +1693,8 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
       ST(pb_misses)++;
       j0 = 1;
       int64_t span;
-      const int64_t n = fetch_span(c, s, fid, page, seg_end, &span, s.b.sync_m);
+      const int64_t n = s.b.early ? fetch_end(c, s, fid, page, &span)
+                                  : fetch_span(c, s, fid, page, seg_end, &span, s.b.sync_m);
       if (n < 0) {
         status = 2;
       } else if (n == 0) {

@@ -376,7 +376,13 @@ static void worker_main(gfs_ctx* ctx, int wid) {
     const uint64_t t_wait = now_ns();
     ctx->w_pos[wid].store(h, std::memory_order_relaxed);
     ctx->w_phase[wid].store(0, std::memory_order_relaxed);
-    while (__atomic_load_n(&e->seq, __ATOMIC_ACQUIRE) != seq) {
+    const uint64_t lap = ring_lap(h, mask + 1ull);
+    uint64_t w0, w1, w2;
+    for (;;) {  // the entry is complete when all three words carry this lap (see RpcReq)
+      w0 = __atomic_load_n(&e->w[0], __ATOMIC_ACQUIRE);
+      w1 = __atomic_load_n(&e->w[1], __ATOMIC_ACQUIRE);
+      w2 = __atomic_load_n(&e->w[2], __ATOMIC_ACQUIRE);
+      if ((w0 & 0xFFFF) == lap && (w1 & 0xFFFF) == lap && (w2 & 0xFFFF) == lap) break;
       if (ctx->stop.load(std::memory_order_relaxed)) return;
       if (++spins < 20000) {
         _mm_pause();
@@ -388,8 +394,9 @@ static void worker_main(gfs_ctx* ctx, int wid) {
     const uint64_t t0 = now_ns();
     ctx->t_idle.fetch_add((int64_t)(t0 - t_wait), std::memory_order_relaxed);
     ctx->w_phase[wid].store(1, std::memory_order_relaxed);
-    const int64_t off = e->offset, size = e->size;
-    const int fid = e->fid, slot = e->slot & 0x3FFFFFFF, half = (e->slot >> 30) & 1;
+    const int64_t off = (int64_t)(w0 >> 16), size = (int64_t)(w1 >> 32);
+    const int fid = (int)((w1 >> 16) & 0xFFFF);
+    const int slot = (int)((w2 >> 16) & 0x7FFF), half = (int)((w2 >> 31) & 1);
     // the entry's fields are copied out: the device may reuse it (ring wrap) from now on,
     // whether or not the CTA that asked has come back for its answer yet
     __atomic_store_n(&ctx->h_consumed[h & mask], seq, __ATOMIC_RELEASE);
@@ -856,6 +863,7 @@ extern "C" int gfs_transfer(gfs_ctx* ctx, int* transfer, int* downgraded_from) {
 
 extern "C" int gfs_gopen(gfs_ctx* ctx, const char* path, int flags, int64_t content_id, int* fid) {
   if (!ctx || !path || !fid) return fail(GFS_EINVAL, "gfs_gopen: null argument");
+  if (ctx->files.size() >= 65535) return fail(GFS_EINVAL, "gfs_gopen: at most 65535 files per context");
   HostFile f;
   f.path = path;
   f.read_only = (flags & GFS_O_RDWR) ? 0 : 1;
@@ -870,6 +878,11 @@ extern "C" int gfs_gopen(gfs_ctx* ctx, const char* path, int flags, int64_t cont
     return fail(GFS_EIO, "stat %s: %s", path, strerror(errno));
   }
   f.size = (int64_t)sb.st_size;
+  if (f.size >= (1ll << 48)) {  // ring entries carry 48-bit offsets
+    close(f.fd_buffered);
+    if (f.fd_direct >= 0) close(f.fd_direct);
+    return fail(GFS_EINVAL, "gfs_gopen: %s is larger than 256 TiB", path);
+  }
   f.npages = (f.size + ctx->cfg.page_size - 1) / ctx->cfg.page_size + 1;
   cudaSetDevice(ctx->cfg.device);
   if (!ctx->cfg.raw_mode) {
@@ -1303,8 +1316,9 @@ static int run_prepared(gfs_ctx* ctx, const gfs_program* prog, void* dst, const 
       const uint32_t seq = (uint32_t)g.error_arg;
       char b[256];
       const RpcReq* e = &ctx->h_ring[(seq - 1) & (ctx->ring_size - 1)];
-      snprintf(b, sizeof b, "; slot %d half %d seq %u: ring entry seq %u slot %d, mailbox seq %u", slot,
-               mb % ctx->landing_halves, seq, e->seq, e->slot,
+      snprintf(b, sizeof b, "; slot %d half %d seq %u: ring entry lap %u (want %u) slot %d, mailbox seq %u", slot,
+               mb % ctx->landing_halves, seq, (unsigned)(e->w[2] & 0xFFFF),
+               ring_lap(seq - 1, ctx->ring_size), (int)((e->w[2] >> 16) & 0x7FFF),
                slot < ctx->n_ctas ? ctx->h_resp[mb].seq : 0);
       diag += b;
       if (ctx->d_doorbell && slot < ctx->n_ctas) {

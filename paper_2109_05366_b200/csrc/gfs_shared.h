@@ -19,15 +19,22 @@ constexpr int RET_POOLS = 32;                 // retired-frame FIFOs (per-tb-lra
 // Copy-engine windows of at least 2 pieces can land piece by piece, each piece followed
 // by a "landed" marker: the CTA starts on the first piece while the rest copy.
 
-// Request record in the mapped request ring (device writes, host daemon reads).
+// Request record in the mapped request ring (device writes, host daemon reads): three
+// 64-bit words, each tagged in its low 16 bits with the entry's lap (ring position / ring
+// size, mod 65535, + 1).  A 64-bit store from the GPU reaches host memory as one piece and
+// an aligned 64-bit load on the host is atomic, so the daemon takes the entry once all three
+// words show the lap it expects — the device needs no system-scope fence to publish a
+// request (a membar.sys waits behind the link's read traffic: ~30 us per request under
+// load; 16-byte stores are not seen whole by the host).
+//   w0 = offset << 16 | lap                        (offsets < 2^48)
+//   w1 = size << 32 | fid << 16 | lap              (size < 2^32, fid < 2^16)
+//   w2 = tb << 32 | (slot | half << 15) << 16 | lap  (slot < 2^15)
 struct alignas(32) RpcReq {
-  int64_t offset;
-  int64_t size;
-  int32_t fid;
-  int32_t slot;     // resident CTA slot: response + staging index
-  int32_t tb;
-  uint32_t seq;     // written last (release): ring position + 1
+  unsigned long long w[4];  // w[3] unused
 };
+__host__ __device__ inline uint32_t ring_lap(unsigned long long pos, unsigned long long q) {
+  return (uint32_t)((pos / q) % 65535ull) + 1u;
+}
 
 // Response mailbox per CTA slot (host writes, device polls).  One cache line
 // each so concurrent workers never share a line.

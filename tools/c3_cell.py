@@ -52,7 +52,7 @@ def main():
             out = {"cell": cell, "arm": a.arm, "set": a.set, "gbps": round(size / st["kernel_ns"], 3),
                    "transfer": fs.transfer, "ctas": st["ctas"], "rpc_count": st["rpc_count"],
                    "per_cta_ms": {k: round(st[k] / max(1, min(n_tb, st["ctas"])) / 1e6, 2)
-                                  for k in ("wait_ns", "meta_ns", "copy_ns", "install_ns")},
+                                  for k in ("wait_ns", "meta_ns", "copy_ns", "install_ns", "lookup_ns", "alloc_ns")},
                    "kernel_ms": round(st["kernel_ns"] / 1e6, 2)}
             if a.timeline and r.timeline is not None:
                 d = timeline.decode(r.timeline)
