@@ -62,8 +62,11 @@ __device__ __forceinline__ uint64_t ld_acquire_sys64(const unsigned long long* p
   asm volatile("ld.acquire.sys.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.sys.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+// Hand a host pool buffer back to the daemon.  Only *loads* from the buffer precede it, and
+// they have all returned (the caller passed a barrier after using the values), so a relaxed
+// system-scope store is enough: no membar.sys, which would wait behind the link's reads.
+__device__ __forceinline__ void st_relaxed_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 // device-memory counters shared by CTAs: relaxed loads at GPU scope (no system-scope
 // strong load needed: the host never writes them while the kernel runs)
@@ -1111,8 +1114,7 @@ __device__ int od_drain(const DevCtx& c, Smem& s, int h) {
   if (n < 0 || !wait_landed(c, s, h, n)) return -1;
   if (s.pull_n > 0) {  // never pulled: hand a bounce buffer straight back
     if (s.pull_buf >= 0) {
-      __threadfence_system();
-      st_release_sys(&c.bounce_release[s.pull_buf], s.pull_seq);
+      st_relaxed_sys(&c.bounce_release[s.pull_buf], s.pull_seq);
     }
     s.pull_n = 0;
   }
@@ -1339,8 +1341,7 @@ __device__ void pull_span(const DevCtx& c, Smem& s) {
   __syncthreads();  // every load has returned: the buffer may be reused
   if (threadIdx.x == 0) {
     if (s.pull_buf >= 0) {
-      __threadfence_system();
-      st_release_sys(&c.bounce_release[s.pull_buf], s.pull_seq);
+      st_relaxed_sys(&c.bounce_release[s.pull_buf], s.pull_seq);
     }
     s.pull_n = 0;
   }
