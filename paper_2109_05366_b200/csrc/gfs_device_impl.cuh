@@ -815,7 +815,7 @@ __device__ int64_t rpc_wait(const DevCtx& c, Smem& s, int64_t fid, int64_t off, 
     }
   } else {
     const RpcResp* r = &c.resp[(int64_t)slot * c.landing_halves + half];
-    __nanosleep(2000);
+    __nanosleep(c.poll_first_ns);
     for (;;) {
       if (ld_acquire_sys(&r->seq) == seq) {
         n = *(volatile const int64_t*)&r->nbytes;
@@ -842,7 +842,7 @@ __device__ int64_t rpc_wait(const DevCtx& c, Smem& s, int64_t fid, int64_t off, 
         c.g->error_arg = ((unsigned long long)(slot * c.landing_halves + half) << 32) | seq;
         return -1;
       }
-      __nanosleep(4000);
+      __nanosleep(c.poll_ns);
     }
   }
   atomicMax(&c.done_pos[pos & c.ring_mask], pos + 1);

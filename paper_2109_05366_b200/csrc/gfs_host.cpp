@@ -1208,6 +1208,9 @@ static int run_prepared(gfs_ctx* ctx, const gfs_program* prog, void* dst, const 
   c.done_pos = ctx->d_done_pos;
   c.slot_busy = ctx->d_slot_busy;
   c.ref_slots = cfg.rpc_slots;
+  c.poll_first_ns = 2000;  // mailbox polls are PCIe reads queued behind the data: not too eager
+  c.poll_ns = 4000;
+  if (const char* e = getenv("GFS_POLL_NS")) c.poll_first_ns = c.poll_ns = (uint32_t)atoi(e);  // experiments
   c.k1_direct = cfg.k1_direct && (cfg.transfer == GFS_XFER_MAPPED_ZC || cfg.transfer == GFS_XFER_MAPPED_HYBRID);
   c.ce_min = ctx->ce_min;
   c.stats = ctx->d_stats;

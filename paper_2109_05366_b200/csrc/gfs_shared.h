@@ -149,6 +149,7 @@ struct DevCtx {
   // the reference's RPC slot partition (rpc.n_slots): requests outstanding per slot tb % n
   uint32_t* slot_busy;
   int32_t ref_slots;
+  uint32_t poll_first_ns, poll_ns;  // host-memory mailbox polling: first wait, then period
   int32_t k1_direct;         // pulled spans (mapped, small mapped_hybrid) are read by K1 straight
                              // from the pinned file mapping: no landing copy
   int64_t ce_min;            // mapped_hybrid / pread_hybrid: spans of at least this size go by copy engine
