@@ -1,11 +1,6 @@
-cd "${GRAFT_REPO_ROOT:-/root/repo}"; O=gpurun_out/x17; mkdir -p $O
-C="--cell 64x4K --cell 64x64K --cell 128x4K --cell 128x64K --cell 1024x64K"
-for p in 4000 1000 500 250; do
-  GFS_POLL_NS=$p timeout 600 python tools/c3_cell.py $C --arm prefetch_static > $O/cells_$p.log 2>&1
-  GFS_POLL_NS=$p timeout 600 python tools/consumer_probe.py > $O/cons_$p.log 2>&1
-  GFS_POLL_NS=$p timeout 600 python tools/preset_probe.py > $O/preset_$p.log 2>&1
-done
-for p in 4000 1000 500 250; do echo "== $p"; grep -h cell $O/cells_$p.log | python3 -c "
-import sys,json
-for l in sys.stdin:
-    d=json.loads(l); print(d['cell'], d['gbps'], d['per_cta_ms']['wait_ns'])"; grep variant $O/cons_$p.log | cut -c1-60; grep '"rep": 2' $O/preset_$p.log | cut -c1-80; done
+cd "${GRAFT_REPO_ROOT:-/root/repo}"; O=gpurun_out/x18; mkdir -p $O/timeline
+timeout 1500 python tools/sweep_c3.py --out $O/c3.json > $O/c3.log 2>&1
+timeout 900 python tools/timeline_run.py --out $O/timeline > $O/timeline.log 2>&1
+GFS_BENCH_SHARE_GPU=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 3 --warmup 3 --total-gib 8 --quick > $O/bench_n2_shared.log 2>&1
+timeout 600 python tools/preset_probe.py > $O/preset.log 2>&1
+tail -3 $O/c3.log; tail -c 300 $O/bench_n2_shared.log
