@@ -24,7 +24,10 @@ from paper_2109_05366_b200.runtime import Simulation  # noqa: E402
 base = bench.make_cfg(bench.headline_overrides(16 << 30, 1, "/dev/shm"), [])
 bench.ensure_file(base, bench.Dist(1))
 for label, mcfg in PRESETS["mosaic"](base):
-    for extra in ({}, {"io.transfer": "bounce"}, {"workload.n_tb": 512}, {"workload.requests_per_tb": 1024}):
+    extras = [{}, {"io.transfer": "bounce"}, {"workload.n_tb": 512}, {"workload.requests_per_tb": 1024}]
+    if os.environ.get("GFS_MOSAIC_EXTRAS"):  # e.g. '[{}, {"gpu.k1_direct": false}]'
+        extras = json.loads(os.environ["GFS_MOSAIC_EXTRAS"])
+    for extra in extras:
         cfg = mcfg.copy_with({"workload.file_bytes": base["workload.file_bytes"], "mode.timeline": True, **extra})
         sim = Simulation(cfg, 42)
         t0 = time.time(); rep = sim.run(); wall = time.time() - t0
