@@ -126,13 +126,19 @@ __device__ __forceinline__ uint8_t ld1(const uint8_t* p) {
 
 // ----------------------------------------------------------------- CTA state
 
-constexpr int TMA_NST = 4;        // K1 stage ring: stages
+constexpr int TMA_NST = 4;        // K1 stage ring: stages (at least)
+constexpr int TMA_NST_MAX = 5;    // ... and at most, when the consumer's shared state leaves room
+// stage and mbarrier phase of chunk g in an n-stage ring (n = 4 or 5: constant divisors)
+__device__ __forceinline__ int stage_of(unsigned long long g, int n) { return n == 5 ? (int)(g % 5) : (int)(g & 3); }
+__device__ __forceinline__ uint32_t phase_of(unsigned long long g, int n) {
+  return n == 5 ? (uint32_t)((g / 5) & 1) : (uint32_t)((g >> 2) & 1);
+}
 constexpr int OD_MARKS = 4;       // readahead markers remembered per TB stream
 constexpr int64_t TMA_CH = 8192;  // bytes per stage (one bulk load, 1-2 bulk stores per page)
 
 struct Smem {
-  unsigned long long tma_bar[TMA_NST];    // stage "full" mbarriers (tx-count)
-  unsigned long long tma_empty[TMA_NST];  // stage "checked" mbarriers (one arrival per checker warp)
+  unsigned long long tma_bar[TMA_NST_MAX];    // stage "full" mbarriers (tx-count)
+  unsigned long long tma_empty[TMA_NST_MAX];  // stage "checked" mbarriers (one arrival per checker warp)
   unsigned long long tma_seq;             // chunks staged since launch (stage / parity)
   uint32_t tma_epend;                     // bit st: stage st awaits its checkers before reuse
   uint32_t tma_epar;                      // bit st: parity of that pending phase
@@ -1797,11 +1803,12 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
     uint8_t* ring = (uint8_t*)cons_smem + c.tma_off;
     const int64_t total_b = (int64_t)kk * pg;
     const int nch = (int)((total_b + TMA_CH - 1) / TMA_CH);
+    const int NST = c.tma_nst;  // stages in flight (4, or 5 when the shared state leaves room)
     const unsigned long long G0 = s.tma_seq;
     const uint8_t* srcb = (const uint8_t*)src4;
     const int warp = tid >> 5;
     auto load = [&](int i) {  // thread 0
-      const int st = (int)((G0 + i) % TMA_NST);
+      const int st = stage_of(G0 + i, NST);
       if (s.tma_epend & (1u << st)) {  // the stage's last chunk must be checked before reuse
         mbar_wait_t(c, &s.tma_empty[st], (s.tma_epar >> st) & 1u, 42,
                     ((G0 + i) << 16) | ((unsigned long long)st << 8) | (unsigned)(i & 0xff));
@@ -1815,12 +1822,12 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
     if (tid == 0) {
       // landing bytes written by the copy engine / generic proxy, read by the async proxy
       asm volatile("fence.proxy.async.global;" ::: "memory");
-      for (int i = 0; i < nch && i < TMA_NST; i++) load(i);
+      for (int i = 0; i < nch && i < NST; i++) load(i);
     }
     for (int i = 0; i < nch; i++) {
       const unsigned long long G = G0 + i;
-      const int st = (int)(G % TMA_NST);
-      const uint32_t par = (uint32_t)((G / TMA_NST) & 1);
+      const int st = stage_of(G, NST);
+      const uint32_t par = phase_of(G, NST);
       const int64_t b0 = (int64_t)i * TMA_CH;
       const int64_t cb = min(TMA_CH, total_b - b0);
       const uint8_t* sbuf = ring + st * TMA_CH;
@@ -1855,9 +1862,9 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
         }
         tma_commit();
         if (chk) s.tma_epend |= 1u << st;
-        if (i >= 1 && i - 1 + TMA_NST < nch) {  // refill the stage chunk i - 1 used
-          tma_wait_read<1>();                   // its stores have read it (chunk i's may not)
-          load(i - 1 + TMA_NST);
+        if (i >= 1 && i - 1 + NST < nch) {  // refill the stage chunk i - 1 used
+          tma_wait_read<1>();               // its stores have read it (chunk i's may not)
+          load(i - 1 + NST);
         }
       }
     }
@@ -2321,7 +2328,7 @@ __device__ void cta_begin(const DevCtx& c, Smem& s) {
     s.tma_epend = 0;
     s.tma_epar = 0;
     if (c.tma) {
-      for (int i = 0; i < TMA_NST; i++) {
+      for (int i = 0; i < TMA_NST_MAX; i++) {
         mbar_init(&s.tma_bar[i], 1);
         mbar_init(&s.tma_empty[i], BS / 32 - 1);  // the checker warps
       }

@@ -45,6 +45,7 @@ cudaError_t occupancy_gread(int cta_threads, int* blocks_per_sm);
 cudaError_t launch_queue_probe(const unsigned long long* flags, int n, uint64_t timeout_ns, int* ok,
                                cudaStream_t st);
 int64_t gread_tma_offset(const gfs_consumer& k, int cta_threads);
+int gread_tma_stages(const gfs_consumer& k, int cta_threads);
 int64_t gread_launch_smem(const gfs_consumer& k, int cta_threads, int tma);
 cudaError_t launch_check_mapping(const DevFile* files, int n_files, const unsigned long long* fkey,
                                  const uint32_t* fstate, uint32_t* owner, int64_t nframes,
@@ -1223,6 +1224,9 @@ static int run_prepared(gfs_ctx* ctx, const gfs_program* prog, void* dst, const 
     if (off >= 0) {
       c.tma = 1;
       c.tma_off = (int32_t)off;
+      c.tma_nst = gread_tma_stages(c.cons, cfg.cta_threads);
+      if (const char* e = getenv("GFS_TMA_STAGES"))  // experiments: fewer stages than fit
+        c.tma_nst = std::max(1, std::min(c.tma_nst, atoi(e)));
     }
   }
   for (int k = 0; k < 5; k++) {

@@ -62,8 +62,13 @@ __host__ __device__ inline int64_t kmeans_ct_off(const gfs_consumer& k, int bs) 
 __host__ __device__ inline int64_t tma_ring_offset(const gfs_consumer& k, int bs) {
   return (consumer_smem_bytes(k, bs) + 127) / 128 * 128;
 }
+// Stages of the ring: five when they fit beside the consumer's state, else four.  Five
+// stages (40 KiB) + the static control block still let 4 CTAs (592 TBs) share an SM.
+inline int tma_ring_stages(const gfs_consumer& k, int bs) {
+  return tma_ring_offset(k, bs) + TMA_NST_MAX * TMA_CH <= CONS_SMEM_MAX ? TMA_NST_MAX : TMA_NST;
+}
 inline int64_t gread_smem_bytes(const gfs_consumer& k, int bs, int tma) {
-  return tma ? tma_ring_offset(k, bs) + TMA_NST * TMA_CH : consumer_smem_bytes(k, bs);
+  return tma ? tma_ring_offset(k, bs) + tma_ring_stages(k, bs) * TMA_CH : consumer_smem_bytes(k, bs);
 }
 
 // y += A x over the request's rows (cols % 4 == 0: one row per 16-byte vector).
@@ -712,6 +717,8 @@ cudaError_t launch_gread(const DevCtx& c, int cta_threads, cudaStream_t st) {
 int64_t gread_launch_smem(const gfs_consumer& k, int cta_threads, int tma) {
   return gread_smem_bytes(k, cta_threads, tma);
 }
+
+int gread_tma_stages(const gfs_consumer& k, int cta_threads) { return tma_ring_stages(k, cta_threads); }
 
 int64_t gread_tma_offset(const gfs_consumer& k, int cta_threads) {
   const int64_t off = tma_ring_offset(k, cta_threads);

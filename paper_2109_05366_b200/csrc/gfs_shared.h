@@ -104,6 +104,7 @@ struct DevCtx {
   int64_t stream_piece;      // piece bytes (windows of >= 2 pieces are streamed)
   unsigned long long* landed;  // [n_ctas * landing_halves]: (4 KiB pages landed << 32) | seq
   int32_t tma_off;           // byte offset of the stage ring in dynamic shared memory
+  int32_t tma_nst;           // stages in the ring
   int32_t n_files, n_tb, n_ctas;
   uint32_t ring_mask;
   uint64_t timeout_ns;
