@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define GFS_ABI_VERSION 8  /* 8: k1_direct; 5: rpc_slots; 4: gfs_run_kernel (user kernels over gfs_device.cuh); 3: ondemand law */
+#define GFS_ABI_VERSION 9  /* 9: k1_early; 8: k1_direct; 5: rpc_slots; 4: gfs_run_kernel (user kernels over gfs_device.cuh); 3: ondemand law */
 
 enum { GFS_OK = 0, GFS_EINVAL = -1, GFS_ECUDA = -2, GFS_EIO = -3, GFS_ENOMEM = -4,
        GFS_ETIMEDOUT = -5, GFS_EDEVICE = -6, GFS_ESTATE = -7 };
@@ -100,6 +100,9 @@ typedef struct gfs_config {
   int32_t k1_direct;       /* gpu.k1_direct: spans of the mapped transfers that the CTA would pull
                               are read by the span copy (K1) straight from the pinned file mapping
                               into frames + user buffer (one pass, no HBM landing copy) */
+  int32_t k1_early;        /* gpu.k1_early: such a span is read before the daemon's answer comes
+                              back (the answer is the span length, known from the file size); the
+                              answer is collected before the CTA's next request and checked */
 } gfs_config;
 
 /* One gread program set (workloads.py:24-31 programs, flattened).
@@ -124,7 +127,7 @@ typedef struct gfs_program {
   X(rpc_requested_bytes) X(slot_collisions) X(preads) X(pread_bytes) X(storage_bytes)       \
   X(pcie_bytes) X(pcie_transfers) X(victims) X(kernel_ns) X(wall_ns) X(ctas) X(word_mismatches) \
   X(wait_ns) X(meta_ns) X(copy_ns) X(lookup_ns) X(alloc_ns) X(install_ns) X(host_pread_ns) \
-  X(host_idle_ns) X(host_xfer_ns) X(host_requests) X(io_workers)
+  X(host_idle_ns) X(host_xfer_ns) X(host_requests) X(io_workers) X(early_answers)
 
 enum {
 #define GFS_X(name) GFS_STAT_##name,

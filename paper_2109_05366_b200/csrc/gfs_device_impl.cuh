@@ -219,6 +219,21 @@ struct Smem {
   uint32_t hp_age;
   uint32_t rpc_out;  // this TB's requests outstanding (submitted, not yet waited for)
   int direct[2];       // half h's span is read straight from the pinned file mapping (K1 direct)
+  int sm_rank;         // this CTA's start order among the CTAs on its SM
+  int first_ticket;    // next_tb has not handed this CTA a TB yet
+  // K1 early: a static request whose span K1 read before the daemon's answer (collected and
+  // checked by early_collect before the CTA's next request / at TB end)
+  struct {
+    int on, half, polled;
+    uint32_t seq;
+    unsigned long long pos;
+    int64_t fid, off, n;
+    uint64_t t_sub;
+  } early;
+  // the answer's mailbox line, fetched by an asynchronous bulk copy while K1 runs
+  unsigned long long poll_bar;
+  uint32_t poll_par;
+  uint4 poll_buf;
   int64_t pull_off;            // file offset of the span waiting to be pulled
   int64_t dbg_land_off[2], dbg_land_n[2];  // what each landing half last received (diagnostics)
   uint32_t pb_absent[MAX_PB_ENTRIES / 32];  // private-buffer entries consumed / dropped
@@ -757,10 +772,17 @@ __device__ bool rpc_submit(const DevCtx& c, Smem& s, int64_t fid, int64_t off, i
   return true;
 }
 
+// A request's answer has been seen (thread 0): its ring entry and slot are free again.
+__device__ __forceinline__ void rpc_retire(const DevCtx& c, Smem& s, unsigned long long pos) {
+  atomicMax(&c.done_pos[pos & c.ring_mask], pos + 1);
+  atomicSub(&c.slot_busy[s.tb % c.ref_slots], 1u);  // slot released when the data is ready (rpc.py:104-113)
+  s.rpc_out--;
+}
+
 // Wait for the completion of request (seq, pos) of file `fid` at `off` (thread 0):
 // rpc.py:192-229.  Returns bytes read, or -1 on abort.
 __device__ int64_t rpc_wait(const DevCtx& c, Smem& s, int64_t fid, int64_t off, uint32_t seq,
-                            unsigned long long pos, int half) {
+                            unsigned long long pos, int half, bool first_nap = true) {
   const unsigned slot = blockIdx.x;
   const uint64_t t0 = globaltimer();
   const uint64_t tw = globaltimer();
@@ -821,7 +843,7 @@ __device__ int64_t rpc_wait(const DevCtx& c, Smem& s, int64_t fid, int64_t off, 
     }
   } else {
     const RpcResp* r = &c.resp[(int64_t)slot * c.landing_halves + half];
-    __nanosleep(c.poll_first_ns);
+    if (first_nap) __nanosleep(c.poll_first_ns);
     for (;;) {
       if (ld_acquire_sys(&r->seq) == seq) {
         n = *(volatile const int64_t*)&r->nbytes;
@@ -851,9 +873,7 @@ __device__ int64_t rpc_wait(const DevCtx& c, Smem& s, int64_t fid, int64_t off, 
       __nanosleep(c.poll_ns);
     }
   }
-  atomicMax(&c.done_pos[pos & c.ring_mask], pos + 1);
-  atomicSub(&c.slot_busy[s.tb % c.ref_slots], 1u);  // slot released when the data is ready (rpc.py:104-113)
-  s.rpc_out--;
+  rpc_retire(c, s, pos);
   if (c.stream_pieces && n > 0) {  // the doorbell comes after the first piece
     s.st_seq[half] = seq;
     s.st_n[half] = n;
@@ -899,10 +919,63 @@ __device__ __forceinline__ const uint8_t* span_base(const DevCtx& c, const Smem&
   return half_base(c, s.span_half);
 }
 
+// K1 early (gpu.k1_early, thread 0).  For the mapped transfers with K1 direct the daemon's
+// answer to a static request carries nothing but the span length, min(size, file size - off)
+// (gfs_host.cpp io_worker, `from_map`), and "read it from the mapping" — for mapped_hybrid
+// when that length is below the copy-engine size.  The device knows both, so K1 starts on the
+// span at once instead of after a mailbox round trip over the loaded link; the request is the
+// same (same ring entry, counters and trace), only its wait moves: early_collect waits for the
+// answer before the CTA's next request and at TB end, and a length other than the one K1
+// used (the file changed under the mapping) fails the run with ERR_IO.
+__device__ bool early_eligible(const DevCtx& c, int64_t n) {
+  return c.k1_early && n > 0 &&
+         (c.transfer == GFS_XFER_MAPPED_ZC || (c.transfer == GFS_XFER_MAPPED_HYBRID && n < c.ce_min));
+}
+
+//
+// Reading the answer is itself a PCIe read, and with the link loaded by K1's reads such a read
+// returns only after the bytes queued ahead of it (~10-20 us).  So K1's producer fetches the
+// mailbox line asynchronously (early_poll: a 16-byte bulk copy into shared memory, issued once
+// the span's first chunk is in — by then the daemon has answered) and early_collect finds the
+// answer already on chip; when the copy caught the mailbox before the answer (or anything
+// does not match) it falls back to polling.
+__device__ __forceinline__ void early_poll(const DevCtx& c, Smem& s) {
+  if (!s.early.on || s.early.polled) return;
+  s.early.polled = 1;
+  const RpcResp* r = &c.resp[(int64_t)blockIdx.x * c.landing_halves + s.early.half];
+  tma_load(&s.poll_buf, r, 16, &s.poll_bar);
+}
+
+__device__ bool early_collect(const DevCtx& c, Smem& s) {
+  if (!s.early.on) return true;
+  s.early.on = 0;
+  if (s.early.polled) {
+    s.early.polled = 0;
+    const uint32_t par = s.poll_par;
+    s.poll_par ^= 1u;
+    if (!mbar_wait_t(c, &s.poll_bar, par, 43, s.early.pos)) return false;
+    const int64_t n = (int64_t)(((unsigned long long)s.poll_buf.y << 32) | s.poll_buf.x);
+    if (s.poll_buf.z == s.early.seq && n == s.early.n) {  // answered: no poll on the link
+      rpc_retire(c, s, s.early.pos);
+      ST(early_answers)++;
+      tl_rec(c, GFS_TL_RPC, s.tb, n, s.early.t_sub, globaltimer());
+      return true;
+    }
+  }
+  const int64_t n = rpc_wait(c, s, s.early.fid, s.early.off, s.early.seq, s.early.pos, s.early.half, false);
+  if (n < 0) return false;
+  if (n != s.early.n || !s.direct[s.early.half]) {
+    set_error(c, ERR_IO, (int)s.early.fid, (unsigned long long)s.early.off);
+    return false;
+  }
+  return true;
+}
+
 // Submit and wait (the reference's synchronous RPC).
 __device__ int64_t rpc_call(const DevCtx& c, Smem& s, int64_t fid, int64_t off, int64_t size, int half = 0) {
   uint32_t seq;
   unsigned long long pos;
+  if (!early_collect(c, s)) return -1;
   if (!wait_landed(c, s, half, s.st_n[half])) return -1;  // the half's previous window is in
   if (!rpc_submit(c, s, fid, off, size, half, &seq, &pos)) return -1;
   return rpc_wait(c, s, fid, off, seq, pos, half);
@@ -1240,6 +1313,7 @@ __device__ int od_drain_all(const DevCtx& c, Smem& s) {
 __device__ bool fetch_begin(const DevCtx& c, Smem& s, int64_t fid, int64_t page, int64_t seg_end,
                             int64_t sync_pages) {
   const int64_t pg = c.page_size;
+  if (!early_collect(c, s)) return false;  // the previous request's answer, before the next one
   if (c.readahead == GFS_RA_ONDEMAND && c.files[fid].read_only) {
     if (sync_pages < 0) sync_pages = od_plan_sync(c, s, fid, page, page, page + 1);
     const int64_t fs = c.files[fid].size;
@@ -1271,7 +1345,8 @@ __device__ bool fetch_begin(const DevCtx& c, Smem& s, int64_t fid, int64_t page,
   return true;
 }
 
-__device__ int64_t fetch_end(const DevCtx& c, Smem& s, int64_t fid, int64_t page, int64_t* span_out) {
+__device__ int64_t fetch_end(const DevCtx& c, Smem& s, int64_t fid, int64_t page, int64_t* span_out,
+                             bool early = false) {
   const int64_t span = s.b.fb_span;
   *span_out = span;
   if (s.b.fb_od) {
@@ -1282,7 +1357,24 @@ __device__ int64_t fetch_end(const DevCtx& c, Smem& s, int64_t fid, int64_t page
   }
   const int h = s.b.fb_h;
   const int64_t pg = c.page_size;
-  const int64_t n = span > 0 ? rpc_wait(c, s, fid, page * pg, s.b.fb_seq, s.b.fb_pos, h) : 0;
+  const int64_t fs = c.files[fid].size;
+  const int64_t en = span > 0 && page * pg < fs ? min(span, fs - page * pg) : 0;  // the answer's length
+  int64_t n;
+  if (early && early_eligible(c, en)) {  // K1 early: read it now, collect the answer later
+    s.early.on = 1;
+    s.early.half = h;
+    s.early.seq = s.b.fb_seq;
+    s.early.pos = s.b.fb_pos;
+    s.early.fid = fid;
+    s.early.off = page * pg;
+    s.early.n = en;
+    s.early.polled = 0;
+    s.early.t_sub = globaltimer();
+    s.direct[h] = 1;
+    n = en;
+  } else {
+    n = span > 0 ? rpc_wait(c, s, fid, page * pg, s.b.fb_seq, s.b.fb_pos, h) : 0;
+  }
   if (n >= 0) {
     log_rec(c, GFS_LOG_RPCS, s.tb, fid, page * pg, span);
     ST(rpc_count)++;
@@ -1700,7 +1792,7 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
       ST(pb_misses)++;
       j0 = 1;
       int64_t span;
-      const int64_t n = s.b.early ? fetch_end(c, s, fid, page, &span)
+      const int64_t n = s.b.early ? fetch_end(c, s, fid, page, &span, true)
                                   : fetch_span(c, s, fid, page, seg_end, &span, s.b.sync_m);
       if (n < 0) {
         status = 2;
@@ -1849,6 +1941,7 @@ __device__ int64_t gread_batch(const DevCtx& c, Smem& s, int64_t fid, int64_t g_
       }
       if (tid == 0) {  // producer
         mbar_wait_t(c, &s.tma_bar[st], par, 40, (G << 16) | ((unsigned long long)st << 8) | (unsigned)(i & 0xff));
+        if (i == 0) early_poll(c, s);  // the span's answer, fetched while the rest streams
         // the chunk's pieces: page j gets [max(b0, j pg), min(b0 + cb, (j+1) pg))
         for (int64_t b = b0; b < b0 + cb;) {
           const int j = (int)(b / pg);
@@ -2327,11 +2420,17 @@ __device__ void cta_begin(const DevCtx& c, Smem& s) {
     s.fresh_done = 0;
     s.tma_epend = 0;
     s.tma_epar = 0;
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    s.sm_rank = smid < (uint32_t)GFS_MAX_SMS ? (int)atomicAdd(&c.g->sm_ctas[smid], 1u) : 0;
+    s.first_ticket = 1;
     if (c.tma) {
       for (int i = 0; i < TMA_NST_MAX; i++) {
         mbar_init(&s.tma_bar[i], 1);
         mbar_init(&s.tma_empty[i], BS / 32 - 1);  // the checker warps
       }
+      mbar_init(&s.poll_bar, 1);
+      s.poll_par = 0;
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     // ring base for this launch: the daemon's completed-request count
@@ -2349,7 +2448,28 @@ __device__ void cta_begin(const DevCtx& c, Smem& s) {
 
 // Dispatcher (gpu_exec.py:242-265): the next TB id in activation order, or -1 when every
 // TB has been handed out (or the run failed).
+//
+// Which CTA takes which ticket is free (per-TB observables are schedule-invariant), and it
+// matters when there are fewer TBs than resident CTAs: 64 TBs taken by whichever CTAs come
+// first put two or three of them on one SM, where they share its load/TMA issue and run
+// ~30 % slower than the rest, and the pass waits for them (C3 64 TBs x 4 KiB: most TBs done
+// at 45 ms, the SM-sharing ones at 56-62 ms).  So a CTA that is the r-th to start on its
+// SM takes its first ticket only once r x (SMs in use) tickets are gone — the first wave is
+// one TB per SM, then two, ... — or after 50 us, whichever comes first.
 __device__ int next_tb(const DevCtx& c, Smem& s) {
+  if (threadIdx.x == 0 && s.first_ticket) {
+    s.first_ticket = 0;
+    if (c.spread && s.sm_rank > 0) {
+      const int used = c.n_sms < c.n_ctas ? c.n_sms : c.n_ctas;
+      const unsigned long long want = (unsigned long long)s.sm_rank * (unsigned long long)used;
+      const uint64_t t0 = globaltimer();
+      for (;;) {
+        const unsigned long long k = ld_volatile_u64(&c.g->next_tb);
+        if (k >= want || k >= (unsigned long long)c.n_tb || has_error(c) || globaltimer() - t0 > 50000) break;
+        __nanosleep(256);
+      }
+    }
+  }
   if (threadIdx.x == 0) s.k = has_error(c) ? (int64_t)c.n_tb : (int64_t)atomicAdd(&c.g->next_tb, 1ull);
   __syncthreads();
   const int64_t k = s.k;
@@ -2381,6 +2501,8 @@ __device__ void tb_begin(const DevCtx& c, Smem& s, int tb) {
     s.seg_hi = 0;
     s.seg_ord = 0;
     s.rpc_out = 0;
+    s.early.on = 0;
+    s.early.polled = 0;
   }
   __syncthreads();
 }
@@ -2392,6 +2514,7 @@ __device__ void tb_end(const DevCtx& c, Smem& s) {
   const int tid = threadIdx.x;
   __shared__ unsigned long long ret_pos;
   if (tid == 0) {
+    if (!early_collect(c, s)) set_error(c, ERR_IO, -1, 0);
     if (od_drain_all(c, s) < 0) set_error(c, ERR_IO, -1, 0);
     ST(pb_discarded_bytes) += s.pb_filled;
     s.pb_filled = 0;

@@ -1177,6 +1177,9 @@ static int run_prepared(gfs_ctx* ctx, const gfs_program* prog, void* dst, const 
   c.n_files = (int32_t)ctx->files.size();
   c.n_tb = prog->n_tb;
   c.n_ctas = ctx->n_ctas;
+  c.n_sms = ctx->sms;
+  c.spread = 1;
+  if (const char* e = getenv("GFS_SPREAD")) c.spread = atoi(e);  // experiments
   c.ring_mask = ctx->ring_size - 1;
   c.timeout_ns = 60ull * 1000000000ull;
   c.segs = ctx->d_segs.p;
@@ -1213,6 +1216,9 @@ static int run_prepared(gfs_ctx* ctx, const gfs_program* prog, void* dst, const 
   c.poll_ns = 4000;
   if (const char* e = getenv("GFS_POLL_NS")) c.poll_first_ns = c.poll_ns = (uint32_t)atoi(e);  // experiments
   c.k1_direct = cfg.k1_direct && (cfg.transfer == GFS_XFER_MAPPED_ZC || cfg.transfer == GFS_XFER_MAPPED_HYBRID);
+  // K1 early: only where the daemon's answer is the span length (mapped transfers, K1 direct)
+  // and the request is the static request_span / doubling RPC (not an ondemand window)
+  c.k1_early = cfg.k1_early && c.k1_direct && cfg.readahead != GFS_RA_ONDEMAND;
   c.ce_min = ctx->ce_min;
   c.stats = ctx->d_stats;
   if (cons) c.cons = *cons;

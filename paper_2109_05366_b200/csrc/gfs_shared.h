@@ -54,6 +54,8 @@ struct DevFile {
   const uint8_t* map; // mapped transfers: device pointer of the pinned file mapping
 };
 
+constexpr int GFS_MAX_SMS = 256;
+
 // Global run state in device memory (zeroed per run).
 struct DevGlobals {
   unsigned long long next_tb;      // dispatcher ticket
@@ -72,6 +74,7 @@ struct DevGlobals {
   int error_info;
   unsigned long long error_arg;
   unsigned long long done_ctas;
+  uint32_t sm_ctas[GFS_MAX_SMS];   // CTAs of this launch started on each SM (cta_begin)
   // first K1 word mismatch seen (diagnostics, GFS_DEBUG_MISMATCH): set, tb, fid, file
   // offset of the word, the word read, landing half, span offset, batch pages | cta << 32,
   // then the landing half's last pull (file offset, bytes), pb_base, pb_off_adj, pb_count,
@@ -106,6 +109,8 @@ struct DevCtx {
   int32_t tma_off;           // byte offset of the stage ring in dynamic shared memory
   int32_t tma_nst;           // stages in the ring
   int32_t n_files, n_tb, n_ctas;
+  int32_t n_sms;      // SMs of the device: first TBs go one per SM (next_tb)
+  int32_t spread;     // 0 = plain ticket order (GFS_SPREAD=0, experiments)
   uint32_t ring_mask;
   uint64_t timeout_ns;
   // program (device)
@@ -153,6 +158,7 @@ struct DevCtx {
   uint32_t poll_first_ns, poll_ns;  // host-memory mailbox polling: first wait, then period
   int32_t k1_direct;         // pulled spans (mapped, small mapped_hybrid) are read by K1 straight
                              // from the pinned file mapping: no landing copy
+  int32_t k1_early;          // static spans K1 reads from the mapping start before the answer (checked later)
   int64_t ce_min;            // mapped_hybrid / pread_hybrid: spans of at least this size go by copy engine
   // fused consumer (gfs_run_consume)
   gfs_consumer cons;

@@ -21,7 +21,7 @@ RA_CLAMP = {"segment": 0, "eof": 1}
 TRANSFER = {"zerocopy": 0, "dma": 1, "bounce": 2, "mapped_dma": 3, "mapped": 4,
             "mapped_hybrid": 5, "pread_hybrid": 6}
 O_RDONLY, O_RDWR = 0, 2
-ABI_VERSION = 8  # include/gfs.h GFS_ABI_VERSION: the struct layouts below
+ABI_VERSION = 9  # include/gfs.h GFS_ABI_VERSION: the struct layouts below
 LOG_DELIVERIES, LOG_RPCS, LOG_VICTIMS, LOG_WINDOWS, LOG_TIMELINE = 0, 1, 2, 3, 4
 LOG_WIDTH = {LOG_DELIVERIES: 3, LOG_RPCS: 4, LOG_VICTIMS: 3, LOG_WINDOWS: 2, LOG_TIMELINE: 4}
 TL_RPC, TL_GREAD, TL_CONSUME = 0, 1, 2
@@ -48,7 +48,7 @@ class GfsConfig(C.Structure):
         ("raw_mode", C.c_int32), ("pcie_disabled", C.c_int32), ("log", C.c_int32),
         ("verify", C.c_int32), ("timeline", C.c_int32), ("k1_tma", C.c_int32),
         ("numa_pin", C.c_int32), ("lookahead", C.c_int32), ("ra_clamp", C.c_int32),
-        ("rpc_slots", C.c_int32), ("k1_direct", C.c_int32),
+        ("rpc_slots", C.c_int32), ("k1_direct", C.c_int32), ("k1_early", C.c_int32),
     ]
 
 

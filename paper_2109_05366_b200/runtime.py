@@ -66,6 +66,7 @@ def native_config(cfg: ExperimentConfig, max_request_bytes: int = 0) -> native.G
     c.ra_clamp = native.RA_CLAMP[cfg["io.ra_clamp"]]
     c.rpc_slots = cfg["rpc.n_slots"]
     c.k1_direct = int(bool(cfg["gpu.k1_direct"]))
+    c.k1_early = int(bool(cfg["gpu.k1_early"]))
     return c
 
 

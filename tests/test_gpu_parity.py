@@ -58,6 +58,22 @@ def test_golden_case_on_device(name, transfer, synth_dir):
     assert rep["user_bytes"] == g["counters"]["user_bytes"]
 
 
+@pytest.mark.parametrize("name", gu.case_names())
+@pytest.mark.parametrize("transfer", ["mapped", "mapped_hybrid"])
+def test_golden_case_k1_early_off(name, transfer, synth_dir):
+    """gpu.k1_early=false (K1 waits for the daemon's answer before reading the mapping) keeps
+    the same golden counters, traces and bytes as the default early read."""
+    g = gu.load(name)
+    sim, rep = run_sim(g["overrides"], g["seed"], synth_dir,
+                       **{"io.transfer": transfer, "gpu.k1_early": False})
+    st = sim.result.stats
+    errs = gu.compare(g, st, sim.result.deliveries, sim.result.rpcs, sim.result.victims)
+    assert not errs, f"{name}/{transfer}: " + "; ".join(errs)
+    assert st["word_mismatches"] == 0 and sim.mismatched_words == 0
+    want, _ = oracle_checksum(gu.config_of(g, seed=g["seed"]), g["seed"])
+    assert sim.checksum == want
+
+
 @pytest.mark.parametrize("policy", ["per-tb-lra", "global-lru-dealloc"])
 @pytest.mark.parametrize("readahead", ["static", "adaptive", "doubling"])
 def test_pressure_many_waves_vs_oracle(policy, readahead, synth_dir):

@@ -64,11 +64,48 @@ def _case_id(k: int) -> str:
     return f"{k}-{TRANSFERS[k % len(TRANSFERS)]}-{('tma', 'ldg')[(k // len(TRANSFERS)) % 2]}"
 
 
+def eof_case(k: int):
+    """EOF-heavy programs: every TB reads to the end of a file from a random point in its last
+    48 MiB, so TBs end on short EOF pages and release frames at the same time — under
+    global-lru-dealloc, where every release and recycled take goes through the one global
+    lock (take_recycled / release_frame), and a cache far smaller than the pages touched."""
+    r = SeededRng(9000 + k)
+    n_tb = 200 + r.below(300)
+    page = 4096
+    request = [4 * KiB, 10_000, 64 * KiB][r.below(3)]
+    progs = []
+    for _ in range(n_tb):
+        fid = r.below(len(FILE_BYTES))
+        fs = FILE_BYTES[fid]
+        ln = 1 + r.below(48 * MiB)
+        progs.append([(fid, fs - ln, ln)])
+    cfg = {
+        "gpufs.page_size": page,
+        "gpufs.prefetch_bytes": page * r.below(16),
+        "gpufs.cache_bytes": [64 * MiB, 128 * MiB][r.below(2)],
+        "gpufs.policy": "global-lru-dealloc" if k % 4 else "per-tb-lra",
+        "io.readahead": ["static", "adaptive", "doubling"][k % 3],
+        "io.ra_max_bytes": page << (4 + r.below(6)),
+        "io.transfer": TRANSFERS[k % len(TRANSFERS)],
+        "workload.request_bytes": request,
+        "mode.verify": True,
+    }
+    return cfg, progs, request
+
+
 @pytest.mark.parametrize("k", range(N_CASES), ids=_case_id)
 def test_random_multisegment_programs_full_residency(k):
+    _run_case(k, *random_case(k))
+
+
+@pytest.mark.parametrize("k", range(12), ids=lambda k: f"eof{k}-{TRANSFERS[k % len(TRANSFERS)]}")
+def test_eof_heavy_programs_full_residency(k):
+    _run_case(k, *eof_case(k))
+
+
+def _run_case(k, over, progs, request):
     import torch
     from paper_2109_05366_b200.runtime import GpuFS, ensure_synthetic
-    over, progs, request = random_case(k)
     d = "/dev/shm/gfs_stress"
     os.makedirs(d, exist_ok=True)
     paths = [ensure_synthetic(d, cid, fb) for cid, fb in enumerate(FILE_BYTES)]

@@ -50,7 +50,7 @@ def main():
             r = fs.run(table, req, dst)
             st = r.stats
             out = {"cell": cell, "arm": a.arm, "set": a.set, "gbps": round(size / st["kernel_ns"], 3),
-                   "transfer": fs.transfer, "ctas": st["ctas"], "rpc_count": st["rpc_count"],
+                   "transfer": fs.transfer, "ctas": st["ctas"], "rpc_count": st["rpc_count"], "early_answers": st.get("early_answers"),
                    "per_cta_ms": {k: round(st[k] / max(1, min(n_tb, st["ctas"])) / 1e6, 2)
                                   for k in ("wait_ns", "meta_ns", "copy_ns", "install_ns", "lookup_ns", "alloc_ns")},
                    "kernel_ms": round(st["kernel_ns"] / 1e6, 2)}
@@ -62,6 +62,21 @@ def main():
                         dur = (d["t1"][m] - d["t0"][m]) / 1e3
                         out[f"{name}_us_p50_p90"] = [round(float(np.percentile(dur, 50)), 1),
                                                     round(float(np.percentile(dur, 90)), 1)]
+                m = d["kind"] == 1
+                if m.any():  # per TB: first gread start .. last gread end, against the pass
+                    t0, t1, tb = d["t0"][m], d["t1"][m], d["tb"][m]
+                    g0 = int(t0.min())
+                    life = [(int(t0[tb == t].min()) - g0, int(t1[tb == t].max()) - g0) for t in np.unique(tb)]
+                    ends = np.array([b for _, b in life]) / 1e6
+                    starts = np.array([a for a, _ in life]) / 1e6
+                    out["tb_start_ms_max"] = round(float(starts.max()), 2)
+                    tbs = np.unique(tb)
+                    cta_of = {int(t): int(d["cta"][m][tb == t][0]) for t in tbs}
+                    late = np.argsort(ends)[-6:][::-1]
+                    out["latest_tbs"] = [(int(tbs[i]), cta_of[int(tbs[i])], round(float(ends[i]), 2)) for i in late]
+                    out["tb_end_ms_p10_p50_max"] = [round(float(np.percentile(ends, 10)), 2),
+                                                    round(float(np.percentile(ends, 50)), 2),
+                                                    round(float(ends.max()), 2)]
             print(json.dumps(out), flush=True)
 
 
