@@ -940,7 +940,8 @@ __device__ bool early_eligible(const DevCtx& c, int64_t n) {
 // answer already on chip; when the copy caught the mailbox before the answer (or anything
 // does not match) it falls back to polling.
 __device__ __forceinline__ void early_poll(const DevCtx& c, Smem& s) {
-  if (!s.early.on || s.early.polled) return;
+  // (mapped_hybrid answers through the HBM doorbell: nothing to fetch over the link)
+  if (!s.early.on || s.early.polled || c.transfer != GFS_XFER_MAPPED_ZC) return;
   s.early.polled = 1;
   const RpcResp* r = &c.resp[(int64_t)blockIdx.x * c.landing_halves + s.early.half];
   tma_load(&s.poll_buf, r, 16, &s.poll_bar);
