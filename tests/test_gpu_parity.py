@@ -140,6 +140,41 @@ def test_gread_api_offsets_and_eof(synth_dir):
         fs.gclose(fid)
 
 
+@pytest.mark.parametrize("early", [True, False])
+def test_k1_early_answers_fetched_during_k1(early, synth_dir):
+    """Static spans over the `mapped` transfer: with gpu.k1_early K1 reads each span before
+    the daemon's answer and fetches the answer's mailbox line by a bulk copy while the span
+    streams — nearly every answer is found that way (the rest fall back to polling); the
+    counters, bytes and RPC trace are the oracle's either way."""
+    from paper_2109_05366_b200.runtime import GpuFS, ensure_synthetic
+    import torch
+    size = 64 * MiB
+    path = ensure_synthetic(synth_dir, 0, size)
+    over = {"workload.n_tb": 64, "workload.file_bytes": size, "workload.request_bytes": 4 * KiB,
+            "gpufs.page_size": 4 * KiB, "gpufs.prefetch_bytes": 60 * KiB, "gpufs.cache_bytes": 16 * MiB,
+            "gpufs.policy": "per-tb-lra", "io.readahead": "static", "io.transfer": "mapped",
+            "gpu.k1_early": early, "io.dir": synth_dir, "mode.deterministic": True}
+    cfg = ExperimentConfig(over)
+    wl = build_workload(cfg)
+    table = ProgramTable.from_programs(wl.programs)
+    with GpuFS(cfg, max_request_bytes=4 * KiB) as fs:
+        fs.gopen(path, content_id=0)
+        dst = torch.empty(table.dst_bytes, dtype=torch.uint8, device="cuda")
+        r = fs.run(table, 4 * KiB, dst)
+        csum = fs.checksum(dst)
+    ref = orc.run_oracle(cfg, wl, source=orc.SRC_SYNTH, materialize_dst=True)
+    st = r.stats
+    for k in ("user_bytes", "greads", "rpc_count", "rpc_requested_bytes", "pb_hits", "pc_misses",
+              "pcie_bytes", "victims"):
+        assert st[k] == ref.stats[k], k
+    assert np.array_equal(gu.by_tb(r.rpcs), gu.by_tb(ref.rpcs))
+    assert st["word_mismatches"] == 0 and csum == ref.checksum
+    if early:
+        assert st["early_answers"] >= 0.5 * st["rpc_count"], (st["early_answers"], st["rpc_count"])
+    else:
+        assert st["early_answers"] == 0
+
+
 def test_consume_only_and_raw_mode(synth_dir):
     from paper_2109_05366_b200.runtime import GpuFS, ensure_synthetic
     import torch
